@@ -1,0 +1,168 @@
+/*
+ * sbd.h -- C ABI of the B200-native Selected Basis Diagonalization backend.
+ *
+ * The reference package (`sbdiag`, arxiv 2601.16637) has no C ABI: its
+ * drop-in boundary is the Python operator protocol consumed by
+ * `davidson_solve` (pkg/src/sbdiag/davidson.py:191-196,242):
+ *
+ *     apply_h(x: float64[N]) -> float64[N]   plus   diag: float64[N]
+ *
+ * implemented by `HamiltonianApplier` (apply.py:651-704) and
+ * `DistributedApplier` (distsim.py:130-316).  Every entry point below
+ * replaces one piece of that stack; the reference interface it stands in for
+ * is cited beside it.  The Python package `paper_2601_16637_b200` binds this
+ * header with ctypes and re-exposes the reference API.
+ *
+ * Conventions
+ *   - every call returns SBD_OK (0), SBD_EINVAL (1, -> ValueError) or
+ *     SBD_ECUDA (2, -> RuntimeError); sbd_last_error() describes the failure;
+ *   - pointers named *_host are host memory, *_dev device memory on the
+ *     context's GPU; all device work is ordered on the context's stream
+ *     (sbd_set_stream), and calls returning host data synchronise it;
+ *   - strings are uint64 occupation masks (bit p = orbital p, norb <= 64) in
+ *     CALLER order; determinant (ia, ib) has index ia*n_beta + ib
+ *     (basis.py:208-213);
+ *   - integrals use the reference layout: h[norb*norb] row-major,
+ *     eri[npair*(npair+1)/2] tri-of-tri (integrals.py:39-41,94-97).
+ */
+#ifndef SBD_B200_H
+#define SBD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBD_OK 0
+#define SBD_EINVAL 1
+#define SBD_ECUDA 2
+
+#define SBD_SPIN_ALPHA 0
+#define SBD_SPIN_BETA 1
+
+typedef struct sbd_ctx sbd_ctx;
+
+/* library / error plumbing */
+int sbd_abi_version(void);
+const char *sbd_last_error(const sbd_ctx *ctx); /* ctx may be NULL: thread-global last error */
+
+/* Context lifetime.  Replaces HamiltonianApplier.__init__ state ownership
+ * (apply.py:659-686): the context owns tables, diagonal and scratch. */
+int sbd_create(int device, sbd_ctx **out);
+int sbd_destroy(sbd_ctx *ctx);
+int sbd_set_stream(sbd_ctx *ctx, void *cuda_stream); /* NULL = legacy default stream */
+
+/* IntegralTable upload (integrals.py:44-103). */
+int sbd_set_integrals(sbd_ctx *ctx, int norb, const double *h_host, const double *eri_host,
+                      int64_t n_eri, double e_core);
+
+/* One spin sector's string list, caller order (SelectedBasis.product,
+ * basis.py:138-160).  Validates popcount == n_elec and bits < norb. */
+int sbd_set_strings(sbd_ctx *ctx, int spin, const uint64_t *strings_host, int64_t n, int n_elec);
+
+/* Configuration processing + excitation generation on the device:
+ * radix sort/unique of each sector's strings, CSR in-set singles/doubles
+ * with phases (build_excitation_table, basis.py:362-403; build_spin_tables,
+ * apply.py:557-563), per-entry Slater-Condon coefficients and the
+ * diagonal building blocks.  Duplicated strings -> SBD_EINVAL. */
+int sbd_build_tables(sbd_ctx *ctx);
+
+/* Table sizes and bit-exact export in the reference's column layout
+ * (ExcitationTable, basis.py:316-338); any pointer may be NULL to skip. */
+int sbd_table_counts(sbd_ctx *ctx, int spin, int64_t *n_strings, int64_t *n_singles, int64_t *n_doubles);
+int sbd_export_table(sbd_ctx *ctx, int spin,
+                     int64_t *s_off_host, int64_t *s_tgt_host, int16_t *s_hole_host,
+                     int16_t *s_part_host, int8_t *s_phase_host,
+                     int64_t *d_off_host, int64_t *d_tgt_host, int16_t *d_hole1_host,
+                     int16_t *d_hole2_host, int16_t *d_part1_host, int16_t *d_part2_host,
+                     int8_t *d_phase_host);
+/* Sorted strings and sort permutation (sorted[i] = strings[perm[i]]). */
+int sbd_export_sorted(sbd_ctx *ctx, int spin, uint64_t *sorted_host, int64_t *perm_host);
+
+/* Rows this context owns: alpha rows [alpha_lo, alpha_hi) x all beta
+ * (make_partition semantics, distsim.py:63-77).  Default: all rows. */
+int sbd_set_row_window(sbd_ctx *ctx, int64_t alpha_lo, int64_t alpha_hi);
+
+/* Hamiltonian diagonal of the owned rows (compute_diagonal, apply.py:573-586). */
+int sbd_diag(sbd_ctx *ctx, double *out_dev);
+
+/* sigma = H x for the owned rows (HamiltonianApplier.__call__, apply.py:688-695;
+ * _apply_product, apply.py:608-623).  x_full_dev holds ALL n_alpha*n_beta
+ * amplitudes, y_dev the owned rows.  Row-owned, no atomics on y. */
+int sbd_sigma(sbd_ctx *ctx, const double *x_full_dev, double *y_dev);
+
+/* Split form for multi-GPU overlap (the ring of distsim.py:200-259):
+ *   sbd_sigma_local  -- beta-beta part from the OWNED rows only (no remote data);
+ *   sbd_sigma_remote -- alpha-alpha + alpha-beta part once x_full is gathered,
+ *                       combined with the local part into y_dev. */
+int sbd_sigma_local(sbd_ctx *ctx, const double *x_own_dev);
+int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full_dev, double *y_dev);
+
+/* End-to-end form: host x (all rows) in, host y (owned rows) out; H2D and D2H
+ * happen inside the call on the context's stream (numpy protocol of
+ * davidson.py:242). */
+int sbd_sigma_host(sbd_ctx *ctx, const double *x_full_host, double *y_host);
+
+/* Mean in-set alpha connections per alpha string (c-bar)
+ * and the algorithmic sigma bytes 8*N_own*(3 + c-bar). */
+int sbd_sigma_model(sbd_ctx *ctx, double *cbar_alpha, double *bytes_per_sigma);
+
+/* ---- Davidson building blocks (davidson.py), all device-resident ---- */
+
+/* out[i] = <V_i, w> for i < k; V_i = V + i*ldv.  Partial per-rank sums
+ * (all-reduce them for multi-GPU).  out_dev has k doubles. */
+int sbd_vdots(sbd_ctx *ctx, const double *V_dev, int k, int64_t ldv, int64_t n,
+              const double *w_dev, double *out_dev);
+
+/* One pass, two right-hand sides: out[i] = <V_i, w>, out[k + i] = <V_i, u>
+ * (projected-matrix column davidson.py:248-249 and the Gram row of the
+ * newest basis vector used for ortho_history, davidson.py:260-263). */
+int sbd_vdots2(sbd_ctx *ctx, const double *V_dev, int k, int64_t ldv, int64_t n, const double *w_dev,
+               const double *u_dev, double *out_dev);
+
+/* Fused Ritz/residual/preconditioner (davidson.py:252-258,277-278,159-163):
+ * for j < m: r_j = sum_i Y[i,j] W_i - theta_j sum_i Y[i,j] V_i; t_j = precond(r_j)
+ * written to T + j*ldt.  Output (k + 1 + m doubles, device):
+ *   out[0:k] = <V_i, t_target>, out[k] = |t_target|^2, out[k+1+j] = |r_j|^2.
+ * Y is k x m row-major, theta m doubles, both on the device; m <= 8.
+ * sbd_residual_precond is the target = 0 form with rn2 == proj + k + 1. */
+int sbd_residual_precond(sbd_ctx *ctx, const double *V_dev, const double *W_dev, int k, int64_t ldv,
+                         int64_t n, const double *Y_dev, const double *theta_dev, int m,
+                         const double *diag_dev, double delta, double *T_dev, int64_t ldt,
+                         double *rn2_dev, double *proj_dev);
+int sbd_residual_precond_target(sbd_ctx *ctx, const double *V_dev, const double *W_dev, int k, int64_t ldv,
+                                int64_t n, const double *Y_dev, const double *theta_dev, int m, int target,
+                                const double *diag_dev, double delta, double *T_dev, int64_t ldt,
+                                double *out_dev);
+
+/* Block Gram-Schmidt step (CGS pass of orthogonalize, davidson.py:166-185):
+ * t <- t - sum_i c[i] V_i, then out2[i] = <V_i, t> (next pass) and
+ * out2[k] = |t|^2.  out2_dev has k+1 doubles.  The _nodots form only
+ * writes |t|^2 to out2_dev[0] (last pass). */
+int sbd_gs_update(sbd_ctx *ctx, const double *V_dev, int k, int64_t ldv, int64_t n,
+                  const double *c_dev, double *t_dev, double *out2_dev);
+int sbd_gs_update_nodots(sbd_ctx *ctx, const double *V_dev, int k, int64_t ldv, int64_t n,
+                         const double *c_dev, double *t_dev, double *out_norm2_dev);
+
+/* dst = src * (*scale_dev)  (normalisation, scale stays on the device). */
+int sbd_scale_copy(sbd_ctx *ctx, const double *src_dev, double *dst_dev, int64_t n, const double *scale_dev);
+
+/* Thick restart (davidson.py:280-289): V[:,0:keep] <- V[:,0:k] . Y[:, 0:keep]
+ * in place (Y k x keep row-major on the device). */
+int sbd_rotate(sbd_ctx *ctx, double *V_dev, int k, int64_t ldv, int64_t n, const double *Y_dev, int keep);
+
+/* Ritz vectors U_j = sum_i Y[i,j] V_i (davidson.py:256), j < m. */
+int sbd_combine(sbd_ctx *ctx, const double *V_dev, int k, int64_t ldv, int64_t n,
+                const double *Y_dev, int m, double *U_dev, int64_t ldu);
+
+/* Projected eigensolve on the device (jacobi_eigh, davidson.py:86-148):
+ * A k x k (row-major, symmetrised inside) -> ascending evals, evec columns
+ * (row-major k x k).  info_dev[0] = sweeps used (>= max_sweeps: failure). */
+int sbd_jacobi(sbd_ctx *ctx, const double *A_dev, int k, int lda, double *evals_dev,
+               double *evecs_dev, int max_sweeps, int *info_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,66 @@
+"""B200-native Selected Basis Diagonalization (drop-in for the `sbdiag` reference API).
+
+Host side: Python + PyTorch (device memory, streams, torch.distributed/NCCL).
+Compute: hand-written sm_100a CUDA kernels in ``libsbd_b200.so`` behind the
+C ABI of ``include/sbd.h``.  Public names follow the reference package
+(``pkg/src/sbdiag/__init__.py:17-39``).
+"""
+
+from __future__ import annotations
+
+from .apply import (
+    HamiltonianApplier,
+    SpinTables,
+    apply_H,
+    apply_H_full,
+    build_excitation_table,
+    build_spin_tables,
+    compute_diagonal,
+)
+from .basis import (
+    Determinant,
+    ExcitationTable,
+    IngestReport,
+    SampleFormatError,
+    SelectedBasis,
+    det_to_line,
+    enumerate_doubles,
+    enumerate_singles,
+    ingest_samples,
+    popcount,
+    single_phase,
+)
+from .davidson import DavidsonOptions, DavidsonResult, DavidsonStats, davidson_solve
+from .integrals import FcidumpError, IntegralTable, parse_fcidump, write_fcidump
+
+__all__ = [
+    "Determinant",
+    "IngestReport",
+    "SelectedBasis",
+    "ingest_samples",
+    "IntegralTable",
+    "parse_fcidump",
+    "HamiltonianApplier",
+    "apply_H",
+    "DavidsonOptions",
+    "DavidsonResult",
+    "davidson_solve",
+    # lower-level reference names
+    "SpinTables",
+    "build_spin_tables",
+    "build_excitation_table",
+    "compute_diagonal",
+    "apply_H_full",
+    "ExcitationTable",
+    "DavidsonStats",
+    "FcidumpError",
+    "write_fcidump",
+    "SampleFormatError",
+    "det_to_line",
+    "enumerate_singles",
+    "enumerate_doubles",
+    "single_phase",
+    "popcount",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,149 @@
+"""ctypes binding of ``include/sbd.h`` (libsbd_b200.so, built in-tree for sm_100a).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, every entry point raises.  Status codes map to the reference's
+exception types: SBD_EINVAL -> ValueError, SBD_ECUDA -> RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsbd_b200.so")
+
+_c_i64 = ctypes.c_int64
+_c_int = ctypes.c_int
+_c_dbl = ctypes.c_double
+_vp = ctypes.c_void_p
+
+# name -> argtypes (all return int status unless listed in _RESTYPE)
+_SIGS = {
+    "sbd_abi_version": [],
+    "sbd_last_error": [_vp],
+    "sbd_create": [_c_int, ctypes.POINTER(_vp)],
+    "sbd_destroy": [_vp],
+    "sbd_set_stream": [_vp, _vp],
+    "sbd_set_integrals": [_vp, _c_int, _vp, _vp, _c_i64, _c_dbl],
+    "sbd_set_strings": [_vp, _c_int, _vp, _c_i64, _c_int],
+    "sbd_build_tables": [_vp],
+    "sbd_table_counts": [_vp, _c_int, _vp, _vp, _vp],
+    "sbd_export_table": [_vp, _c_int] + [_vp] * 12,
+    "sbd_export_sorted": [_vp, _c_int, _vp, _vp],
+    "sbd_set_row_window": [_vp, _c_i64, _c_i64],
+    "sbd_diag": [_vp, _vp],
+    "sbd_sigma": [_vp, _vp, _vp],
+    "sbd_sigma_local": [_vp, _vp],
+    "sbd_sigma_remote": [_vp, _vp, _vp],
+    "sbd_sigma_host": [_vp, _vp, _vp],
+    "sbd_sigma_model": [_vp, _vp, _vp],
+    "sbd_vdots": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _vp],
+    "sbd_vdots2": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _vp, _vp],
+    "sbd_residual_precond": [_vp, _vp, _vp, _c_int, _c_i64, _c_i64, _vp, _vp, _c_int, _vp, _c_dbl, _vp,
+                             _c_i64, _vp, _vp],
+    "sbd_residual_precond_target": [_vp, _vp, _vp, _c_int, _c_i64, _c_i64, _vp, _vp, _c_int, _c_int, _vp,
+                                    _c_dbl, _vp, _c_i64, _vp],
+    "sbd_gs_update": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _vp, _vp],
+    "sbd_gs_update_nodots": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _vp, _vp],
+    "sbd_scale_copy": [_vp, _vp, _vp, _c_i64, _vp],
+    "sbd_rotate": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _c_int],
+    "sbd_combine": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _c_int, _vp, _c_i64],
+    "sbd_jacobi": [_vp, _vp, _c_int, _c_int, _vp, _vp, _c_int, _vp],
+}
+_RESTYPE = {"sbd_last_error": ctypes.c_char_p}
+
+EXPORTED = tuple(_SIGS)
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+class ExtensionMissing(ImportError):
+    pass
+
+
+def load() -> ctypes.CDLL:
+    """Load libsbd_b200.so (raises ExtensionMissing if it was never built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ExtensionMissing(
+                f"{LIB_PATH} not found: build the sm_100a extension first "
+                "(python -m paper_2601_16637_b200._build or __graft_entry__.build())")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPE.get(name, _c_int)
+        _lib = lib
+    return _lib
+
+
+def last_error(ctx=None) -> str:
+    msg = load().sbd_last_error(ctx)
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, ctx=None, what: str = "") -> None:
+    if rc == 0:
+        return
+    msg = last_error(ctx)
+    if rc == 1:
+        raise ValueError(msg or what)
+    raise RuntimeError(f"{what}: {msg}" if what else msg)
+
+
+def ptr(x) -> int:
+    """Raw address of a numpy array or torch tensor (no copies)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+def call(name: str, *args, ctx=None):
+    rc = getattr(load(), name)(*args)
+    check(rc, ctx, name)
+
+
+class Context:
+    """Owns one ``sbd_ctx`` on one CUDA device (HamiltonianApplier state)."""
+
+    def __init__(self, device: int = 0):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2601_16637_b200 needs a CUDA device (no CPU fallback)")
+        self.device = int(device)
+        h = _vp()
+        check(load().sbd_create(self.device, ctypes.byref(h)), None, "sbd_create")
+        self._h = h
+        self.bind_stream()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def bind_stream(self, stream=None) -> None:
+        import torch
+
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        self(("sbd_set_stream"), _vp(s.cuda_stream))
+
+    def __call__(self, name: str, *args):
+        rc = getattr(load(), name)(self._h, *args)
+        check(rc, self._h, name)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            load().sbd_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,342 @@
+// Excitation generation on the device + kernel-ready coefficients.
+//
+// Reference semantics (bit-exact target):
+//   enumerate_singles  basis.py:72-81   p occupied ascending, r virtual ascending
+//   enumerate_doubles  basis.py:84-103  combinations(occ,2) x combinations(virt,2),
+//                                       phase = sign(p->r on s) * sign(q->s on mid)
+//   build_excitation_table basis.py:362-403: keep in-set targets only, CSR per
+//                                       source string in caller order.
+//
+// Design: one warp per source string.  Lanes take consecutive candidates in
+// enumeration order (32 per step), build the target mask, and look it up by
+// binary search over the sorted sector (a shared-memory splitter level, then a
+// short search in the L1-resident sorted array).  A ballot + popc compaction
+// keeps enumeration order, so the count pass and the fill pass produce exactly
+// the reference's entry order; targets are mapped back to caller indices
+// through the sort permutation.
+#include "sbd_internal.cuh"
+
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kSplit = 4096;  // splitter keys kept in shared memory
+
+struct EnumSmem {
+    u64 spl[kSplit];
+    uint16_t hole_pairs[2016];  // (a | a2 << 8) for a < a2 < n_occ, lexicographic
+    uint16_t virt_pairs[2016];
+    uint8_t occ[kWarpsPerBlock][64];
+    uint8_t virt[kWarpsPerBlock][64];
+};
+
+__device__ __forceinline__ int sign_between(u64 w, int p, int r) {
+    int lo = min(p, r), hi = max(p, r);
+    u64 mask = ((1ull << hi) - 1) & ~((2ull << lo) - 1);
+    return (__popcll(w & mask) & 1) ? -1 : 1;
+}
+
+// sorted position of key or -1
+__device__ __forceinline__ int lookup(const EnumSmem &sm, int nspl, int stride, const u64 *__restrict__ sorted,
+                                      i64 n, u64 key) {
+    // largest j with spl[j] <= key
+    int lo = 0, hi = nspl;  // invariant answer in [lo-1, hi-1]
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (sm.spl[mid] <= key) lo = mid + 1;
+        else hi = mid;
+    }
+    int j = lo - 1;
+    if (j < 0) return -1;
+    if (stride == 1) return sm.spl[j] == key ? j : -1;
+    i64 a = (i64)j * stride, b = min(n, a + stride);
+    while (a < b) {
+        i64 mid = (a + b) >> 1;
+        if (__ldg(sorted + mid) < key) a = mid + 1;
+        else b = mid;
+    }
+    return (a < n && __ldg(sorted + a) == key) ? (int)a : -1;
+}
+
+template <bool FILL>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+enum_kernel(const u64 *__restrict__ str, const u64 *__restrict__ sorted, const int32_t *__restrict__ perm, i64 n,
+            int norb, int n_elec, int stride, int nspl,
+            int64_t *__restrict__ cnt_s, int64_t *__restrict__ cnt_d,            // count pass: [n]
+            const int64_t *__restrict__ s_off, const int64_t *__restrict__ d_off,  // fill pass
+            int32_t *__restrict__ s_tgt, int16_t *__restrict__ s_hole, int16_t *__restrict__ s_part,
+            int8_t *__restrict__ s_phase, int32_t *__restrict__ d_tgt, int16_t *__restrict__ d_h1,
+            int16_t *__restrict__ d_h2, int16_t *__restrict__ d_p1, int16_t *__restrict__ d_p2,
+            int8_t *__restrict__ d_phase) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    EnumSmem &sm = *reinterpret_cast<EnumSmem *>(smem_raw);
+    const int no = n_elec, nv = norb - n_elec;
+    const int nhp = no * (no - 1) / 2, nvp = nv * (nv - 1) / 2;
+    for (int j = threadIdx.x; j < nspl; j += blockDim.x) sm.spl[j] = sorted[(i64)j * stride];
+    for (int k = threadIdx.x; k < nhp; k += blockDim.x) {
+        int a = 0, rem = k;
+        while (rem >= no - a - 1) rem -= no - a - 1, ++a;
+        sm.hole_pairs[k] = (uint16_t)(a | ((a + 1 + rem) << 8));
+    }
+    for (int k = threadIdx.x; k < nvp; k += blockDim.x) {
+        int a = 0, rem = k;
+        while (rem >= nv - a - 1) rem -= nv - a - 1, ++a;
+        sm.virt_pairs[k] = (uint16_t)(a | ((a + 1 + rem) << 8));
+    }
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1;
+    uint8_t *occ = sm.occ[w], *virt = sm.virt[w];
+    for (i64 i = (i64)blockIdx.x * kWarpsPerBlock + w; i < n; i += (i64)gridDim.x * kWarpsPerBlock) {
+        const u64 s = str[i];
+        // occupied / virtual orbital lists in ascending order
+        for (int base = 0; base < norb; base += 32) {
+            int o = base + lane;
+            bool in = o < norb, occd = in && ((s >> o) & 1);
+            unsigned mo = __ballot_sync(0xffffffffu, occd), mv = __ballot_sync(0xffffffffu, in && !occd);
+            int before_o = __popcll(s & ((1ull << base) - 1));
+            int before_v = base - before_o;
+            if (occd) occ[before_o + __popc(mo & lt)] = (uint8_t)o;
+            if (in && !occd) virt[before_v + __popc(mv & lt)] = (uint8_t)o;
+        }
+        __syncwarp();
+        i64 ws = FILL ? s_off[i] : 0, wd = FILL ? d_off[i] : 0;
+        // singles: candidate c -> (occ[c / nv], virt[c % nv])
+        const int ts = no * nv;
+        for (int base = 0; base < ts; base += 32) {
+            int c = base + lane;
+            int pos = -1, p = 0, r = 0;
+            if (c < ts) {
+                p = occ[c / nv];
+                r = virt[c % nv];
+                pos = lookup(sm, nspl, stride, sorted, n, (s & ~(1ull << p)) | (1ull << r));
+            }
+            unsigned m = __ballot_sync(0xffffffffu, pos >= 0);
+            if (FILL && pos >= 0) {
+                i64 k = ws + __popc(m & lt);
+                s_tgt[k] = perm[pos];
+                s_hole[k] = (int16_t)p;
+                s_part[k] = (int16_t)r;
+                s_phase[k] = (int8_t)sign_between(s, p, r);
+            }
+            ws += __popc(m);
+        }
+        // doubles: candidate c -> hole pair c / nvp, particle pair c % nvp
+        const i64 td = (i64)nhp * nvp;
+        for (i64 base = 0; base < td; base += 32) {
+            i64 c = base + lane;
+            int pos = -1, p = 0, q = 0, r = 0, t = 0;
+            u64 mid = 0;
+            if (c < td) {
+                uint16_t hp = sm.hole_pairs[c / nvp], vp = sm.virt_pairs[c % nvp];
+                p = occ[hp & 0xFF];
+                q = occ[hp >> 8];
+                r = virt[vp & 0xFF];
+                t = virt[vp >> 8];
+                mid = (s & ~(1ull << p)) | (1ull << r);
+                pos = lookup(sm, nspl, stride, sorted, n, (mid & ~(1ull << q)) | (1ull << t));
+            }
+            unsigned m = __ballot_sync(0xffffffffu, pos >= 0);
+            if (FILL && pos >= 0) {
+                i64 k = wd + __popc(m & lt);
+                d_tgt[k] = perm[pos];
+                d_h1[k] = (int16_t)p;
+                d_h2[k] = (int16_t)q;
+                d_p1[k] = (int16_t)r;
+                d_p2[k] = (int16_t)t;
+                d_phase[k] = (int8_t)(sign_between(s, p, r) * sign_between(mid, q, t));
+            }
+            wd += __popc(m);
+        }
+        if (!FILL && lane == 0) {
+            cnt_s[i] = ws;
+            cnt_d[i] = wd;
+        }
+        __syncwarp();
+    }
+}
+
+// out[0] = 0, out[i+1] = sum_{j<=i} in[j]   (single block, n small)
+__global__ void offsets_from_counts(const int64_t *__restrict__ in, int64_t *__restrict__ out, i64 n) {
+    __shared__ int64_t part[1024];
+    int t = threadIdx.x, nt = blockDim.x;
+    i64 per = (n + nt - 1) / nt, lo = t * per, hi = min(n, lo + per);
+    int64_t s = 0;
+    for (i64 i = lo; i < hi; ++i) s += in[i];
+    part[t] = s;
+    __syncthreads();
+    if (t == 0) {
+        int64_t run = 0;
+        for (int i = 0; i < nt; ++i) {
+            int64_t v = part[i];
+            part[i] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    int64_t run = part[t];
+    if (t == 0) out[0] = 0;
+    for (i64 i = lo; i < hi; ++i) {
+        run += in[i];
+        out[i + 1] = run;
+    }
+}
+
+__device__ __forceinline__ double eri4(const double *__restrict__ eri, int p, int q, int r, int s) {
+    return __ldg(eri + tri_idx(tri_idx(p, q), tri_idx(r, s)));
+}
+
+// Per source string: pack singles (with F = h_pr + sum_common[(pr|qq)-(pq|qr)],
+// the spectator-free part of apply.py:115-134) and doubles (the full
+// spectator-free element of apply.py:137-149) into Conn records; singles also
+// into SConn records for the opposite-spin term; same-spin diagonal energy
+// (apply.py:84-97) in the reference's operation order.
+__global__ void coeff_kernel(const u64 *__restrict__ str, i64 n, int norb, const double *__restrict__ h,
+                             const double *__restrict__ eri, const int64_t *__restrict__ s_off,
+                             const int32_t *__restrict__ s_tgt, const int16_t *__restrict__ s_hole,
+                             const int16_t *__restrict__ s_part, const int8_t *__restrict__ s_phase,
+                             const int64_t *__restrict__ d_off, const int32_t *__restrict__ d_tgt,
+                             const int16_t *__restrict__ d_h1, const int16_t *__restrict__ d_h2,
+                             const int16_t *__restrict__ d_p1, const int16_t *__restrict__ d_p2,
+                             const int8_t *__restrict__ d_phase, int64_t *__restrict__ conn_off,
+                             Conn *__restrict__ conn, SConn *__restrict__ sconn, double *__restrict__ energy) {
+    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const u64 s = str[i];
+    i64 base = s_off[i] + d_off[i];
+    conn_off[i] = base;
+    if (i == n - 1) conn_off[n] = s_off[n] + d_off[n];
+    i64 o = base;
+    for (i64 k = s_off[i]; k < s_off[i + 1]; ++k, ++o) {
+        int p = s_hole[k], r = s_part[k], ph = s_phase[k];
+        double F = __ldg(h + p * norb + r);
+        for (u64 t = s & ~(1ull << p); t; t &= t - 1) {
+            int q = __ffsll((long long)t) - 1;
+            F = __dadd_rn(F, __dsub_rn(eri4(eri, p, r, q, q), eri4(eri, p, q, q, r)));
+        }
+        int P = (int)tri_idx(p, r);
+        Conn c;
+        c.tgt = s_tgt[k];
+        c.info = ph * (P + 1);
+        c.c = ph * F;
+        conn[o] = c;
+        SConn sc;
+        sc.tgt = s_tgt[k];
+        sc.info = ph * (P + 1);
+        sconn[k] = sc;
+    }
+    for (i64 k = d_off[i]; k < d_off[i + 1]; ++k, ++o) {
+        int p = d_h1[k], q = d_h2[k], r = d_p1[k], t = d_p2[k];
+        Conn c;
+        c.tgt = d_tgt[k];
+        c.info = 0;
+        c.c = d_phase[k] * __dsub_rn(eri4(eri, p, r, q, t), eri4(eri, p, t, q, r));
+        conn[o] = c;
+    }
+    double e = 0.0;
+    for (u64 t = s; t; t &= t - 1) {
+        int p = __ffsll((long long)t) - 1;
+        e = __dadd_rn(e, __ldg(h + p * norb + p));
+        for (u64 t2 = s; t2; t2 &= t2 - 1) {
+            int q = __ffsll((long long)t2) - 1;
+            e = __dadd_rn(e, __dmul_rn(0.5, __dsub_rn(eri4(eri, p, p, q, q), eri4(eri, p, q, q, p))));
+        }
+    }
+    energy[i] = e;
+}
+
+// J[P][i] = sum_{q in string i, ascending} (P|qq)  -- spectator part of a single
+__global__ void jtable_kernel(const u64 *__restrict__ str, i64 n, i64 npair, const double *__restrict__ eri,
+                              double *__restrict__ J) {
+    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    i64 P = blockIdx.y;
+    if (i >= n || P >= npair) return;
+    double acc = 0.0;
+    for (u64 t = str[i]; t; t &= t - 1) {
+        int q = __ffsll((long long)t) - 1;
+        acc = __dadd_rn(acc, __ldg(eri + tri_idx(P, tri_idx(q, q))));
+    }
+    J[P * n + i] = acc;
+}
+
+}  // namespace
+
+int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s) {
+    const i64 n = s.n;
+    cudaStream_t st = ctx->stream;
+    SBD_CUDA(ctx, s.s_off.ensure(sizeof(int64_t) * (n + 1)));
+    SBD_CUDA(ctx, s.d_off.ensure(sizeof(int64_t) * (n + 1)));
+    if (n == 0) {
+        SBD_CUDA(ctx, cudaMemsetAsync(s.s_off.p, 0, sizeof(int64_t), st));
+        SBD_CUDA(ctx, cudaMemsetAsync(s.d_off.p, 0, sizeof(int64_t), st));
+        s.ns = s.nd = 0;
+        return SBD_OK;
+    }
+    int stride = (int)((n + kSplit - 1) / kSplit);
+    int nspl = (int)((n + stride - 1) / stride);
+    DevBuf cs, cd;
+    SBD_CUDA(ctx, cs.ensure(sizeof(int64_t) * n));
+    SBD_CUDA(ctx, cd.ensure(sizeof(int64_t) * n));
+    size_t smem = sizeof(EnumSmem);
+    SBD_CUDA(ctx, cudaFuncSetAttribute(enum_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SBD_CUDA(ctx, cudaFuncSetAttribute(enum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    unsigned blocks = (unsigned)std::min<i64>((n + kWarpsPerBlock - 1) / kWarpsPerBlock, (i64)ctx->num_sms * 8);
+    enum_kernel<false><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
+        s.str.as<u64>(), s.sorted.as<u64>(), s.perm.as<int32_t>(), n, ctx->norb, s.n_elec, stride, nspl,
+        cs.as<int64_t>(), cd.as<int64_t>(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+        nullptr, nullptr, nullptr, nullptr);
+    SBD_LAUNCHED(ctx, "enum count");
+    offsets_from_counts<<<1, 1024, 0, st>>>(cs.as<int64_t>(), s.s_off.as<int64_t>(), n);
+    offsets_from_counts<<<1, 1024, 0, st>>>(cd.as<int64_t>(), s.d_off.as<int64_t>(), n);
+    SBD_LAUNCHED(ctx, "enum offsets");
+    int64_t tot[2];
+    SBD_CUDA(ctx, cudaMemcpyAsync(&tot[0], s.s_off.as<int64_t>() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SBD_CUDA(ctx, cudaMemcpyAsync(&tot[1], s.d_off.as<int64_t>() + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SBD_CUDA(ctx, cudaStreamSynchronize(st));
+    s.ns = tot[0];
+    s.nd = tot[1];
+    if (s.ns + s.nd >= (i64)INT32_MAX) return sbd_fail(ctx, SBD_EINVAL, "excitation table too large");
+    SBD_CUDA(ctx, s.s_tgt.ensure(sizeof(int32_t) * (s.ns + 1)));
+    SBD_CUDA(ctx, s.s_hole.ensure(sizeof(int16_t) * (s.ns + 1)));
+    SBD_CUDA(ctx, s.s_part.ensure(sizeof(int16_t) * (s.ns + 1)));
+    SBD_CUDA(ctx, s.s_phase.ensure(sizeof(int8_t) * (s.ns + 1)));
+    SBD_CUDA(ctx, s.d_tgt.ensure(sizeof(int32_t) * (s.nd + 1)));
+    SBD_CUDA(ctx, s.d_h1.ensure(sizeof(int16_t) * (s.nd + 1)));
+    SBD_CUDA(ctx, s.d_h2.ensure(sizeof(int16_t) * (s.nd + 1)));
+    SBD_CUDA(ctx, s.d_p1.ensure(sizeof(int16_t) * (s.nd + 1)));
+    SBD_CUDA(ctx, s.d_p2.ensure(sizeof(int16_t) * (s.nd + 1)));
+    SBD_CUDA(ctx, s.d_phase.ensure(sizeof(int8_t) * (s.nd + 1)));
+    enum_kernel<true><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
+        s.str.as<u64>(), s.sorted.as<u64>(), s.perm.as<int32_t>(), n, ctx->norb, s.n_elec, stride, nspl, nullptr,
+        nullptr, s.s_off.as<int64_t>(), s.d_off.as<int64_t>(), s.s_tgt.as<int32_t>(), s.s_hole.as<int16_t>(),
+        s.s_part.as<int16_t>(), s.s_phase.as<int8_t>(), s.d_tgt.as<int32_t>(), s.d_h1.as<int16_t>(),
+        s.d_h2.as<int16_t>(), s.d_p1.as<int16_t>(), s.d_p2.as<int16_t>(), s.d_phase.as<int8_t>());
+    SBD_LAUNCHED(ctx, "enum fill");
+    SBD_CUDA(ctx, cudaStreamSynchronize(st));
+    return SBD_OK;
+}
+
+int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other) {
+    (void)other;
+    const i64 n = s.n;
+    cudaStream_t st = ctx->stream;
+    SBD_CUDA(ctx, s.conn_off.ensure(sizeof(int64_t) * (n + 1)));
+    SBD_CUDA(ctx, s.conn.ensure(sizeof(Conn) * (s.ns + s.nd + 1)));
+    SBD_CUDA(ctx, s.sconn.ensure(sizeof(SConn) * (s.ns + 1)));
+    SBD_CUDA(ctx, s.energy.ensure(sizeof(double) * (n + 1)));
+    SBD_CUDA(ctx, s.J.ensure(sizeof(double) * (ctx->npair * n + 1)));
+    if (n == 0) {
+        SBD_CUDA(ctx, cudaMemsetAsync(s.conn_off.p, 0, sizeof(int64_t), st));
+        return SBD_OK;
+    }
+    coeff_kernel<<<grid_for(n, 128), 128, 0, st>>>(
+        s.str.as<u64>(), n, ctx->norb, ctx->h.as<double>(), ctx->eri.as<double>(), s.s_off.as<int64_t>(),
+        s.s_tgt.as<int32_t>(), s.s_hole.as<int16_t>(), s.s_part.as<int16_t>(), s.s_phase.as<int8_t>(),
+        s.d_off.as<int64_t>(), s.d_tgt.as<int32_t>(), s.d_h1.as<int16_t>(), s.d_h2.as<int16_t>(),
+        s.d_p1.as<int16_t>(), s.d_p2.as<int16_t>(), s.d_phase.as<int8_t>(), s.conn_off.as<int64_t>(),
+        s.conn.as<Conn>(), s.sconn.as<SConn>(), s.energy.as<double>());
+    SBD_LAUNCHED(ctx, "coefficients");
+    dim3 g(grid_for(n, 128), (unsigned)ctx->npair);
+    jtable_kernel<<<g, 128, 0, st>>>(s.str.as<u64>(), n, ctx->npair, ctx->eri.as<double>(), s.J.as<double>());
+    SBD_LAUNCHED(ctx, "jtable");
+    return SBD_OK;
+}

@@ -1,0 +1,120 @@
+// Internal declarations shared by the sbd_*.cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sbd.h"
+
+typedef uint64_t u64;
+typedef int64_t i64;
+
+// One kernel-ready connection of a source string (same-spin excitation).
+//   info == 0      : double; coefficient c (spectator independent)
+//   info == +-(P+1): single with orbital pair P = tri(p, r) and phase sign(info);
+//                    c = phase * F, full coefficient c + phase * J[P][spectator]
+struct __align__(16) Conn {
+    int32_t tgt;
+    int32_t info;
+    double c;
+};
+
+// A bare single (for the opposite-spin alpha-single x beta-single term):
+// info = phase * (P + 1).
+struct __align__(8) SConn {
+    int32_t tgt;
+    int32_t info;
+};
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    ~DevBuf() { release(); }
+    void release();
+    cudaError_t ensure(size_t nbytes);  // grow-only
+    template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+struct Sector {
+    i64 n = 0;
+    int n_elec = 0;
+    bool present = false;
+    std::vector<u64> host;  // caller order
+    DevBuf str;             // u64[n] caller order
+    DevBuf sorted, perm;    // u64[n], int32[n]
+    // reference-layout CSR (device)
+    i64 ns = 0, nd = 0;
+    DevBuf s_off, s_tgt, s_hole, s_part, s_phase;
+    DevBuf d_off, d_tgt, d_h1, d_h2, d_p1, d_p2, d_phase;
+    // kernel-ready
+    DevBuf conn_off, conn;   // i64[n+1], Conn[ns+nd]
+    DevBuf sconn;            // SConn[ns] (offsets = s_off)
+    DevBuf energy;           // f64[n]: same-spin diagonal energy per string
+    DevBuf J;                // f64[npair][n]: J[P][i] = sum_{q in string i} (P|qq)
+    bool built = false;
+};
+
+struct sbd_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int norb = 0;
+    i64 npair = 0, n_eri = 0;
+    double e_core = 0.0;
+    bool have_integrals = false;
+    DevBuf h, eri, dpq;  // h[norb*norb], eri, dpq[norb*norb] = (pp|qq)
+    Sector sec[2];
+    i64 row_lo = 0, row_hi = -1;  // owned alpha rows (row_hi < 0: all)
+    // scratch for sigma
+    DevBuf xt, yt;               // [n_beta][ld_t]
+    i64 ld_t = 0;
+    DevBuf diag;                 // owned rows, cached
+    bool diag_valid = false;
+    DevBuf red;                  // reduction scratch
+    DevBuf hx, hy;               // device staging for sbd_sigma_host
+    int num_sms = 148;
+
+    i64 own_lo() const { return row_lo; }
+    i64 own_hi() const { return row_hi < 0 ? sec[0].n : row_hi; }
+    i64 own_rows() const { return own_hi() - own_lo(); }
+};
+
+// error helpers (sbd_context.cu)
+int sbd_fail(sbd_ctx *ctx, int code, const std::string &msg);
+int sbd_cuda_fail(sbd_ctx *ctx, cudaError_t e, const char *where);
+
+#define SBD_CHECK_CTX(ctx)                                                   \
+    do {                                                                     \
+        if (!(ctx)) return sbd_fail(nullptr, SBD_EINVAL, "null context");    \
+        cudaError_t _e = cudaSetDevice((ctx)->device);                       \
+        if (_e != cudaSuccess) return sbd_cuda_fail((ctx), _e, "cudaSetDevice"); \
+    } while (0)
+
+#define SBD_CUDA(ctx, call)                                                  \
+    do {                                                                     \
+        cudaError_t _e = (call);                                             \
+        if (_e != cudaSuccess) return sbd_cuda_fail((ctx), _e, #call);       \
+    } while (0)
+
+#define SBD_LAUNCHED(ctx, name)                                              \
+    do {                                                                     \
+        cudaError_t _e = cudaGetLastError();                                 \
+        if (_e != cudaSuccess) return sbd_cuda_fail((ctx), _e, name);        \
+    } while (0)
+
+// cross-TU entry points
+int sbd_sort_strings(sbd_ctx *ctx, Sector &s);              // sbd_strings.cu
+int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s);       // sbd_excite.cu
+int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other);  // sbd_excite.cu
+
+__host__ __device__ inline i64 tri_idx(i64 a, i64 b) {
+    return a >= b ? a * (a + 1) / 2 + b : b * (b + 1) / 2 + a;
+}
+
+inline unsigned grid_for(i64 n, int block) {
+    i64 g = (n + block - 1) / block;
+    return (unsigned)(g < 1 ? 1 : g);
+}

@@ -1,0 +1,411 @@
+// The Davidson sigma build y = H x over the alpha x beta determinant tensor.
+//
+// Reference: _product_row (apply.py:183-245) evaluates, for each bra row
+// (ia, ib), the diagonal, task 1 (beta singles/doubles, alpha fixed), task 2
+// (alpha singles/doubles, beta fixed) and task 0 (alpha single x beta single),
+// recomputing every Slater-Condon element from determinant words
+// (_hij_words, apply.py:152-177).
+//
+// B200 formulation.  With X the (n_alpha x n_beta) amplitude matrix:
+//
+//   sigma = diag o X + A X + (B X^T)^T + cross
+//
+// where A (B) is the alpha (beta) same-spin connection matrix.  A double's
+// element is spectator independent (one f64 per CSR entry); a single's is
+// phase*(F + J[P][spectator]) with F per entry and J per (orbital pair,
+// spectator string) precomputed once (sbd_excite.cu).  Both same-spin parts
+// become "row streams": output row r accumulates c_e * X[tgt_e, :] over its
+// CSR entries -- 128-bit coalesced loads of whole X rows, no gathers, no
+// atomics, every output element owned by one lane.  The beta part runs on
+// X^T (one tiled transpose) so it has the same shape; its result Y^T is
+// folded into the alpha kernel's epilogue through a shared-memory transpose.
+// Grid order keeps all SMs on one column tile of X at a time, so the ~c-bar
+// re-reads of each X row segment are served from L2.
+#include <algorithm>
+
+#include "sbd_internal.cuh"
+
+namespace {
+
+constexpr int kRowsPerCta = 8;   // one warp per output row
+constexpr int kColsPerWarp = 128;  // 4 columns per lane
+
+struct SideArgs {
+    i64 n_rows, row_base;          // output rows (local) and global row of local row 0
+    i64 n_cols, col_base;          // output columns; J column offset
+    const double *X;               // input rows indexed by connection target
+    i64 ldx;
+    double *Y;
+    i64 ldy;
+    const int64_t *conn_off;       // indexed by global row
+    const Conn *conn;
+    const double *J;               // J[P * ldj + col_base + col] of the spectator sector
+    i64 ldj;
+    // alpha side only
+    const double *diag;            // [n_rows][ldy]
+    const double *YT;              // beta-side result, [n_cols][ldyt]
+    i64 ldyt;
+    const int64_t *s_off_self;     // alpha singles of the row (global row index)
+    const SConn *sconn_self;
+    const int64_t *s_off_other;    // beta singles of the column
+    const SConn *sconn_other;
+    const double *eri;
+};
+
+template <bool VEC>
+__device__ __forceinline__ i64 lane_col(i64 c0, int lane, int j) {
+    return VEC ? c0 + (j >> 1) * 64 + 2 * lane + (j & 1) : c0 + j * 32 + lane;
+}
+
+template <bool VEC>
+__device__ __forceinline__ void load4(const double *__restrict__ row, i64 c0, int lane, const bool (&ok)[4],
+                                      double (&v)[4]) {
+    if (VEC) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (ok[2 * h]) {
+                double2 t = __ldg(reinterpret_cast<const double2 *>(row + c0 + h * 64 + 2 * lane));
+                v[2 * h] = t.x;
+                v[2 * h + 1] = t.y;
+            } else {
+                v[2 * h] = v[2 * h + 1] = 0.0;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = ok[j] ? __ldg(row + c0 + j * 32 + lane) : 0.0;
+    }
+}
+
+template <bool VEC, bool ALPHA>
+__global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const i64 r = (i64)blockIdx.x * kRowsPerCta + w;
+    const i64 c0 = (i64)blockIdx.y * kColsPerWarp;
+    const bool row_ok = r < a.n_rows;
+    bool ok[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ok[j] = lane_col<VEC>(c0, lane, j) < a.n_cols;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+
+    if (row_ok) {
+        const i64 g = a.row_base + r;
+        const i64 e0 = a.conn_off[g], e1 = a.conn_off[g + 1];
+        i64 e = e0;
+        // batches of 4 connections: 8 independent 128-bit loads in flight per lane
+        for (; e + 4 <= e1; e += 4) {
+            Conn cn[4];
+            double xv[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) cn[u] = a.conn[e + u];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) load4<VEC>(a.X + (i64)cn[u].tgt * a.ldx, c0, lane, ok, xv[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (cn[u].info == 0) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[j] = fma(cn[u].c, xv[u][j], acc[j]);
+                } else {
+                    const int P = abs(cn[u].info) - 1;
+                    const double sg = cn[u].info > 0 ? 1.0 : -1.0;
+                    const double *jr = a.J + (i64)P * a.ldj + a.col_base;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        double jv = ok[j] ? __ldg(jr + lane_col<VEC>(c0, lane, j)) : 0.0;
+                        acc[j] = fma(fma(sg, jv, cn[u].c), xv[u][j], acc[j]);
+                    }
+                }
+            }
+        }
+        for (; e < e1; ++e) {
+            Conn cn = a.conn[e];
+            double xv[4];
+            load4<VEC>(a.X + (i64)cn.tgt * a.ldx, c0, lane, ok, xv);
+            if (cn.info == 0) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[j] = fma(cn.c, xv[j], acc[j]);
+            } else {
+                const int P = abs(cn.info) - 1;
+                const double sg = cn.info > 0 ? 1.0 : -1.0;
+                const double *jr = a.J + (i64)P * a.ldj + a.col_base;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    double jv = ok[j] ? __ldg(jr + lane_col<VEC>(c0, lane, j)) : 0.0;
+                    acc[j] = fma(fma(sg, jv, cn.c), xv[j], acc[j]);
+                }
+            }
+        }
+        if (ALPHA) {
+            // diagonal term (apply.py:217)
+            double dv[4], xo[4];
+            load4<VEC>(a.diag + r * a.ldy, c0, lane, ok, dv);
+            load4<VEC>(a.X + g * a.ldx, c0, lane, ok, xo);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] = fma(dv[j], xo[j], acc[j]);
+            // task 0: alpha single x beta single (apply.py:235-238):
+            //   s_a s_b (pa ra | pb rb) X[ja, jb]
+            const i64 k0 = a.s_off_self[g], k1 = a.s_off_self[g + 1];
+            for (i64 k = k0; k < k1; ++k) {
+                const SConn sa = a.sconn_self[k];
+                const int Pa = abs(sa.info) - 1;
+                const double sga = sa.info > 0 ? 1.0 : -1.0;
+                const double *xr = a.X + (i64)sa.tgt * a.ldx;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (!ok[j]) continue;
+                    const i64 ib = lane_col<VEC>(c0, lane, j);
+                    const i64 m0 = a.s_off_other[ib], m1 = a.s_off_other[ib + 1];
+                    double t = 0.0;
+                    for (i64 m = m0; m < m1; ++m) {
+                        const SConn sb = a.sconn_other[m];
+                        const int Pb = abs(sb.info) - 1;
+                        const double v = __ldg(a.eri + tri_idx(Pa, Pb));
+                        t = fma(sb.info > 0 ? v : -v, __ldg(xr + sb.tgt), t);
+                    }
+                    acc[j] = fma(sga, t, acc[j]);
+                }
+            }
+        }
+    }
+
+    if (ALPHA) {
+        // + (B X^T)^T : tile YT[c0:c0+128, r0:r0+8] through shared memory
+        __shared__ double tile[kColsPerWarp][kRowsPerCta + 1];
+        const i64 r0 = (i64)blockIdx.x * kRowsPerCta;
+        {
+            const int i = threadIdx.x >> 1, half = (threadIdx.x & 1) * 4;
+            if (c0 + i < a.n_cols) {
+                const double2 *src = reinterpret_cast<const double2 *>(a.YT + (c0 + i) * a.ldyt + r0 + half);
+                double2 u = src[0], v = src[1];
+                tile[i][half + 0] = u.x;
+                tile[i][half + 1] = u.y;
+                tile[i][half + 2] = v.x;
+                tile[i][half + 3] = v.y;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const i64 lc = lane_col<VEC>(c0, lane, j) - c0;
+            if (row_ok && ok[j]) acc[j] += tile[lc][w];
+        }
+    }
+
+    if (row_ok) {
+        double *yr = a.Y + r * a.ldy;
+        if (VEC) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const i64 c = c0 + h * 64 + 2 * lane;
+                if (ok[2 * h] && ok[2 * h + 1]) {
+                    __stcs(reinterpret_cast<double2 *>(yr + c), make_double2(acc[2 * h], acc[2 * h + 1]));
+                } else if (ok[2 * h]) {
+                    yr[c] = acc[2 * h];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (ok[j]) yr[c0 + j * 32 + lane] = acc[j];
+        }
+    }
+}
+
+// X_own [rows][ld_in] -> XT [cols][ld_out]
+__global__ void transpose_kernel(const double *__restrict__ in, i64 rows, i64 cols, i64 ld_in, double *__restrict__ out,
+                                 i64 ld_out) {
+    __shared__ double t[32][33];
+    const i64 bc = (i64)blockIdx.x * 32, br = (i64)blockIdx.y * 32;
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        i64 rr = br + k, cc = bc + threadIdx.x;
+        t[k][threadIdx.x] = (rr < rows && cc < cols) ? __ldcs(in + rr * ld_in + cc) : 0.0;
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        i64 cc = bc + k, rr = br + threadIdx.x;
+        if (cc < cols && rr < rows) out[cc * ld_out + rr] = t[threadIdx.x][k];
+    }
+}
+
+// Diagonal, reference operation order (apply.py:100-112):
+//   e = (e_core + E_a) + E_b; for p in alpha: for q in beta: e += (pp|qq)
+__global__ void diag_kernel(i64 n_rows, i64 row_base, i64 nb, const u64 *__restrict__ astr,
+                            const u64 *__restrict__ bstr, const double *__restrict__ ea,
+                            const double *__restrict__ eb, const double *__restrict__ dpq, int norb, double e_core,
+                            double *__restrict__ out) {
+    extern __shared__ double sd[];
+    for (int i = threadIdx.x; i < norb * norb; i += blockDim.x) sd[i] = dpq[i];
+    __syncthreads();
+    const i64 total = n_rows * nb;
+    for (i64 idx = (i64)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (i64)gridDim.x * blockDim.x) {
+        const i64 r = idx / nb, ib = idx - r * nb;
+        const i64 g = row_base + r;
+        const u64 aw = astr[g], bw = bstr[ib];
+        double e = __dadd_rn(__dadd_rn(e_core, ea[g]), eb[ib]);
+        for (u64 ta = aw; ta; ta &= ta - 1) {
+            const int p = __ffsll((long long)ta) - 1;
+            for (u64 tb = bw; tb; tb &= tb - 1) e = __dadd_rn(e, sd[p * norb + __ffsll((long long)tb) - 1]);
+        }
+        out[idx] = e;
+    }
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int require_ready(sbd_ctx *ctx) {
+    if (!ctx->sec[0].built || !ctx->sec[1].built)
+        return sbd_fail(ctx, SBD_EINVAL, "tables not built (call sbd_build_tables)");
+    return SBD_OK;
+}
+
+int ensure_diag(sbd_ctx *ctx) {
+    if (ctx->diag_valid) return SBD_OK;
+    const i64 rows = ctx->own_rows(), nb = ctx->sec[1].n;
+    SBD_CUDA(ctx, ctx->diag.ensure(sizeof(double) * (rows * nb + 2)));
+    if (rows * nb > 0) {
+        size_t smem = sizeof(double) * ctx->norb * ctx->norb;
+        unsigned blocks = (unsigned)std::min<i64>(grid_for(rows * nb, 256), (i64)ctx->num_sms * 16);
+        diag_kernel<<<blocks, 256, smem, ctx->stream>>>(rows, ctx->own_lo(), nb, ctx->sec[0].str.as<u64>(),
+                                                        ctx->sec[1].str.as<u64>(), ctx->sec[0].energy.as<double>(),
+                                                        ctx->sec[1].energy.as<double>(), ctx->dpq.as<double>(),
+                                                        ctx->norb, ctx->e_core, ctx->diag.as<double>());
+        SBD_LAUNCHED(ctx, "diag_kernel");
+    }
+    ctx->diag_valid = true;
+    return SBD_OK;
+}
+
+int ensure_scratch(sbd_ctx *ctx) {
+    const i64 rows = ctx->own_rows(), nb = ctx->sec[1].n;
+    ctx->ld_t = std::max<i64>(kColsPerWarp, (rows + kColsPerWarp - 1) / kColsPerWarp * kColsPerWarp);
+    size_t bytes = sizeof(double) * (size_t)std::max<i64>(nb, 1) * ctx->ld_t;
+    SBD_CUDA(ctx, ctx->xt.ensure(bytes));
+    SBD_CUDA(ctx, ctx->yt.ensure(bytes));
+    return SBD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sbd_diag(sbd_ctx *ctx, double *out_dev) {
+    SBD_CHECK_CTX(ctx);
+    int rc = require_ready(ctx);
+    if (rc) return rc;
+    rc = ensure_diag(ctx);
+    if (rc) return rc;
+    const i64 n = ctx->own_rows() * ctx->sec[1].n;
+    if (out_dev && n)
+        SBD_CUDA(ctx, cudaMemcpyAsync(out_dev, ctx->diag.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    return SBD_OK;
+}
+
+int sbd_sigma_local(sbd_ctx *ctx, const double *x_own) {
+    SBD_CHECK_CTX(ctx);
+    int rc = require_ready(ctx);
+    if (rc) return rc;
+    rc = ensure_scratch(ctx);
+    if (rc) return rc;
+    const Sector &A = ctx->sec[0], &B = ctx->sec[1];
+    const i64 rows = ctx->own_rows(), nb = B.n;
+    if (rows == 0 || nb == 0) return SBD_OK;
+    cudaStream_t st = ctx->stream;
+    dim3 tg((unsigned)((nb + 31) / 32), (unsigned)((rows + 31) / 32));
+    transpose_kernel<<<tg, dim3(32, 8), 0, st>>>(x_own, rows, nb, nb, ctx->xt.as<double>(), ctx->ld_t);
+    SBD_LAUNCHED(ctx, "transpose_kernel");
+    SideArgs a{};
+    a.n_rows = nb;
+    a.row_base = 0;
+    a.n_cols = rows;
+    a.col_base = ctx->own_lo();
+    a.X = ctx->xt.as<double>();
+    a.ldx = ctx->ld_t;
+    a.Y = ctx->yt.as<double>();
+    a.ldy = ctx->ld_t;
+    a.conn_off = B.conn_off.as<int64_t>();
+    a.conn = B.conn.as<Conn>();
+    a.J = A.J.as<double>();
+    a.ldj = A.n;
+    dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((rows + kColsPerWarp - 1) / kColsPerWarp));
+    side_kernel<true, false><<<g, kRowsPerCta * 32, 0, st>>>(a);
+    SBD_LAUNCHED(ctx, "side_kernel<beta>");
+    return SBD_OK;
+}
+
+int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full, double *y) {
+    SBD_CHECK_CTX(ctx);
+    int rc = require_ready(ctx);
+    if (rc) return rc;
+    rc = ensure_diag(ctx);
+    if (rc) return rc;
+    const Sector &A = ctx->sec[0], &B = ctx->sec[1];
+    const i64 rows = ctx->own_rows(), nb = B.n;
+    if (rows == 0 || nb == 0) return SBD_OK;
+    SideArgs a{};
+    a.n_rows = rows;
+    a.row_base = ctx->own_lo();
+    a.n_cols = nb;
+    a.col_base = 0;
+    a.X = x_full;
+    a.ldx = nb;
+    a.Y = y;
+    a.ldy = nb;
+    a.conn_off = A.conn_off.as<int64_t>();
+    a.conn = A.conn.as<Conn>();
+    a.J = B.J.as<double>();
+    a.ldj = nb;
+    a.diag = ctx->diag.as<double>();
+    a.YT = ctx->yt.as<double>();
+    a.ldyt = ctx->ld_t;
+    a.s_off_self = A.s_off.as<int64_t>();
+    a.sconn_self = A.sconn.as<SConn>();
+    a.s_off_other = B.s_off.as<int64_t>();
+    a.sconn_other = B.sconn.as<SConn>();
+    a.eri = ctx->eri.as<double>();
+    dim3 g((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kColsPerWarp - 1) / kColsPerWarp));
+    const bool vec = (nb % 2 == 0) && aligned16(x_full) && aligned16(y);
+    if (vec) side_kernel<true, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
+    else side_kernel<false, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
+    SBD_LAUNCHED(ctx, "side_kernel<alpha>");
+    return SBD_OK;
+}
+
+int sbd_sigma(sbd_ctx *ctx, const double *x_full, double *y) {
+    SBD_CHECK_CTX(ctx);
+    int rc = require_ready(ctx);
+    if (rc) return rc;
+    if (!x_full || !y) return sbd_fail(ctx, SBD_EINVAL, "null vector");
+    rc = sbd_sigma_local(ctx, x_full + ctx->own_lo() * ctx->sec[1].n);
+    if (rc) return rc;
+    return sbd_sigma_remote(ctx, x_full, y);
+}
+
+int sbd_sigma_host(sbd_ctx *ctx, const double *x_host, double *y_host) {
+    SBD_CHECK_CTX(ctx);
+    int rc = require_ready(ctx);
+    if (rc) return rc;
+    const i64 nfull = ctx->sec[0].n * ctx->sec[1].n, nown = ctx->own_rows() * ctx->sec[1].n;
+    SBD_CUDA(ctx, ctx->hx.ensure(sizeof(double) * (nfull + 2)));
+    SBD_CUDA(ctx, ctx->hy.ensure(sizeof(double) * (nown + 2)));
+    if (nfull)
+        SBD_CUDA(ctx, cudaMemcpyAsync(ctx->hx.p, x_host, sizeof(double) * nfull, cudaMemcpyHostToDevice, ctx->stream));
+    rc = sbd_sigma(ctx, ctx->hx.as<double>(), ctx->hy.as<double>());
+    if (rc) return rc;
+    if (nown)
+        SBD_CUDA(ctx, cudaMemcpyAsync(y_host, ctx->hy.p, sizeof(double) * nown, cudaMemcpyDeviceToHost, ctx->stream));
+    SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SBD_OK;
+}
+
+int sbd_sigma_model(sbd_ctx *ctx, double *cbar, double *bytes) {
+    SBD_CHECK_CTX(ctx);
+    int rc = require_ready(ctx);
+    if (rc) return rc;
+    const Sector &A = ctx->sec[0];
+    double cb = A.n ? (double)(A.ns + A.nd) / (double)A.n : 0.0;
+    if (cbar) *cbar = cb;
+    if (bytes) *bytes = 8.0 * (double)ctx->own_rows() * (double)ctx->sec[1].n * (3.0 + cb);
+    return SBD_OK;
+}
+
+}  // extern "C"

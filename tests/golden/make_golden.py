@@ -1,0 +1,193 @@
+"""Generate golden fixtures by running the REFERENCE (sbdiag) in this container.
+
+    PYTHONPATH=/root/reference/pkg/src:/root/reference/pkg/tests \
+    NUMBA_CACHE_DIR=/tmp/nc python tests/golden/make_golden.py small cfg1 cfg2 [cfg1-davidson] [cfg4]
+
+The reference is not present on the GPU box, so its outputs are committed as
+small fixtures here: full arrays for the small instances, and for cfg1/cfg2/
+cfg4 SHA-256 digests of every excitation-table column plus sigma/diagonal
+values on windows of alpha rows (the reference's own windowed apply,
+``apply.py:501-546,608-623``, as used by ``test_apply.py:238-255``).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+from sbdiag import synth  # noqa: E402
+from sbdiag.apply import (  # noqa: E402
+    HamiltonianApplier,
+    _apply_product,
+    build_det_cache,
+    build_spin_tables,
+    compute_diagonal,
+)
+from sbdiag.basis import build_excitation_table, enumerate_doubles, enumerate_singles  # noqa: E402
+from sbdiag.davidson import DavidsonOptions, davidson_solve  # noqa: E402
+
+FIELDS = ("s_off", "s_tgt", "s_hole", "s_part", "s_phase",
+          "d_off", "d_tgt", "d_hole1", "d_hole2", "d_part1", "d_part2", "d_phase")
+DTYPES = dict(s_off=np.int64, s_tgt=np.int64, s_hole=np.int16, s_part=np.int16, s_phase=np.int8,
+              d_off=np.int64, d_tgt=np.int64, d_hole1=np.int16, d_hole2=np.int16,
+              d_part1=np.int16, d_part2=np.int16, d_phase=np.int8)
+
+
+def digest(arr, dtype) -> str:
+    return hashlib.sha256(np.ascontiguousarray(np.asarray(arr, dtype=dtype)).tobytes()).hexdigest()
+
+
+def table_digests(tab) -> dict:
+    return {f: digest(getattr(tab, f), DTYPES[f]) for f in FIELDS}
+
+
+def strings_digest(strings) -> str:
+    return digest(np.asarray(strings, dtype=np.uint64), np.uint64)
+
+
+def _hubbard():
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from conftest import hubbard_dimer_basis, hubbard_dimer_table
+    return hubbard_dimer_basis(), hubbard_dimer_table()
+
+
+SMALL_CASES = [
+    # name, norb, na, nb, n_alpha_strings (None = full), n_beta_strings, integral seed, basis seed
+    ("full_4_2_2_s0", 4, 2, 2, None, None, 0, None),
+    ("full_4_2_2_s3", 4, 2, 2, None, None, 3, None),
+    ("full_5_2_3_s5", 5, 2, 3, None, None, 5, None),
+    ("partial_5_2_3", 5, 2, 3, 6, 7, 9, 1),
+    ("partial_6_3_3", 6, 3, 3, 8, 8, 21, 5),
+    ("partial_8_4_3", 8, 4, 3, 30, 25, 7, 11),
+    ("full_6_3_2_s2", 6, 3, 2, None, None, 2, None),
+    ("single_det_3", 3, 2, 2, 1, 1, 42, 0),
+    ("partial_10_5_5", 10, 5, 5, 60, 50, 13, 17),
+]
+
+
+def make_small():
+    out = {}
+    meta = {}
+    for name, norb, na, nb, nsa, nsb, iseed, bseed in SMALL_CASES:
+        table = synth.random_integrals(norb, seed=iseed)
+        if nsa is None:
+            basis = synth.full_product_basis(norb, na, nb)
+        else:
+            basis = synth.random_product_basis(norb, na, nb, nsa, nsb, seed=bseed)
+        tabs = build_spin_tables(basis)
+        app = HamiltonianApplier(basis, table, tables=tabs, exec_policy="deterministic")
+        rng = np.random.default_rng(1000 + iseed)
+        xs = rng.standard_normal((3, basis.dimension))
+        ys = np.stack([app(x) for x in xs])
+        opts = DavidsonOptions(n_roots=min(2, basis.dimension), restart_keep=min(4, basis.dimension),
+                               max_subspace=min(32, basis.dimension)) if basis.dimension >= 2 else \
+            DavidsonOptions(n_roots=1, restart_keep=1, max_subspace=1)
+        res = davidson_solve(app, app.diag, opts=opts)
+        out[f"{name}/alpha"] = np.asarray(basis.alpha_strings, dtype=np.uint64)
+        out[f"{name}/beta"] = np.asarray(basis.beta_strings, dtype=np.uint64)
+        out[f"{name}/diag"] = app.diag
+        out[f"{name}/x"] = xs
+        out[f"{name}/y"] = ys
+        out[f"{name}/energies"] = res.energies
+        for spin, tab in (("ta", tabs.alpha), ("tb", tabs.beta)):
+            for f in FIELDS:
+                out[f"{name}/{spin}/{f}"] = np.asarray(getattr(tab, f), dtype=DTYPES[f])
+        meta[name] = dict(norb=norb, na=na, nb=nb, nsa=nsa, nsb=nsb, iseed=iseed, bseed=bseed,
+                          iterations=res.stats.iterations, converged=res.stats.converged,
+                          n_roots=opts.n_roots)
+    hb, ht = _hubbard()
+    happ = HamiltonianApplier(hb, ht)
+    out["hubbard/diag"] = happ.diag
+    out["hubbard/col0"] = happ(np.array([1.0, 0.0, 0.0, 0.0]))
+    out["hubbard/dense"] = np.column_stack([happ(np.eye(4)[:, j]) for j in range(4)])
+    out["hubbard/energy"] = davidson_solve(happ, happ.diag, opts=DavidsonOptions(max_subspace=4)).energies
+    # worked enumeration examples (test_basis.py:107-122)
+    out["enum/singles_0b0011_3"] = np.array(enumerate_singles(0b0011, 3), dtype=np.int64)
+    out["enum/doubles_0b0011_4"] = np.array(enumerate_doubles(0b0011, 4), dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "small.npz"), **out)
+    with open(os.path.join(HERE, "small_meta.json"), "w") as f:
+        json.dump(meta, f, indent=1, sort_keys=True)
+    print("small: wrote", len(out), "arrays")
+
+
+def _big(name, norb, na, nb, ns, windows, strings=None):
+    t0 = time.time()
+    table = synth.random_integrals(norb, seed=1)
+    if strings is None:
+        basis = synth.full_product_basis(norb, na, nb) if ns is None else \
+            synth.random_product_basis(norb, na, nb, ns, ns, seed=2)
+    else:
+        from sbdiag.basis import SelectedBasis
+        basis = SelectedBasis.product(strings[0], strings[1], norb, na, nb)
+    t_basis = time.time() - t0
+    t0 = time.time()
+    tabs = build_spin_tables(basis)
+    t_tab = time.time() - t0
+    nbeta = len(basis.beta_strings)
+    rec = dict(norb=norb, na=na, nb=nb, n_alpha=len(basis.alpha_strings), n_beta=nbeta,
+               alpha_digest=strings_digest(basis.alpha_strings),
+               beta_digest=strings_digest(basis.beta_strings),
+               h_digest=digest(table.h, np.float64), eri_digest=digest(table.eri, np.float64),
+               ta=table_digests(tabs.alpha), tb=table_digests(tabs.beta),
+               ta_counts=[int(tabs.alpha.s_off[-1]), int(tabs.alpha.d_off[-1])],
+               tb_counts=[int(tabs.beta.s_off[-1]), int(tabs.beta.d_off[-1])],
+               seconds_basis=t_basis, seconds_tables=t_tab, windows=[])
+    arrays = {}
+    if windows:
+        x = np.random.default_rng(12345).standard_normal(basis.dimension)
+        cache = None
+        for lo, hi in windows:
+            cache = build_det_cache(basis, ((lo, hi), (0, nbeta)), None, cache)
+            d = compute_diagonal(basis, table, cache)
+            t0 = time.time()
+            y = _apply_product(x, basis, table, tabs, cache, d, "parallel")
+            rec["windows"].append(dict(lo=lo, hi=hi, seconds=time.time() - t0))
+            arrays[f"diag_{lo}_{hi}"] = d
+            arrays[f"sigma_{lo}_{hi}"] = y
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **arrays)
+    with open(os.path.join(HERE, f"{name}.json"), "w") as f:
+        json.dump(rec, f, indent=1, sort_keys=True)
+    print(name, "done", {k: rec[k] for k in ("ta_counts", "tb_counts", "seconds_basis", "seconds_tables")})
+    return basis, table, tabs
+
+
+def make_cfg1():
+    _big("cfg1", 12, 6, 6, None, [(0, 8), (457, 461), (916, 924)])
+
+
+def make_cfg1_davidson():
+    table = synth.random_integrals(12, seed=1)
+    basis = synth.full_product_basis(12, 6, 6)
+    app = HamiltonianApplier(basis, table)
+    t0 = time.time()
+    res = davidson_solve(app, app.diag)
+    rec = dict(energy=float(res.energies[0]), iterations=res.stats.iterations,
+               restarts=res.stats.restarts, converged=res.stats.converged,
+               seconds=time.time() - t0, mean_apply=float(np.mean(res.stats.apply_seconds)),
+               threads=int(os.environ.get("NUMBA_NUM_THREADS", os.cpu_count())))
+    with open(os.path.join(HERE, "cfg1_davidson.json"), "w") as f:
+        json.dump(rec, f, indent=1)
+    print("cfg1 davidson", rec)
+
+
+def make_cfg2():
+    _big("cfg2", 26, 7, 7, 10000, [(0, 2), (5000, 5001), (9998, 10000)])
+
+
+def make_cfg4():
+    # the reference generator enumerates C(36,27)=94M strings (~400 s, 7.5 GB)
+    _big("cfg4", 36, 27, 27, 30000, [(0, 1)])
+
+
+if __name__ == "__main__":
+    jobs = dict(small=make_small, cfg1=make_cfg1, cfg2=make_cfg2, cfg4=make_cfg4,
+                **{"cfg1-davidson": make_cfg1_davidson})
+    for arg in sys.argv[1:]:
+        jobs[arg]()
