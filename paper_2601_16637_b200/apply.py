@@ -206,12 +206,12 @@ class HamiltonianApplier:
             self._ctx("sbd_sigma", _lib.ptr(x), _lib.ptr(y))
         return y
 
-    def __call__(self, x):
+    def __call__(self, x, out=None):
         try:
             import torch
 
             if isinstance(x, torch.Tensor) and x.is_cuda:
-                return self.sigma_device(x.reshape(-1))
+                return self.sigma_device(x.reshape(-1), out=out)
         except ImportError:  # pragma: no cover
             pass
         xa = np.asarray(x, dtype=np.float64)
@@ -219,7 +219,9 @@ class HamiltonianApplier:
             raise ValueError(f"expected vector of length {self.n}, got shape {xa.shape}")
         xa = np.ascontiguousarray(xa)
         self.apply_count += 1
-        y = np.empty(self.n_own, dtype=np.float64)
+        y = np.empty(self.n_own, dtype=np.float64) if out is None else out
+        if y.shape != (self.n_own,) or y.dtype != np.float64 or not y.flags.c_contiguous:
+            raise ValueError("out must be a contiguous float64 array of the owned length")
         self._ctx.bind_stream()
         if self.n_own:
             self._ctx("sbd_sigma_host", _lib.ptr(xa), _lib.ptr(y))

@@ -195,7 +195,7 @@ def _operator(apply_h, n: int, device):
 
 def davidson_solve(apply_h: Callable, diag, x0=None, opts: Optional[DavidsonOptions] = None,
                    device=None, return_device: bool = False, allreduce=None,
-                   rank_offset: int = 0) -> DavidsonResult:
+                   rank_offset: int = 0, ctx=None) -> DavidsonResult:
     """Lowest ``opts.n_roots`` eigenpairs (reference ``davidson.py:191-306``).
 
     ``allreduce(tensor)`` (optional) sums a small CUDA tensor over ranks in
@@ -231,15 +231,19 @@ def davidson_solve(apply_h: Callable, diag, x0=None, opts: Optional[DavidsonOpti
     dev = torch.device("cuda", int(device))
     with torch.cuda.device(dev):
         return _solve(apply_h, diag_dev if diag_dev is not None else torch.from_numpy(diag_np).to(dev),
-                      x0, opts, n, n_loc, dev, return_device, allreduce, rank_offset)
+                      x0, opts, n, n_loc, dev, return_device, allreduce, rank_offset, ctx)
 
 
-def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce, rank_offset):
+def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce, rank_offset, ctx):
     import torch
 
     f64 = dict(dtype=torch.float64, device=dev)
     diag_dev = diag_dev.to(dev).contiguous()
-    apply_fn, ctx = _operator(apply_h, n_loc, dev) if allreduce is None else (apply_h, None)
+    if allreduce is None:
+        apply_fn, op_ctx = _operator(apply_h, n_loc, dev)
+        ctx = ctx if ctx is not None else op_ctx
+    else:
+        apply_fn = apply_h
     eng = _Engine(dev.index, ctx)
     reduce = allreduce if allreduce is not None else (lambda t: None)
 
@@ -319,18 +323,21 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
         if int(jac_info.item()) >= 64:
             raise RuntimeError("Jacobi sweep limit 64 reached without convergence")
         evals, evecs = jw.copy(), jv.cpu().numpy().copy()
-        theta = evals[:m].copy()
-        Y = np.ascontiguousarray(evecs[:, :m])
+        # numpy slicing in the reference keeps min(m, k) roots while k < m
+        mk = min(m, k)
+        theta = evals[:mk].copy()
+        Y = np.ascontiguousarray(evecs[:, :mk])
         ritz_rotated = False
 
         # residuals, preconditioned corrections and V^T t in one pass
-        Y_dev[: k * m].copy_(torch.from_numpy(Y.reshape(-1)))
-        th_dev[:m].copy_(torch.from_numpy(theta))
-        eng("sbd_residual_precond_target", _p(V), _p(W), k, ld, n_loc, _p(Y_dev), _p(th_dev), m, jp,
+        Y_dev[: k * mk].copy_(torch.from_numpy(Y.reshape(-1)))
+        th_dev[:mk].copy_(torch.from_numpy(theta))
+        jp = min(jp, mk - 1)
+        eng("sbd_residual_precond_target", _p(V), _p(W), k, ld, n_loc, _p(Y_dev), _p(th_dev), mk, jp,
             _p(diag_dev), float(opts.precond_delta), _p(Tv), ld, _p(small))
-        reduce(small[: k + 1 + m])
-        out = small[: k + 1 + m].cpu().numpy()
-        res_norms = np.sqrt(np.maximum(out[k + 1:k + 1 + m], 0.0))
+        reduce(small[: k + 1 + mk])
+        out = small[: k + 1 + mk].cpu().numpy()
+        res_norms = np.sqrt(np.maximum(out[k + 1:k + 1 + mk], 0.0))
         proj = out[:k].copy()
         t_norm2 = float(out[k])
 
@@ -400,15 +407,16 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
         stats.iter_seconds.append(time.perf_counter() - t_iter)
 
     # Ritz vectors of the last Rayleigh-Ritz (davidson.py:256), computed once
+    mk = Y.shape[1]
     if ritz_rotated:
-        Yr = np.zeros((k, m))
-        Yr[:m, :m] = np.eye(m)
+        Yr = np.zeros((k, mk))
+        Yr[:mk, :mk] = np.eye(mk)
     else:
         Yr = Y
     kk = Yr.shape[0]
-    Y_dev[: kk * m].copy_(torch.from_numpy(np.ascontiguousarray(Yr).reshape(-1)))
-    U = torch.empty((m, n_loc), **f64)
-    eng("sbd_combine", _p(V), kk, ld, n_loc, _p(Y_dev), m, _p(U), n_loc)
+    Y_dev[: kk * mk].copy_(torch.from_numpy(np.ascontiguousarray(Yr).reshape(-1)))
+    U = torch.empty((mk, n_loc), **f64)
+    eng("sbd_combine", _p(V), kk, ld, n_loc, _p(Y_dev), mk, _p(U), n_loc)
     torch.cuda.current_stream(dev).synchronize()
     vectors = U if return_device else U.cpu().numpy()
     if eng.own_ctx:
