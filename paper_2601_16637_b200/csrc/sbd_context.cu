@@ -112,6 +112,14 @@ int sbd_set_integrals(sbd_ctx *ctx, int norb, const double *h_host, const double
     SBD_CUDA(ctx, cudaMemcpy(ctx->h.p, h_host, sizeof(double) * norb * norb, cudaMemcpyHostToDevice));
     SBD_CUDA(ctx, cudaMemcpy(ctx->eri.p, eri_host, sizeof(double) * n_eri, cudaMemcpyHostToDevice));
     SBD_CUDA(ctx, cudaMemcpy(ctx->dpq.p, dpq.data(), sizeof(double) * norb * norb, cudaMemcpyHostToDevice));
+    ctx->ld_vpp = (npair + 1) / 2 * 2;
+    {
+        std::vector<double> vpp((size_t)npair * ctx->ld_vpp, 0.0);
+        for (i64 P = 0; P < npair; ++P)
+            for (i64 Q = 0; Q < npair; ++Q) vpp[(size_t)P * ctx->ld_vpp + Q] = eri_host[tri_idx(P, Q)];
+        SBD_CUDA(ctx, ctx->vpp.ensure(sizeof(double) * vpp.size()));
+        SBD_CUDA(ctx, cudaMemcpy(ctx->vpp.p, vpp.data(), sizeof(double) * vpp.size(), cudaMemcpyHostToDevice));
+    }
     ctx->have_integrals = true;
     ctx->sec[0].built = ctx->sec[1].built = false;
     ctx->diag_valid = false;

@@ -16,6 +16,7 @@
 //   sbd_rotate           thick restart V <- V Y_keep in place       (davidson.py:280-289)
 //   sbd_jacobi           projected k x k eigensolve, one warp       (davidson.py:86-148)
 #include <algorithm>
+#include <utility>
 
 #include "sbd_internal.cuh"
 
@@ -61,44 +62,121 @@ __global__ void finish_partials(const double *__restrict__ partial, int nblocks,
     out[i] = s;
 }
 
-template <int K>
+// Streaming over element "slots": with V2 a slot is a 16-byte pair of doubles
+// (128-bit loads), otherwise one double.  Callers guarantee 16-byte aligned
+// bases and even leading dimensions for V2; the odd tail element of a V2 run
+// is folded in by thread 0 of block 0.
+template <bool V2>
+struct Slot {
+    static constexpr int W = V2 ? 2 : 1;
+    double v[2];
+    __device__ __forceinline__ void load(const double *p, i64 s) {
+        if (V2) {
+            const double2 t = __ldg(reinterpret_cast<const double2 *>(p) + s);
+            v[0] = t.x;
+            v[1] = t.y;
+        } else {
+            v[0] = __ldg(p + s);
+            v[1] = 0.0;
+        }
+    }
+    __device__ __forceinline__ void load_cs(const double *p, i64 s) {
+        if (V2) {
+            const double2 t = __ldcs(reinterpret_cast<const double2 *>(p) + s);
+            v[0] = t.x;
+            v[1] = t.y;
+        } else {
+            v[0] = __ldcs(p + s);
+            v[1] = 0.0;
+        }
+    }
+    __device__ __forceinline__ void load_rw(const double *p, i64 s) {  // data written earlier in this kernel
+        if (V2) {
+            const double2 t = reinterpret_cast<const double2 *>(p)[s];
+            v[0] = t.x;
+            v[1] = t.y;
+        } else {
+            v[0] = p[s];
+            v[1] = 0.0;
+        }
+    }
+    __device__ __forceinline__ void store(double *p, i64 s) const {
+        if (V2) reinterpret_cast<double2 *>(p)[s] = make_double2(v[0], v[1]);
+        else p[s] = v[0];
+    }
+    __device__ __forceinline__ double dot(const Slot &o) const { return V2 ? fma(v[0], o.v[0], v[1] * o.v[1]) : v[0] * o.v[0]; }
+};
+
+// visit every slot once (grid-stride), then the scalar tail (n odd, V2) once
+template <bool V2, class FS, class FT>
+__device__ __forceinline__ void for_slots(i64 n, FS &&slot_fn, FT &&tail_fn) {
+    const i64 ns = V2 ? n / 2 : n;
+    for (i64 s = (i64)blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += (i64)gridDim.x * blockDim.x) slot_fn(s);
+    if (V2 && (n & 1) && blockIdx.x == 0 && threadIdx.x == 0) tail_fn(n - 1);
+}
+
+template <int K, bool V2>
 __global__ void __launch_bounds__(kBlock) vdots_kernel(const double *__restrict__ V, int k, i64 ldv, i64 n,
                                                        const double *__restrict__ w, double *__restrict__ partial) {
     double acc[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) acc[i] = 0.0;
-    for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (i64)gridDim.x * blockDim.x) {
-        const double we = __ldcs(w + e);
+    const i64 ldvs = V2 ? ldv / 2 : ldv;
+    for_slots<V2>(n, [&](i64 s) {
+        Slot<V2> ws;
+        ws.load_cs(w, s);
 #pragma unroll
         for (int i = 0; i < K; ++i)
-            if (i < k) acc[i] = fma(__ldcs(V + i * ldv + e), we, acc[i]);
-    }
+            if (i < k) {
+                Slot<V2> vs;
+                vs.load_cs(V + i * ldv, s);
+                acc[i] += vs.dot(ws);
+            }
+    }, [&](i64 e) {
+        const double we = w[e];
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (i < k) acc[i] = fma(V[i * ldv + e], we, acc[i]);
+    });
+    (void)ldvs;
     block_partials<K>(acc, partial);
 }
 
 // out[i] = V_i . w, out[K + i] = V_i . u  (one pass over V, two right-hand sides)
-template <int K>
+template <int K, bool V2>
 __global__ void __launch_bounds__(kBlock) vdots2_kernel(const double *__restrict__ V, int k, i64 ldv, i64 n,
                                                         const double *__restrict__ w, const double *__restrict__ u,
                                                         double *__restrict__ partial) {
     double acc[2 * K];
 #pragma unroll
     for (int i = 0; i < 2 * K; ++i) acc[i] = 0.0;
-    for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (i64)gridDim.x * blockDim.x) {
-        const double we = __ldcs(w + e), ue = __ldg(u + e);
+    for_slots<V2>(n, [&](i64 s) {
+        Slot<V2> ws, us;
+        ws.load_cs(w, s);
+        us.load(u, s);
 #pragma unroll
         for (int i = 0; i < K; ++i)
             if (i < k) {
-                const double v = __ldcs(V + i * ldv + e);
+                Slot<V2> vs;
+                vs.load_cs(V + i * ldv, s);
+                acc[i] += vs.dot(ws);
+                acc[K + i] += vs.dot(us);
+            }
+    }, [&](i64 e) {
+        const double we = w[e], ue = u[e];
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (i < k) {
+                const double v = V[i * ldv + e];
                 acc[i] = fma(v, we, acc[i]);
                 acc[K + i] = fma(v, ue, acc[K + i]);
             }
-    }
+    });
     block_partials<2 * K>(acc, partial);
 }
 
-// K >= k; m <= 8 roots; jp = root whose preconditioned residual is projected
-template <int K, int M>
+// Ritz residual, preconditioner and projections (M = compile-time bound on roots)
+template <int K, int M, bool V2>
 __global__ void __launch_bounds__(kBlock)
 residual_kernel(const double *__restrict__ V, const double *__restrict__ W, int k, i64 ldv, i64 n,
                 const double *__restrict__ Y, const double *__restrict__ theta, int m, int jp,
@@ -113,70 +191,422 @@ residual_kernel(const double *__restrict__ V, const double *__restrict__ W, int 
     double acc[K + 1 + M];
 #pragma unroll
     for (int i = 0; i < K + 1 + M; ++i) acc[i] = 0.0;
-    for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (i64)gridDim.x * blockDim.x) {
-        double u[M], wy[M];
-#pragma unroll
-        for (int j = 0; j < M; ++j) u[j] = wy[j] = 0.0;
-        // Ritz vector and image components (davidson.py:256-257): u = Y^T V, wy = Y^T W
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            if (i < k) {
-                const double v = V[i * ldv + e], ww = __ldcs(W + i * ldv + e);
-#pragma unroll
-                for (int j = 0; j < M; ++j)
-                    if (j < m) {
-                        u[j] = fma(ys[i * m + j], v, u[j]);
-                        wy[j] = fma(ys[i * m + j], ww, wy[j]);
-                    }
-            }
-        }
-        const double d = diag[e];
+    auto element = [&](const double (&u)[M], const double (&wy)[M], double d, double *tout, i64 ldt_, i64 pos,
+                       double &tj_out) {
         double tj = 0.0;
 #pragma unroll
         for (int j = 0; j < M; ++j) {
             if (j < m) {
                 const double r = wy[j] - th[j] * u[j];
                 acc[K + 1 + j] = fma(r, r, acc[K + 1 + j]);
-                // precondition (davidson.py:159-163): sign(0) = +1, clamp at delta
                 const double g = d - th[j];
-                const double den = (g >= 0.0 ? 1.0 : -1.0) * fmax(fabs(g), delta);
+                const double den = (g >= 0.0 ? 1.0 : -1.0) * fmax(fabs(g), delta);  // davidson.py:159-163
                 const double t = r / den;
-                T[j * ldt + e] = t;
+                tout[j * ldt_ + pos] = t;
                 if (j == jp) tj = t;
             }
         }
         acc[K] = fma(tj, tj, acc[K]);
+        tj_out = tj;
+    };
+    for_slots<V2>(n, [&](i64 s) {
+        double u[2][M], wy[2][M];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < M; ++j) u[h][j] = wy[h][j] = 0.0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            if (i < k) {
+                Slot<V2> vs, wsl;
+                vs.load(V + i * ldv, s);
+                wsl.load_cs(W + i * ldv, s);
+#pragma unroll
+                for (int j = 0; j < M; ++j)
+                    if (j < m) {
+                        const double yij = ys[i * m + j];
+#pragma unroll
+                        for (int h = 0; h < Slot<V2>::W; ++h) {
+                            u[h][j] = fma(yij, vs.v[h], u[h][j]);
+                            wy[h][j] = fma(yij, wsl.v[h], wy[h][j]);
+                        }
+                    }
+            }
+        }
+        Slot<V2> ds;
+        ds.load(diag, s);
+        double tjv[2] = {0.0, 0.0};
+#pragma unroll
+        for (int h = 0; h < Slot<V2>::W; ++h) element(u[h], wy[h], ds.v[h], T, ldt, (V2 ? 2 * s : s) + h, tjv[h]);
+        Slot<V2> ts;
+        ts.v[0] = tjv[0];
+        ts.v[1] = tjv[1];
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (i < k) {
+                Slot<V2> vs;
+                vs.load(V + i * ldv, s);  // second touch: L1
+                acc[i] += vs.dot(ts);
+            }
+    }, [&](i64 e) {
+        double u[M], wy[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) u[j] = wy[j] = 0.0;
+        for (int i = 0; i < k; ++i)
+#pragma unroll
+            for (int j = 0; j < M; ++j)
+                if (j < m) {
+                    u[j] = fma(ys[i * m + j], V[i * ldv + e], u[j]);
+                    wy[j] = fma(ys[i * m + j], W[i * ldv + e], wy[j]);
+                }
+        double tj;
+        element(u, wy, diag[e], T, ldt, e, tj);
 #pragma unroll
         for (int i = 0; i < K; ++i)
             if (i < k) acc[i] = fma(V[i * ldv + e], tj, acc[i]);
-    }
+    });
     block_partials<K + 1 + M>(acc, partial);
 }
 
-// t -= sum_i c_i V_i ; then partial dots V_i . t (i < kdot) and |t|^2 (slot kdot)
-template <int K>
+// t -= sum_i c_i V_i ; then partial dots V_i . t (i < kdot) and |t|^2 (slot K)
+template <int K, bool V2>
 __global__ void __launch_bounds__(kBlock) gs_kernel(const double *__restrict__ V, int k, i64 ldv, i64 n,
                                                     const double *__restrict__ c, int kdot, double *__restrict__ t,
                                                     double *__restrict__ partial) {
-    __shared__ double cs[K];
+    __shared__ double cs[K > 0 ? K : 1];
     for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = c[i];
     __syncthreads();
     double acc[K + 1];
 #pragma unroll
     for (int i = 0; i <= K; ++i) acc[i] = 0.0;
-    for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (i64)gridDim.x * blockDim.x) {
+    for_slots<V2>(n, [&](i64 s) {
+        Slot<V2> ts;
+        ts.load_rw(t, s);
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (i < k) {
+                Slot<V2> vs;
+                vs.load(V + i * ldv, s);
+#pragma unroll
+                for (int h = 0; h < Slot<V2>::W; ++h) ts.v[h] = fma(-cs[i], vs.v[h], ts.v[h]);
+            }
+        ts.store(t, s);
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (i < kdot) {
+                Slot<V2> vs;
+                vs.load(V + i * ldv, s);  // second touch: L1
+                acc[i] += vs.dot(ts);
+            }
+        acc[K] += ts.dot(ts);
+    }, [&](i64 e) {
         double te = t[e];
-#pragma unroll
-        for (int i = 0; i < K; ++i)
-            if (i < k) te = fma(-cs[i], V[i * ldv + e], te);
+        for (int i = 0; i < k; ++i) te = fma(-cs[i], V[i * ldv + e], te);
         t[e] = te;
-        // second touch of the same V lines: served by L1
 #pragma unroll
         for (int i = 0; i < K; ++i)
-            if (i < kdot) acc[i] = fma(__ldg(V + i * ldv + e), te, acc[i]);
+            if (i < kdot) acc[i] = fma(V[i * ldv + e], te, acc[i]);
         acc[K] = fma(te, te, acc[K]);
-    }
+    });
     block_partials<K + 1>(acc, partial);
+}
+
+// ---------------------------------------------------------------------------
+// Tile kernels (the aligned fast path).  A CTA walks tiles of TT contiguous
+// elements; its 8 warps split the k basis vectors (warp w owns vectors w,
+// w+8, ...), and each lane issues QD independent 128-bit loads per vector, so
+// a warp has QD*512 B in flight per vector with O(k/8) accumulators -- the
+// register pressure of a per-element design is gone.  Cross-warp sums over
+// the vectors (t - V c, Y^T V, Y^T W) go through shared memory.  Requires
+// 16-byte aligned bases and even leading dimensions (the Python driver
+// allocates that way); the per-element kernels above stay as the fallback.
+constexpr int kWarpsT = kBlock / 32;
+
+__device__ __forceinline__ double2 ld2(const double *__restrict__ p, i64 e, i64 n) {
+    // p + e is 16-byte aligned (e even); elements >= n read as 0
+    if (e + 1 < n) return __ldcs(reinterpret_cast<const double2 *>(p + e));
+    if (e < n) return make_double2(__ldcs(p + e), 0.0);
+    return make_double2(0.0, 0.0);
+}
+__device__ __forceinline__ double2 ld2_keep(const double *__restrict__ p, i64 e, i64 n) {
+    if (e + 1 < n) return __ldg(reinterpret_cast<const double2 *>(p + e));
+    if (e < n) return make_double2(__ldg(p + e), 0.0);
+    return make_double2(0.0, 0.0);
+}
+__device__ __forceinline__ double dot2(double2 a, double2 b) { return fma(a.x, b.x, a.y * b.y); }
+
+// out[i] = V_i . w, out[K + i] = V_i . u
+template <int K>
+__global__ void __launch_bounds__(kBlock) vdots2_tile(const double *__restrict__ V, int k, i64 ldv, i64 n,
+                                                      const double *__restrict__ w, const double *__restrict__ u,
+                                                      double *__restrict__ partial) {
+    constexpr int TT = 1024, QD = TT / 64, KW = (K + kWarpsT - 1) / kWarpsT;
+    __shared__ double2 ws[TT / 2], us[TT / 2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double aw[KW], au[KW];
+#pragma unroll
+    for (int a = 0; a < KW; ++a) aw[a] = au[a] = 0.0;
+    for (i64 base = (i64)blockIdx.x * TT; base < n; base += (i64)gridDim.x * TT) {
+        const i64 rem = n - base;
+        for (int d = threadIdx.x; d < TT / 2; d += blockDim.x) {
+            ws[d] = ld2(w + base, 2 * d, rem);
+            us[d] = ld2_keep(u + base, 2 * d, rem);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < KW; ++a) {
+            const int i = warp + kWarpsT * a;
+            if (i < k) {
+                const double *vi = V + i * ldv + base;
+                double2 v[QD];
+#pragma unroll
+                for (int q = 0; q < QD; ++q) v[q] = ld2(vi, 2 * (lane + 32 * q), rem);
+#pragma unroll
+                for (int q = 0; q < QD; ++q) {
+                    aw[a] += dot2(v[q], ws[lane + 32 * q]);
+                    au[a] += dot2(v[q], us[lane + 32 * q]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < KW; ++a) {
+        const int i = warp + kWarpsT * a;
+        const double sw = warp_sum(aw[a]), su = warp_sum(au[a]);
+        if (lane == 0 && i < K) {
+            partial[(i64)blockIdx.x * 2 * K + i] = i < k ? sw : 0.0;
+            partial[(i64)blockIdx.x * 2 * K + K + i] = i < k ? su : 0.0;
+        }
+    }
+}
+
+// t -= V c ; dots V_i . t (i < kdot) ; |t|^2  -> partial[b * (K+1) + ...]
+template <int K>
+__global__ void __launch_bounds__(kBlock) gs_tile(const double *__restrict__ V, int k, i64 ldv, i64 n,
+                                                  const double *__restrict__ c, int kdot, double *__restrict__ t,
+                                                  double *__restrict__ partial) {
+    constexpr int TT = 512, QD = TT / 64, KW = (K + kWarpsT - 1) / kWarpsT;
+    __shared__ double2 part[kWarpsT][TT / 2];
+    __shared__ double2 ts[TT / 2];
+    __shared__ double cs[K];
+    __shared__ double nrm[kWarpsT];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = c[i];
+    double acc[KW];
+#pragma unroll
+    for (int a = 0; a < KW; ++a) acc[a] = 0.0;
+    double n2 = 0.0;
+    __syncthreads();
+    for (i64 base = (i64)blockIdx.x * TT; base < n; base += (i64)gridDim.x * TT) {
+        const i64 rem = n - base;
+        // phase 1: warp partial of sum_i c_i V_i over its vectors
+        double2 s[QD];
+#pragma unroll
+        for (int q = 0; q < QD; ++q) s[q] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int a = 0; a < KW; ++a) {
+            const int i = warp + kWarpsT * a;
+            if (i < k) {
+                const double *vi = V + i * ldv + base;
+                const double ci = cs[i];
+#pragma unroll
+                for (int q = 0; q < QD; ++q) {
+                    const double2 v = ld2_keep(vi, 2 * (lane + 32 * q), rem);
+                    s[q].x = fma(ci, v.x, s[q].x);
+                    s[q].y = fma(ci, v.y, s[q].y);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < QD; ++q) part[warp][lane + 32 * q] = s[q];
+        __syncthreads();
+        // combine: t_new = t - sum over warps
+        for (int d = threadIdx.x; d < TT / 2; d += blockDim.x) {
+            const i64 e = base + 2 * d;
+            double2 tv = make_double2(0.0, 0.0);
+            if (e + 1 < n) tv = *reinterpret_cast<const double2 *>(t + e);
+            else if (e < n) tv.x = t[e];
+#pragma unroll
+            for (int ww = 0; ww < kWarpsT; ++ww) {
+                tv.x -= part[ww][d].x;
+                tv.y -= part[ww][d].y;
+            }
+            if (e + 1 < n) *reinterpret_cast<double2 *>(t + e) = tv;
+            else if (e < n) t[e] = tv.x;
+            if (e >= n) tv.x = 0.0;
+            if (e + 1 >= n) tv.y = 0.0;
+            ts[d] = tv;
+            n2 += dot2(tv, tv);
+        }
+        __syncthreads();
+        // phase 2: dots with the updated t (V tile re-read: L1/L2)
+        if (kdot > 0) {
+#pragma unroll
+            for (int a = 0; a < KW; ++a) {
+                const int i = warp + kWarpsT * a;
+                if (i < kdot) {
+                    const double *vi = V + i * ldv + base;
+#pragma unroll
+                    for (int q = 0; q < QD; ++q) acc[a] += dot2(ld2_keep(vi, 2 * (lane + 32 * q), rem), ts[lane + 32 * q]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    n2 = warp_sum(n2);
+    if (lane == 0) nrm[warp] = n2;
+#pragma unroll
+    for (int a = 0; a < KW; ++a) {
+        const int i = warp + kWarpsT * a;
+        const double sa = warp_sum(acc[a]);
+        if (lane == 0 && i < K) partial[(i64)blockIdx.x * (K + 1) + i] = i < kdot ? sa : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int ww = 0; ww < kWarpsT; ++ww) s += nrm[ww];
+        partial[(i64)blockIdx.x * (K + 1) + K] = s;
+    }
+}
+
+// Ritz residuals, preconditioned corrections T_j and projections V^T t_jp.
+// partial layout per block (stride K + 1 + M): [0,K) dots | K: |t_jp|^2 | K+1+j: |r_j|^2
+template <int K, int M>
+__global__ void __launch_bounds__(kBlock)
+residual_tile(const double *__restrict__ V, const double *__restrict__ W, int k, i64 ldv, i64 n,
+              const double *__restrict__ Y, const double *__restrict__ theta, int m, int jp,
+              const double *__restrict__ diag, double delta, double *__restrict__ T, i64 ldt,
+              double *__restrict__ partial) {
+    constexpr int TT = 512 / M, QD = TT / 64 > 0 ? TT / 64 : 1, KW = (K + kWarpsT - 1) / kWarpsT;
+    extern __shared__ double2 rsm[];
+    double2 *pu = rsm;                                  // [kWarpsT][M][TT/2]
+    double2 *pw = rsm + kWarpsT * M * (TT / 2);         // [kWarpsT][M][TT/2]
+    double2 *ts = pw + kWarpsT * M * (TT / 2);          // [TT/2]
+    __shared__ double ys[64 * 8];
+    __shared__ double th[8];
+    __shared__ double red[kWarpsT][M + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < k * m; i += blockDim.x) ys[i] = Y[i];
+    if (threadIdx.x < m) th[threadIdx.x] = theta[threadIdx.x];
+    double acc[KW];
+#pragma unroll
+    for (int a = 0; a < KW; ++a) acc[a] = 0.0;
+    double rn2[M], tn2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) rn2[j] = 0.0;
+    __syncthreads();
+    for (i64 base = (i64)blockIdx.x * TT; base < n; base += (i64)gridDim.x * TT) {
+        const i64 rem = n - base;
+        double2 u[M][QD], wy[M][QD];
+#pragma unroll
+        for (int j = 0; j < M; ++j)
+#pragma unroll
+            for (int q = 0; q < QD; ++q) u[j][q] = wy[j][q] = make_double2(0.0, 0.0);
+        const bool lane_on = 2 * lane < TT;  // M = 8: a tile is 64 elements = 32 pairs
+#pragma unroll
+        for (int a = 0; a < KW; ++a) {
+            const int i = warp + kWarpsT * a;
+            if (i < k && lane_on) {
+                const double *vi = V + i * ldv + base, *wi = W + i * ldv + base;
+                double2 v[QD], x[QD];
+#pragma unroll
+                for (int q = 0; q < QD; ++q) {
+                    v[q] = ld2_keep(vi, 2 * (lane + 32 * q), rem);
+                    x[q] = ld2(wi, 2 * (lane + 32 * q), rem);
+                }
+#pragma unroll
+                for (int j = 0; j < M; ++j) {
+                    if (j < m) {
+                        const double y = ys[i * m + j];
+#pragma unroll
+                        for (int q = 0; q < QD; ++q) {
+                            u[j][q].x = fma(y, v[q].x, u[j][q].x);
+                            u[j][q].y = fma(y, v[q].y, u[j][q].y);
+                            wy[j][q].x = fma(y, x[q].x, wy[j][q].x);
+                            wy[j][q].y = fma(y, x[q].y, wy[j][q].y);
+                        }
+                    }
+                }
+            }
+        }
+        if (lane_on) {
+#pragma unroll
+            for (int j = 0; j < M; ++j)
+#pragma unroll
+                for (int q = 0; q < QD; ++q) {
+                    pu[(warp * M + j) * (TT / 2) + lane + 32 * q] = u[j][q];
+                    pw[(warp * M + j) * (TT / 2) + lane + 32 * q] = wy[j][q];
+                }
+        }
+        __syncthreads();
+        for (int d = threadIdx.x; d < TT / 2; d += blockDim.x) {
+            const i64 e = base + 2 * d;
+            const double2 dg = ld2_keep(diag, e, n);
+            double2 tj = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+                if (j < m) {
+                    double2 uu = make_double2(0.0, 0.0), ww2 = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int w2 = 0; w2 < kWarpsT; ++w2) {
+                        const double2 a1 = pu[(w2 * M + j) * (TT / 2) + d], b1 = pw[(w2 * M + j) * (TT / 2) + d];
+                        uu.x += a1.x;
+                        uu.y += a1.y;
+                        ww2.x += b1.x;
+                        ww2.y += b1.y;
+                    }
+                    // r = Y^T W - theta Y^T V ; t = r / (sign(d - theta) max(|d - theta|, delta))
+                    const double rx = ww2.x - th[j] * uu.x, ry = ww2.y - th[j] * uu.y;
+                    const double gx = dg.x - th[j], gy = dg.y - th[j];
+                    const double tx = rx / ((gx >= 0.0 ? 1.0 : -1.0) * fmax(fabs(gx), delta));
+                    const double ty = ry / ((gy >= 0.0 ? 1.0 : -1.0) * fmax(fabs(gy), delta));
+                    double *tr = T + j * ldt;
+                    if (e + 1 < n) {
+                        *reinterpret_cast<double2 *>(tr + e) = make_double2(tx, ty);
+                        rn2[j] += rx * rx + ry * ry;
+                    } else if (e < n) {
+                        tr[e] = tx;
+                        rn2[j] += rx * rx;
+                    }
+                    if (j == jp) tj = make_double2(e < n ? tx : 0.0, e + 1 < n ? ty : 0.0);
+                }
+            }
+            ts[d] = tj;
+            tn2 += dot2(tj, tj);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < KW; ++a) {
+            const int i = warp + kWarpsT * a;
+            if (i < k && lane_on) {
+                const double *vi = V + i * ldv + base;
+#pragma unroll
+                for (int q = 0; q < QD; ++q) acc[a] += dot2(ld2_keep(vi, 2 * (lane + 32 * q), rem), ts[lane + 32 * q]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < KW; ++a) {
+        const int i = warp + kWarpsT * a;
+        const double s = warp_sum(acc[a]);
+        if (lane == 0 && i < K) partial[(i64)blockIdx.x * (K + 1 + M) + i] = i < k ? s : 0.0;
+    }
+    tn2 = warp_sum(tn2);
+#pragma unroll
+    for (int j = 0; j < M; ++j) rn2[j] = warp_sum(rn2[j]);
+    if (lane == 0) {
+        red[warp][0] = tn2;
+#pragma unroll
+        for (int j = 0; j < M; ++j) red[warp][1 + j] = rn2[j];
+    }
+    __syncthreads();
+    if (threadIdx.x <= M) {
+        double s = 0.0;
+        for (int ww = 0; ww < kWarpsT; ++ww) s += red[ww][threadIdx.x];
+        partial[(i64)blockIdx.x * (K + 1 + M) + K + threadIdx.x] = s;
+    }
 }
 
 __global__ void scale_copy_kernel(const double *__restrict__ src, double *__restrict__ dst, i64 n,
@@ -315,12 +745,25 @@ __global__ void jacobi_kernel(const double *__restrict__ Ain, int k, int lda, do
     }
 }
 
+inline bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+inline bool vec_ok(const double *V, i64 ldv) { return al16(V) && ldv % 2 == 0; }
+template <class... P>
+inline bool vec_ok(const double *V, i64 ldv, const double *p, P... rest) {
+    return al16(p) && vec_ok(V, ldv, rest...);
+}
+
+int tile_blocks(sbd_ctx *ctx, i64 n, int tt) {
+    i64 b = (n + tt - 1) / tt;
+    return (int)std::max<i64>(1, std::min<i64>(b, (i64)ctx->num_sms * 8));
+}
+
 int red_blocks(sbd_ctx *ctx, i64 n) {
     i64 b = (n + kBlock - 1) / kBlock;
     return (int)std::max<i64>(1, std::min<i64>(b, (i64)ctx->num_sms * 4));
 }
 
 int ensure_red(sbd_ctx *ctx, int nblocks, int stride) {
+    nblocks = std::max(nblocks, ctx->num_sms * 8);
     SBD_CUDA(ctx, ctx->red.ensure(sizeof(double) * (size_t)nblocks * stride + 64));
     return SBD_OK;
 }
@@ -343,7 +786,8 @@ struct VdotsL {
     static int run(sbd_ctx *ctx, const double *V, int k, i64 ldv, i64 n, const double *w, double *out) {
         int nb = red_blocks(ctx, n);
         if (int rc = ensure_red(ctx, nb, K)) return rc;
-        vdots_kernel<K><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, w, ctx->red.as<double>());
+        if (vec_ok(V, ldv, w)) vdots_kernel<K, true><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, w, ctx->red.as<double>());
+        else vdots_kernel<K, false><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, w, ctx->red.as<double>());
         finish_partials<<<1, 64, 0, ctx->stream>>>(ctx->red.as<double>(), nb, K, k, K, k, out);
         SBD_LAUNCHED(ctx, "vdots");
         return SBD_OK;
@@ -356,7 +800,15 @@ struct Vdots2L {
                    double *out) {
         int nb = red_blocks(ctx, n);
         if (int rc = ensure_red(ctx, nb, 2 * K)) return rc;
-        vdots2_kernel<K><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, w, u, ctx->red.as<double>());
+        if (vec_ok(V, ldv, w, u)) {
+            const int nt = tile_blocks(ctx, n, 1024);
+            vdots2_tile<K><<<nt, kBlock, 0, ctx->stream>>>(V, k, ldv, n, w, u, ctx->red.as<double>());
+            finish_partials<<<1, 64, 0, ctx->stream>>>(ctx->red.as<double>(), nt, 2 * K, k, K, k, out);
+            finish_partials<<<1, 64, 0, ctx->stream>>>(ctx->red.as<double>() + K, nt, 2 * K, k, K, k, out + k);
+            SBD_LAUNCHED(ctx, "vdots2");
+            return SBD_OK;
+        }
+        vdots2_kernel<K, false><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, w, u, ctx->red.as<double>());
         finish_partials<<<1, 64, 0, ctx->stream>>>(ctx->red.as<double>(), nb, 2 * K, k, K, k, out);
         finish_partials<<<1, 64, 0, ctx->stream>>>(ctx->red.as<double>() + K, nb, 2 * K, k, K, k, out + k);
         SBD_LAUNCHED(ctx, "vdots2");
@@ -366,24 +818,39 @@ struct Vdots2L {
 
 template <int K>
 struct ResidL {
+    // returns (blocks, partial stride) of the launched kernel
     template <int M>
-    static void launch(sbd_ctx *ctx, int nb, const double *V, const double *W, int k, i64 ldv, i64 n,
-                       const double *Y, const double *theta, int m, int jp, const double *diag, double delta,
-                       double *T, i64 ldt) {
-        residual_kernel<K, M><<<nb, kBlock, 0, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T, ldt,
-                                                             ctx->red.as<double>());
+    static std::pair<int, int> launch(sbd_ctx *ctx, int nb, const double *V, const double *W, int k, i64 ldv, i64 n,
+                                      const double *Y, const double *theta, int m, int jp, const double *diag,
+                                      double delta, double *T, i64 ldt) {
+        if (vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0) {
+            constexpr int TT = 512 / M;
+            const int nt = tile_blocks(ctx, n, TT);
+            const size_t smem = sizeof(double2) * (2 * kWarpsT * M * (TT / 2) + TT / 2);
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(residual_tile<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                attr = true;
+            }
+            residual_tile<K, M><<<nt, kBlock, smem, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T,
+                                                                  ldt, ctx->red.as<double>());
+            return {nt, K + 1 + M};
+        }
+        residual_kernel<K, M, false><<<nb, kBlock, 0, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T,
+                                                                    ldt, ctx->red.as<double>());
+        return {nb, K + 1 + M};
     }
     static int run(sbd_ctx *ctx, const double *V, const double *W, int k, i64 ldv, i64 n, const double *Y,
                    const double *theta, int m, int jp, const double *diag, double delta, double *T, i64 ldt,
                    double *out) {
         int nb = red_blocks(ctx, n);
-        if (int rc = ensure_red(ctx, nb, K + 9)) return rc;
-        if (m == 1) launch<1>(ctx, nb, V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T, ldt);
-        else if (m == 2) launch<2>(ctx, nb, V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T, ldt);
-        else if (m <= 4) launch<4>(ctx, nb, V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T, ldt);
-        else launch<8>(ctx, nb, V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T, ldt);
-        const int stride = K + 1 + (m == 1 ? 1 : m == 2 ? 2 : m <= 4 ? 4 : 8);
-        finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nb, stride, k, K, k + 1 + m, out);
+        if (int rc = ensure_red(ctx, (int)ctx->num_sms * 8, K + 9)) return rc;
+        std::pair<int, int> bs;
+        if (m == 1) bs = launch<1>(ctx, nb, V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T, ldt);
+        else if (m == 2) bs = launch<2>(ctx, nb, V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T, ldt);
+        else if (m <= 4) bs = launch<4>(ctx, nb, V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T, ldt);
+        else bs = launch<8>(ctx, nb, V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T, ldt);
+        finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), bs.first, bs.second, k, K, k + 1 + m, out);
         SBD_LAUNCHED(ctx, "residual_precond");
         return SBD_OK;
     }
@@ -395,7 +862,14 @@ struct GsL {
                    double *out) {
         int nb = red_blocks(ctx, n);
         if (int rc = ensure_red(ctx, nb, K + 1)) return rc;
-        gs_kernel<K><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, ctx->red.as<double>());
+        if (vec_ok(V, ldv, t)) {
+            const int nt = tile_blocks(ctx, n, 512);
+            gs_tile<K><<<nt, kBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, ctx->red.as<double>());
+            finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
+            SBD_LAUNCHED(ctx, "gs_update");
+            return SBD_OK;
+        }
+        gs_kernel<K, false><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, ctx->red.as<double>());
         finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nb, K + 1, kdot, K, kdot + 1, out);
         SBD_LAUNCHED(ctx, "gs_update");
         return SBD_OK;

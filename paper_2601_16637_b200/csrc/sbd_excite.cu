@@ -14,6 +14,8 @@
 // keeps enumeration order, so the count pass and the fill pass produce exactly
 // the reference's entry order; targets are mapped back to caller indices
 // through the sort permutation.
+#include <algorithm>
+
 #include "sbd_internal.cuh"
 
 namespace {
@@ -198,7 +200,8 @@ __global__ void coeff_kernel(const u64 *__restrict__ str, i64 n, int norb, const
                              const int16_t *__restrict__ d_h1, const int16_t *__restrict__ d_h2,
                              const int16_t *__restrict__ d_p1, const int16_t *__restrict__ d_p2,
                              const int8_t *__restrict__ d_phase, int64_t *__restrict__ conn_off,
-                             Conn *__restrict__ conn, SConn *__restrict__ sconn, double *__restrict__ energy) {
+                             Conn *__restrict__ conn, SConn *__restrict__ sconn, int32_t *__restrict__ s_row,
+                             double *__restrict__ energy) {
     i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const u64 s = str[i];
@@ -223,6 +226,7 @@ __global__ void coeff_kernel(const u64 *__restrict__ str, i64 n, int norb, const
         sc.tgt = s_tgt[k];
         sc.info = ph * (P + 1);
         sconn[k] = sc;
+        s_row[k] = (int32_t)i;
     }
     for (i64 k = d_off[i]; k < d_off[i + 1]; ++k, ++o) {
         int p = d_h1[k], q = d_h2[k], r = d_p1[k], t = d_p2[k];
@@ -256,6 +260,23 @@ __global__ void jtable_kernel(const u64 *__restrict__ str, i64 n, i64 npair, con
         acc = __dadd_rn(acc, __ldg(eri + tri_idx(P, tri_idx(q, q))));
     }
     J[P * n + i] = acc;
+}
+
+// Slot-major ELL of the singles: ell[slot * ld + i] for slot < count(i), then empty.
+__global__ void ell_kernel(i64 n, const int64_t *__restrict__ s_off, const SConn *__restrict__ sconn, int w, i64 ld,
+                           uint32_t *__restrict__ ell) {
+    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ld) return;
+    const i64 m0 = i < n ? s_off[i] : 0, cnt = i < n ? s_off[i + 1] - m0 : 0;
+    for (int s = 0; s < w; ++s) {
+        uint32_t v = kEllEmpty;
+        if (s < cnt) {
+            const SConn e = sconn[m0 + s];
+            const uint32_t P = (uint32_t)(abs(e.info) - 1);
+            v = ((uint32_t)e.tgt << (kEllPairBits + 1)) | (P << 1) | (e.info < 0 ? 1u : 0u);
+        }
+        ell[s * ld + i] = v;
+    }
 }
 
 }  // namespace
@@ -322,6 +343,7 @@ int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other) {
     SBD_CUDA(ctx, s.conn_off.ensure(sizeof(int64_t) * (n + 1)));
     SBD_CUDA(ctx, s.conn.ensure(sizeof(Conn) * (s.ns + s.nd + 1)));
     SBD_CUDA(ctx, s.sconn.ensure(sizeof(SConn) * (s.ns + 1)));
+    SBD_CUDA(ctx, s.s_row.ensure(sizeof(int32_t) * (s.ns + 1)));
     SBD_CUDA(ctx, s.energy.ensure(sizeof(double) * (n + 1)));
     SBD_CUDA(ctx, s.J.ensure(sizeof(double) * (ctx->npair * n + 1)));
     if (n == 0) {
@@ -333,10 +355,26 @@ int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other) {
         s.s_tgt.as<int32_t>(), s.s_hole.as<int16_t>(), s.s_part.as<int16_t>(), s.s_phase.as<int8_t>(),
         s.d_off.as<int64_t>(), s.d_tgt.as<int32_t>(), s.d_h1.as<int16_t>(), s.d_h2.as<int16_t>(),
         s.d_p1.as<int16_t>(), s.d_p2.as<int16_t>(), s.d_phase.as<int8_t>(), s.conn_off.as<int64_t>(),
-        s.conn.as<Conn>(), s.sconn.as<SConn>(), s.energy.as<double>());
+        s.conn.as<Conn>(), s.sconn.as<SConn>(), s.s_row.as<int32_t>(), s.energy.as<double>());
     SBD_LAUNCHED(ctx, "coefficients");
     dim3 g(grid_for(n, 128), (unsigned)ctx->npair);
     jtable_kernel<<<g, 128, 0, st>>>(s.str.as<u64>(), n, ctx->npair, ctx->eri.as<double>(), s.J.as<double>());
     SBD_LAUNCHED(ctx, "jtable");
+    // ELL of the singles for the opposite-spin (task 0) kernel
+    std::vector<int64_t> off(n + 1);
+    SBD_CUDA(ctx, cudaMemcpyAsync(off.data(), s.s_off.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+    SBD_CUDA(ctx, cudaStreamSynchronize(st));
+    int w = 0;
+    for (i64 i = 0; i < n; ++i) w = std::max<int>(w, (int)(off[i + 1] - off[i]));
+    if (n >= kEllMaxStrings || ctx->npair >= ((i64)1 << kEllPairBits))
+        return sbd_fail(ctx, SBD_EINVAL, "sector too large for the packed single-excitation table");
+    s.ell_w = w;
+    s.ell_ld = (n + 3) / 4 * 4;
+    SBD_CUDA(ctx, s.ell.ensure(sizeof(uint32_t) * ((size_t)std::max(w, 1) * s.ell_ld + 4)));
+    if (w > 0) {
+        ell_kernel<<<grid_for(s.ell_ld, 256), 256, 0, st>>>(n, s.s_off.as<int64_t>(), s.sconn.as<SConn>(), w, s.ell_ld,
+                                                            s.ell.as<uint32_t>());
+        SBD_LAUNCHED(ctx, "ell");
+    }
     return SBD_OK;
 }

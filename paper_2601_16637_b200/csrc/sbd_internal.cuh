@@ -52,8 +52,12 @@ struct Sector {
     // kernel-ready
     DevBuf conn_off, conn;   // i64[n+1], Conn[ns+nd]
     DevBuf sconn;            // SConn[ns] (offsets = s_off)
+    DevBuf s_row;            // int32[ns]: source string of each single
     DevBuf energy;           // f64[n]: same-spin diagonal energy per string
     DevBuf J;                // f64[npair][n]: J[P][i] = sum_{q in string i} (P|qq)
+    DevBuf ell;              // u32[ell_w][ell_ld]: singles, slot-major, packed (tgt<<13 | P<<1 | neg)
+    int ell_w = 0;
+    i64 ell_ld = 0;
     bool built = false;
 };
 
@@ -66,6 +70,8 @@ struct sbd_ctx {
     double e_core = 0.0;
     bool have_integrals = false;
     DevBuf h, eri, dpq;  // h[norb*norb], eri, dpq[norb*norb] = (pp|qq)
+    DevBuf vpp;          // vpp[P * ld_vpp + Q] = (P|Q) over orbital pairs (rows 16-byte aligned)
+    i64 ld_vpp = 0;
     Sector sec[2];
     i64 row_lo = 0, row_hi = -1;  // owned alpha rows (row_hi < 0: all)
     // scratch for sigma
@@ -109,6 +115,10 @@ int sbd_cuda_fail(sbd_ctx *ctx, cudaError_t e, const char *where);
 int sbd_sort_strings(sbd_ctx *ctx, Sector &s);              // sbd_strings.cu
 int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s);       // sbd_excite.cu
 int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other);  // sbd_excite.cu
+
+constexpr uint32_t kEllEmpty = 0xFFFFFFFFu;
+constexpr int kEllPairBits = 12;   // orbital pair index < 4096 (norb <= 64 gives 2080)
+constexpr i64 kEllMaxStrings = (i64)1 << 19;
 
 __host__ __device__ inline i64 tri_idx(i64 a, i64 b) {
     return a >= b ? a * (a + 1) / 2 + b : b * (b + 1) / 2 + a;

@@ -24,6 +24,7 @@
 #include <algorithm>
 
 #include "sbd_internal.cuh"
+#include "sbd_ptx.cuh"
 
 namespace {
 
@@ -45,11 +46,7 @@ struct SideArgs {
     const double *diag;            // [n_rows][ldy]
     const double *YT;              // beta-side result, [n_cols][ldyt]
     i64 ldyt;
-    const int64_t *s_off_self;     // alpha singles of the row (global row index)
-    const SConn *sconn_self;
-    const int64_t *s_off_other;    // beta singles of the column
-    const SConn *sconn_other;
-    const double *eri;
+    const int64_t *a_s_off;        // rows with alpha singles carry task 0 in Y (cross_kernel)
 };
 
 template <bool VEC>
@@ -57,14 +54,15 @@ __device__ __forceinline__ i64 lane_col(i64 c0, int lane, int j) {
     return VEC ? c0 + (j >> 1) * 64 + 2 * lane + (j & 1) : c0 + j * 32 + lane;
 }
 
-template <bool VEC>
+template <bool VEC, bool RO = true>
 __device__ __forceinline__ void load4(const double *__restrict__ row, i64 c0, int lane, const bool (&ok)[4],
                                       double (&v)[4]) {
     if (VEC) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             if (ok[2 * h]) {
-                double2 t = __ldg(reinterpret_cast<const double2 *>(row + c0 + h * 64 + 2 * lane));
+                const double2 *pp = reinterpret_cast<const double2 *>(row + c0 + h * 64 + 2 * lane);
+                double2 t = RO ? __ldg(pp) : *pp;
                 v[2 * h] = t.x;
                 v[2 * h + 1] = t.y;
             } else {
@@ -73,7 +71,7 @@ __device__ __forceinline__ void load4(const double *__restrict__ row, i64 c0, in
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = ok[j] ? __ldg(row + c0 + j * 32 + lane) : 0.0;
+        for (int j = 0; j < 4; ++j) v[j] = ok[j] ? (RO ? __ldg(row + c0 + j * 32 + lane) : row[c0 + j * 32 + lane]) : 0.0;
     }
 }
 
@@ -135,37 +133,6 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
                 }
             }
         }
-        if (ALPHA) {
-            // diagonal term (apply.py:217)
-            double dv[4], xo[4];
-            load4<VEC>(a.diag + r * a.ldy, c0, lane, ok, dv);
-            load4<VEC>(a.X + g * a.ldx, c0, lane, ok, xo);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[j] = fma(dv[j], xo[j], acc[j]);
-            // task 0: alpha single x beta single (apply.py:235-238):
-            //   s_a s_b (pa ra | pb rb) X[ja, jb]
-            const i64 k0 = a.s_off_self[g], k1 = a.s_off_self[g + 1];
-            for (i64 k = k0; k < k1; ++k) {
-                const SConn sa = a.sconn_self[k];
-                const int Pa = abs(sa.info) - 1;
-                const double sga = sa.info > 0 ? 1.0 : -1.0;
-                const double *xr = a.X + (i64)sa.tgt * a.ldx;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (!ok[j]) continue;
-                    const i64 ib = lane_col<VEC>(c0, lane, j);
-                    const i64 m0 = a.s_off_other[ib], m1 = a.s_off_other[ib + 1];
-                    double t = 0.0;
-                    for (i64 m = m0; m < m1; ++m) {
-                        const SConn sb = a.sconn_other[m];
-                        const int Pb = abs(sb.info) - 1;
-                        const double v = __ldg(a.eri + tri_idx(Pa, Pb));
-                        t = fma(sb.info > 0 ? v : -v, __ldg(xr + sb.tgt), t);
-                    }
-                    acc[j] = fma(sga, t, acc[j]);
-                }
-            }
-        }
     }
 
     if (ALPHA) {
@@ -189,6 +156,22 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
             const i64 lc = lane_col<VEC>(c0, lane, j) - c0;
             if (row_ok && ok[j]) acc[j] += tile[lc][w];
         }
+        if (row_ok) {
+            const i64 g = a.row_base + r;
+            // diagonal term (apply.py:217)
+            double dv[4], xo[4];
+            load4<VEC>(a.diag + r * a.ldy, c0, lane, ok, dv);
+            load4<VEC>(a.X + g * a.ldx, c0, lane, ok, xo);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] = fma(dv[j], xo[j], acc[j]);
+            // task 0, already in Y for rows with alpha singles (cross_kernel)
+            if (a.a_s_off[g + 1] != a.a_s_off[g]) {
+                double pv[4];
+                load4<VEC, false>(a.Y + r * a.ldy, c0, lane, ok, pv);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[j] += pv[j];
+            }
+        }
     }
 
     if (row_ok) {
@@ -208,6 +191,124 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
             for (int j = 0; j < 4; ++j)
                 if (ok[j]) yr[c0 + j * 32 + lane] = acc[j];
         }
+    }
+}
+
+// Task 0, the alpha-single x beta-single opposite-spin doubles (apply.py:235-238):
+//   Y[r, ib] = sum_{k in aS(g)} s_k sum_{m in bS(ib)} s_m (Pa_k | Pb_m) X[ja_k, jb_m]
+// written for rows that have alpha singles (the streaming kernel adds it).
+//
+// Work list: the flat list of alpha-single entries of the owned rows, split
+// over CTAs at row boundaries (a row's entries stay in one CTA, so its Y row
+// is read-modify-written by one thread per column, no atomics).  For each
+// entry the gathers X[ja_k, jb] hit arbitrary columns of row ja_k: the whole
+// row and the pair-pair ERI row (Pa_k | *) are brought into shared memory by
+// TMA bulk copies (cp.async.bulk + mbarrier), double-buffered so entry e+1's
+// copy overlaps entry e's gathers.  The beta singles come from a slot-major
+// packed ELL table: each thread owns 4 consecutive columns and reads one
+// 128-bit word per slot.
+constexpr int kCrossThreads = 512;
+
+__device__ __forceinline__ i64 snap_entry(i64 t, i64 e_end, const int64_t *__restrict__ a_s_off,
+                                          const int32_t *__restrict__ a_row) {
+    if (t >= e_end) return e_end;
+    const i64 g = a_row[t];
+    return t == a_s_off[g] ? t : a_s_off[g + 1];
+}
+
+template <bool STAGED>
+__device__ __forceinline__ void cross_entry(const double *xrow, const double *vrow, double sga, bool first, double *yr,
+                                            i64 nb, const uint32_t *__restrict__ ell, int ell_w, i64 ell_ld) {
+    for (i64 ib = (i64)threadIdx.x * 4; ib < nb; ib += (i64)blockDim.x * 4) {
+        double acc[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = (first || ib + j >= nb) ? 0.0 : yr[ib + j];
+        for (int slot0 = 0; slot0 < ell_w; slot0 += 4) {
+            uint4 e4[4];
+            bool any = false;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                e4[s] = slot0 + s < ell_w ? __ldg(reinterpret_cast<const uint4 *>(ell + (i64)(slot0 + s) * ell_ld + ib))
+                                          : make_uint4(kEllEmpty, kEllEmpty, kEllEmpty, kEllEmpty);
+            }
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                const uint32_t ev[4] = {e4[s].x, e4[s].y, e4[s].z, e4[s].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t e = ev[j];
+                    if (e == kEllEmpty) continue;
+                    any = true;
+                    const i64 jb = (i64)(e >> (kEllPairBits + 1));
+                    const int Pb = (int)((e >> 1) & ((1u << kEllPairBits) - 1));
+                    const double v = STAGED ? vrow[Pb] : __ldg(vrow + Pb);
+                    const double x = STAGED ? xrow[jb] : __ldg(xrow + jb);
+                    const double t = sga * v * x;
+                    acc[j] = (e & 1u) ? acc[j] - t : acc[j] + t;
+                }
+            }
+            if (!any) break;  // slots fill in order: an all-empty group ends the row
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (ib + j < nb) yr[ib + j] = acc[j];
+    }
+}
+
+template <bool STAGED>
+__global__ void __launch_bounds__(kCrossThreads)
+cross_kernel(i64 n_rows, i64 row_base, i64 nb, const double *__restrict__ X, double *__restrict__ Y,
+             const int64_t *__restrict__ a_s_off, const SConn *__restrict__ a_sconn, const int32_t *__restrict__ a_row,
+             const uint32_t *__restrict__ ell, int ell_w, i64 ell_ld, const double *__restrict__ vpp, i64 ld_vpp) {
+    extern __shared__ __align__(128) unsigned char csm[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(csm);
+    double *xs0 = reinterpret_cast<double *>(csm + 128);
+    const i64 stage = nb + ld_vpp;  // doubles per stage: X row then ERI row
+    const i64 E0 = a_s_off[row_base], E1 = a_s_off[row_base + n_rows];
+    const i64 tot = E1 - E0;
+    const i64 e0 = snap_entry(E0 + tot * blockIdx.x / gridDim.x, E1, a_s_off, a_row);
+    const i64 e1 = snap_entry(E0 + tot * (blockIdx.x + 1) / gridDim.x, E1, a_s_off, a_row);
+    if (e0 >= e1) return;
+    if (!STAGED) {
+        for (i64 e = e0; e < e1; ++e) {
+            const SConn sa = a_sconn[e];
+            const i64 g = a_row[e];
+            const double sga = sa.info > 0 ? 1.0 : -1.0;
+            cross_entry<false>(X + (i64)sa.tgt * nb, vpp + (i64)(abs(sa.info) - 1) * ld_vpp, sga, e == a_s_off[g],
+                               Y + (g - row_base) * nb, nb, ell, ell_w, ell_ld);
+            __syncthreads();
+        }
+        return;
+    }
+    const uint32_t bx = (uint32_t)(nb * sizeof(double)), bv = (uint32_t)(ld_vpp * sizeof(double));
+    auto issue = [&](i64 e, int s) {
+        const SConn sa = a_sconn[e];
+        double *dst = xs0 + s * stage;
+        mbar_arrive_expect_tx(&bar[s], bx + bv);
+        tma_load_1d(dst, X + (i64)sa.tgt * nb, bx, &bar[s]);
+        tma_load_1d(dst + nb, vpp + (i64)(abs(sa.info) - 1) * ld_vpp, bv, &bar[s]);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        issue(e0, 0);
+        if (e0 + 1 < e1) issue(e0 + 1, 1);
+    }
+    int it = 0;
+    for (i64 e = e0; e < e1; ++e, ++it) {
+        const int s = it & 1;
+        mbar_wait(&bar[s], (uint32_t)((it >> 1) & 1));
+        const SConn sa = a_sconn[e];
+        const i64 g = a_row[e];
+        const double *xr = xs0 + s * stage;
+        cross_entry<true>(xr, xr + nb, sa.info > 0 ? 1.0 : -1.0, e == a_s_off[g], Y + (g - row_base) * nb, nb, ell,
+                          ell_w, ell_ld);
+        __syncthreads();  // stage s fully consumed
+        if (threadIdx.x == 0 && e + 2 < e1) issue(e + 2, s);
     }
 }
 
@@ -354,14 +455,31 @@ int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full, double *y) {
     a.conn = A.conn.as<Conn>();
     a.J = B.J.as<double>();
     a.ldj = nb;
-    a.diag = ctx->diag.as<double>();
     a.YT = ctx->yt.as<double>();
     a.ldyt = ctx->ld_t;
-    a.s_off_self = A.s_off.as<int64_t>();
-    a.sconn_self = A.sconn.as<SConn>();
-    a.s_off_other = B.s_off.as<int64_t>();
-    a.sconn_other = B.sconn.as<SConn>();
-    a.eri = ctx->eri.as<double>();
+    a.diag = ctx->diag.as<double>();
+    a.a_s_off = A.s_off.as<int64_t>();
+    if (A.ns > 0 && B.ns > 0) {
+        const size_t smem = 128 + sizeof(double) * 2 * (size_t)(nb + ctx->ld_vpp);
+        const bool staged = (nb % 2 == 0) && aligned16(x_full) && smem <= 220 * 1024;
+        const unsigned grid = (unsigned)ctx->num_sms;
+        if (staged) {
+            static size_t smem_set = 0;
+            if (smem > smem_set) {
+                SBD_CUDA(ctx, cudaFuncSetAttribute(cross_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)smem));
+                smem_set = smem;
+            }
+            cross_kernel<true><<<grid, kCrossThreads, smem, ctx->stream>>>(
+                rows, ctx->own_lo(), nb, x_full, y, A.s_off.as<int64_t>(), A.sconn.as<SConn>(),
+                A.s_row.as<int32_t>(), B.ell.as<uint32_t>(), B.ell_w, B.ell_ld, ctx->vpp.as<double>(), ctx->ld_vpp);
+        } else {
+            cross_kernel<false><<<grid * 2, kCrossThreads, 0, ctx->stream>>>(
+                rows, ctx->own_lo(), nb, x_full, y, A.s_off.as<int64_t>(), A.sconn.as<SConn>(),
+                A.s_row.as<int32_t>(), B.ell.as<uint32_t>(), B.ell_w, B.ell_ld, ctx->vpp.as<double>(), ctx->ld_vpp);
+        }
+        SBD_LAUNCHED(ctx, "cross_kernel");
+    }
     dim3 g((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kColsPerWarp - 1) / kColsPerWarp));
     const bool vec = (nb % 2 == 0) && aligned16(x_full) && aligned16(y);
     if (vec) side_kernel<true, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);

@@ -56,6 +56,8 @@ class DavidsonOptions:
     # B200 extension: record ||V V^T - I||_F per iteration from the Gram row
     # fused into the V^T w pass (no extra pass over V).
     track_orthogonality: bool = True
+    # B200 extension: per-phase CUDA-event timing in stats.phase_ms (tracing)
+    profile: bool = False
 
     def __post_init__(self):
         if not 1 <= self.n_roots <= self.restart_keep <= self.max_subspace:
@@ -88,6 +90,7 @@ class DavidsonStats:
     apply_seconds: list = field(default_factory=list)
     restart_iters: list = field(default_factory=list)
     iter_seconds: list = field(default_factory=list)  # B200 extension: wall time per iteration
+    phase_ms: dict = field(default_factory=dict)  # B200 extension: summed device time per phase
 
 
 @dataclass
@@ -105,13 +108,48 @@ class DavidsonResult:
 class _Engine:
     """Kernel launcher bound to one device (any context can drive the vector kernels)."""
 
-    def __init__(self, device: int, ctx: Optional[_lib.Context] = None):
+    def __init__(self, device: int, ctx: Optional[_lib.Context] = None, profile: bool = False):
         self.ctx = ctx if ctx is not None else _lib.Context(device)
         self.own_ctx = ctx is None
+        self.profile = profile
+        self._events = []  # (name, start, end)
 
     def __call__(self, name, *args):
         self.ctx.bind_stream()
-        self.ctx(name, *args)
+        if self.profile:
+            with self.phase(name):
+                self.ctx(name, *args)
+        else:
+            self.ctx(name, *args)
+
+    def phase(self, name):
+        import contextlib
+
+        import torch
+
+        if not self.profile:
+            return contextlib.nullcontext()
+        eng = self
+
+        class _P:
+            def __enter__(self):
+                self.s = torch.cuda.Event(enable_timing=True)
+                self.e = torch.cuda.Event(enable_timing=True)
+                self.s.record()
+
+            def __exit__(self, *exc):
+                self.e.record()
+                eng._events.append((name, self.s, self.e))
+        return _P()
+
+    def summary(self) -> dict:
+        import torch
+
+        torch.cuda.synchronize()
+        out = {}
+        for name, s, e in self._events:
+            out[name] = out.get(name, 0.0) + s.elapsed_time(e)
+        return out
 
 
 def _p(t):
@@ -244,7 +282,7 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
         ctx = ctx if ctx is not None else op_ctx
     else:
         apply_fn = apply_h
-    eng = _Engine(dev.index, ctx)
+    eng = _Engine(dev.index, ctx, profile=opts.profile)
     reduce = allreduce if allreduce is not None else (lambda t: None)
 
     m = opts.n_roots
@@ -253,10 +291,12 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
     stats = DavidsonStats()
     rng = np.random.default_rng(0x5BD1A6)
 
-    V = torch.empty((k_max, n_loc), **f64)
-    W = torch.empty((k_max, n_loc), **f64)
-    Tv = torch.empty((m, n_loc), **f64)           # preconditioned residuals (one per root)
-    ld = n_loc
+    # leading dimension padded to a multiple of 32 doubles: 16-byte aligned rows
+    # for the 128-bit tile kernels; vectors are the [:n_loc] views
+    ld = max(32, (n_loc + 31) // 32 * 32)
+    V = torch.zeros((k_max, ld), **f64)[:, :n_loc]
+    W = torch.zeros((k_max, ld), **f64)[:, :n_loc]
+    Tv = torch.zeros((m, ld), **f64)[:, :n_loc]   # preconditioned residuals (one per root)
     small = torch.zeros(2 * 64 + 16, **f64)       # device scratch for dot products
     scale = torch.zeros(1, **f64)
 
@@ -302,7 +342,8 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
         stats.iterations = iteration
         # image of the newest direction (davidson.py:241-245)
         tic = time.perf_counter()
-        apply_fn(V[k - 1], W[k - 1])
+        with eng.phase("sigma"):
+            apply_fn(V[k - 1], W[k - 1])
         torch.cuda.current_stream(dev).synchronize()
         stats.apply_seconds.append(time.perf_counter() - tic)
         stats.n_applies += 1
@@ -417,7 +458,10 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
     Y_dev[: kk * mk].copy_(torch.from_numpy(np.ascontiguousarray(Yr).reshape(-1)))
     U = torch.empty((mk, n_loc), **f64)
     eng("sbd_combine", _p(V), kk, ld, n_loc, _p(Y_dev), mk, _p(U), n_loc)
+    del V, W, Tv
     torch.cuda.current_stream(dev).synchronize()
+    if opts.profile:
+        stats.phase_ms = eng.summary()
     vectors = U if return_device else U.cpu().numpy()
     if eng.own_ctx:
         eng.ctx.close()

@@ -1,0 +1,34 @@
+"""Per-phase device time of the Davidson driver at the bench workload (tracing aid)."""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main(iters: int = 40):
+    import torch
+
+    import bench
+    from paper_2601_16637_b200 import DavidsonOptions, HamiltonianApplier, SelectedBasis, davidson_solve
+
+    table, a, b = bench._instance()
+    app = HamiltonianApplier(SelectedBasis.product(a.tolist(), b.tolist(), 26, 7, 7), table)
+    opts = DavidsonOptions(max_iters=iters, profile=True)
+    t0 = time.perf_counter()
+    res = davidson_solve(app, app.diag_device, opts=opts, return_device=True)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    it = res.stats.iterations
+    ph = {k: v / it for k, v in sorted(res.stats.phase_ms.items(), key=lambda kv: -kv[1])}
+    out = {"iterations": it, "wall_ms_per_iter": wall * 1e3 / it, "device_ms_per_iter_by_phase": ph,
+           "device_ms_per_iter_total": sum(ph.values())}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 40)
