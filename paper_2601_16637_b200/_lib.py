@@ -48,6 +48,7 @@ _SIGS = {
                                     _c_dbl, _vp, _c_i64, _vp],
     "sbd_gs_update": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _vp, _vp],
     "sbd_gs_update_nodots": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _vp, _vp],
+    "sbd_gs_finalize": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp],
     "sbd_scale_copy": [_vp, _vp, _vp, _c_i64, _vp],
     "sbd_rotate": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _c_int],
     "sbd_combine": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _c_int, _vp, _c_i64],

@@ -16,9 +16,11 @@
 //   sbd_rotate           thick restart V <- V Y_keep in place       (davidson.py:280-289)
 //   sbd_jacobi           projected k x k eigensolve, one warp       (davidson.py:86-148)
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 
 #include "sbd_internal.cuh"
+#include "sbd_ptx.cuh"
 
 namespace {
 
@@ -609,6 +611,253 @@ residual_tile(const double *__restrict__ V, const double *__restrict__ W, int k,
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-pipelined kernels (aligned fast path for the multi-phase passes).
+// A CTA owns a strided set of tiles of TT elements.  For each tile one thread
+// issues 1-D bulk copies (cp.async.bulk) of every vector slice the tile
+// needs into a shared-memory stage, counted on that stage's mbarrier; two
+// stages alternate, so tile i+1 streams in from HBM while tile i is computed
+// entirely out of shared memory (no second global touch, no register
+// staging).  Stage size is ~64 KB, i.e. TT = 8192 / (#vectors per tile).
+
+struct TmaPipe {
+    uint64_t *bar;  // [2]
+    __device__ void init() {
+        if (threadIdx.x == 0) {
+            mbar_init(&bar[0], 1);
+            mbar_init(&bar[1], 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
+    }
+};
+
+// copy `cnt` doubles starting at src (16-B aligned) to dst; the odd last
+// element (if any) is loaded by plain loads later -- returns bytes issued
+__device__ __forceinline__ uint32_t bulk_bytes(i64 cnt) { return (uint32_t)((cnt & ~(i64)1) * 8); }
+
+// t_new = t - V c ; out = scale * t_new (out may alias t) ; dots V_i.t_new (i<kdot) ; |t_new|^2
+template <int K>
+__global__ void __launch_bounds__(kBlock)
+gs_tma(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__restrict__ c, int kdot,
+       const double *t, double *out, const double *__restrict__ scale, double *__restrict__ partial) {
+    constexpr int TT = 8192 / (K + 1), KW = (K + kWarpsT - 1) / kWarpsT;
+    constexpr int TTA = TT & ~1;  // keep tiles an even number of elements
+    extern __shared__ __align__(128) unsigned char gsm[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(gsm);
+    double *stage0 = reinterpret_cast<double *>(gsm + 128);
+    const i64 sstride = (i64)(K + 1) * TTA;  // doubles per stage: k V slices + t slice
+    __shared__ double cs[K];
+    __shared__ double nrm[kWarpsT];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) cs[i] = c[i];
+    const double sc = scale ? *scale : 1.0;
+    TmaPipe pipe{bar};
+    pipe.init();
+    const i64 ntiles = (n + TTA - 1) / TTA;
+    auto issue = [&](i64 tile, int s) {
+        const i64 base = tile * TTA, cnt = min((i64)TTA, n - base);
+        const uint32_t b = bulk_bytes(cnt);
+        double *st = stage0 + s * sstride;
+        if (b) {
+            mbar_arrive_expect_tx(&bar[s], b * (uint32_t)(k + 1));
+            for (int i = 0; i < k; ++i) tma_load_1d(st + (i64)i * TTA, V + i * ldv + base, b, &bar[s]);
+            tma_load_1d(st + (i64)K * TTA, t + base, b, &bar[s]);
+        } else {
+            mbar_arrive_expect_tx(&bar[s], 0);
+        }
+    };
+    double acc[KW];
+#pragma unroll
+    for (int a = 0; a < KW; ++a) acc[a] = 0.0;
+    double n2 = 0.0;
+    i64 tile = blockIdx.x;
+    if (threadIdx.x == 0) {
+        if (tile < ntiles) issue(tile, 0);
+        if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);
+    }
+    for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+        const int s = it & 1;
+        const i64 base = tile * TTA, cnt = min((i64)TTA, n - base);
+        double *st = stage0 + s * sstride;
+        mbar_wait(&bar[s], (uint32_t)((it >> 1) & 1));
+        if (cnt & 1) {  // odd tail element: plain loads
+            const i64 e = cnt - 1;
+            if (threadIdx.x == 0) {
+                for (int i = 0; i < k; ++i) st[(i64)i * TTA + e] = V[i * ldv + base + e];
+                st[(i64)K * TTA + e] = t[base + e];
+            }
+            __syncthreads();
+        }
+        double *ts = st + (i64)K * TTA;
+        for (i64 e = threadIdx.x; e < cnt; e += blockDim.x) {
+            double v = ts[e];
+            for (int i = 0; i < k; ++i) v = fma(-cs[i], st[(i64)i * TTA + e], v);
+            ts[e] = v;
+            out[base + e] = v * sc;
+            n2 = fma(v, v, n2);
+        }
+        __syncthreads();
+        if (kdot > 0) {
+#pragma unroll
+            for (int a = 0; a < KW; ++a) {
+                const int i = warp + kWarpsT * a;
+                if (i < kdot) {
+                    const double *vi = st + (i64)i * TTA;
+                    double sacc = 0.0;
+                    for (i64 e = lane; e < cnt; e += 32) sacc = fma(vi[e], ts[e], sacc);
+                    acc[a] += sacc;
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && tile + 2 * gridDim.x < ntiles) issue(tile + 2 * gridDim.x, s);
+    }
+    n2 = warp_sum(n2);
+    if (lane == 0) nrm[warp] = n2;
+#pragma unroll
+    for (int a = 0; a < KW; ++a) {
+        const int i = warp + kWarpsT * a;
+        const double sa = warp_sum(acc[a]);
+        if (lane == 0 && i < K) partial[(i64)blockIdx.x * (K + 1) + i] = i < kdot ? sa : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        for (int ww = 0; ww < kWarpsT; ++ww) sum += nrm[ww];
+        partial[(i64)blockIdx.x * (K + 1) + K] = sum;
+    }
+}
+
+// Ritz residual + preconditioner + projections, TMA-fed (stage: k V + k W + diag slices)
+template <int K, int M>
+__global__ void __launch_bounds__(kBlock)
+residual_tma(const double *__restrict__ V, const double *__restrict__ W, int k, i64 ldv, i64 n,
+             const double *__restrict__ Y, const double *__restrict__ theta, int m, int jp,
+             const double *__restrict__ diag, double delta, double *__restrict__ T, i64 ldt,
+             double *__restrict__ partial) {
+    constexpr int TT0 = 8192 / (2 * K + 1), TTA = TT0 & ~1, KW = (K + kWarpsT - 1) / kWarpsT;
+    extern __shared__ __align__(128) unsigned char rsm2[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(rsm2);
+    double *stage0 = reinterpret_cast<double *>(rsm2 + 128);
+    const i64 sstride = (i64)(2 * K + 1) * TTA;
+    double *ts = stage0 + 2 * sstride;  // [TTA]: the target root's correction
+    __shared__ double ys[64 * 8];
+    __shared__ double th[8];
+    __shared__ double red[kWarpsT][M + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < k * m; i += blockDim.x) ys[i] = Y[i];
+    if (threadIdx.x < m) th[threadIdx.x] = theta[threadIdx.x];
+    TmaPipe pipe{bar};
+    pipe.init();
+    const i64 ntiles = (n + TTA - 1) / TTA;
+    auto issue = [&](i64 tile, int s) {
+        const i64 base = tile * TTA, cnt = min((i64)TTA, n - base);
+        const uint32_t b = bulk_bytes(cnt);
+        double *st = stage0 + s * sstride;
+        if (b) {
+            mbar_arrive_expect_tx(&bar[s], b * (uint32_t)(2 * k + 1));
+            for (int i = 0; i < k; ++i) {
+                tma_load_1d(st + (i64)i * TTA, V + i * ldv + base, b, &bar[s]);
+                tma_load_1d(st + (i64)(K + i) * TTA, W + i * ldv + base, b, &bar[s]);
+            }
+            tma_load_1d(st + (i64)(2 * K) * TTA, diag + base, b, &bar[s]);
+        } else {
+            mbar_arrive_expect_tx(&bar[s], 0);
+        }
+    };
+    double acc[KW];
+#pragma unroll
+    for (int a = 0; a < KW; ++a) acc[a] = 0.0;
+    double rn2[M], tn2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) rn2[j] = 0.0;
+    i64 tile = blockIdx.x;
+    if (threadIdx.x == 0) {
+        if (tile < ntiles) issue(tile, 0);
+        if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, 1);
+    }
+    for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+        const int s = it & 1;
+        const i64 base = tile * TTA, cnt = min((i64)TTA, n - base);
+        double *st = stage0 + s * sstride;
+        mbar_wait(&bar[s], (uint32_t)((it >> 1) & 1));
+        if (cnt & 1) {
+            const i64 e = cnt - 1;
+            if (threadIdx.x == 0) {
+                for (int i = 0; i < k; ++i) {
+                    st[(i64)i * TTA + e] = V[i * ldv + base + e];
+                    st[(i64)(K + i) * TTA + e] = W[i * ldv + base + e];
+                }
+                st[(i64)(2 * K) * TTA + e] = diag[base + e];
+            }
+            __syncthreads();
+        }
+        for (i64 e = threadIdx.x; e < cnt; e += blockDim.x) {
+            double u[M], wy[M];
+#pragma unroll
+            for (int j = 0; j < M; ++j) u[j] = wy[j] = 0.0;
+            for (int i = 0; i < k; ++i) {
+                const double v = st[(i64)i * TTA + e], w = st[(i64)(K + i) * TTA + e];
+#pragma unroll
+                for (int j = 0; j < M; ++j)
+                    if (j < m) {
+                        u[j] = fma(ys[i * m + j], v, u[j]);
+                        wy[j] = fma(ys[i * m + j], w, wy[j]);
+                    }
+            }
+            const double d = st[(i64)(2 * K) * TTA + e];
+            double tj = 0.0;
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+                if (j < m) {
+                    const double r = wy[j] - th[j] * u[j];
+                    rn2[j] = fma(r, r, rn2[j]);
+                    const double g = d - th[j];
+                    const double t = r / ((g >= 0.0 ? 1.0 : -1.0) * fmax(fabs(g), delta));  // davidson.py:159-163
+                    T[j * ldt + base + e] = t;
+                    if (j == jp) tj = t;
+                }
+            }
+            ts[e] = tj;
+            tn2 = fma(tj, tj, tn2);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < KW; ++a) {
+            const int i = warp + kWarpsT * a;
+            if (i < k) {
+                const double *vi = st + (i64)i * TTA;
+                double sacc = 0.0;
+                for (i64 e = lane; e < cnt; e += 32) sacc = fma(vi[e], ts[e], sacc);
+                acc[a] += sacc;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && tile + 2 * gridDim.x < ntiles) issue(tile + 2 * gridDim.x, s);
+    }
+#pragma unroll
+    for (int a = 0; a < KW; ++a) {
+        const int i = warp + kWarpsT * a;
+        const double sa = warp_sum(acc[a]);
+        if (lane == 0 && i < K) partial[(i64)blockIdx.x * (K + 1 + M) + i] = i < k ? sa : 0.0;
+    }
+    tn2 = warp_sum(tn2);
+#pragma unroll
+    for (int j = 0; j < M; ++j) rn2[j] = warp_sum(rn2[j]);
+    if (lane == 0) {
+        red[warp][0] = tn2;
+#pragma unroll
+        for (int j = 0; j < M; ++j) red[warp][1 + j] = rn2[j];
+    }
+    __syncthreads();
+    if (threadIdx.x <= M) {
+        double sum = 0.0;
+        for (int ww = 0; ww < kWarpsT; ++ww) sum += red[ww][threadIdx.x];
+        partial[(i64)blockIdx.x * (K + 1 + M) + K + threadIdx.x] = sum;
+    }
+}
+
 __global__ void scale_copy_kernel(const double *__restrict__ src, double *__restrict__ dst, i64 n,
                                   const double *__restrict__ s) {
     const double f = *s;
@@ -752,6 +1001,15 @@ inline bool vec_ok(const double *V, i64 ldv, const double *p, P... rest) {
     return al16(p) && vec_ok(V, ldv, rest...);
 }
 
+inline bool use_tma() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SBD_NO_TMA");
+        v = (e && *e && *e != '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 int tile_blocks(sbd_ctx *ctx, i64 n, int tt) {
     i64 b = (n + tt - 1) / tt;
     return (int)std::max<i64>(1, std::min<i64>(b, (i64)ctx->num_sms * 8));
@@ -823,6 +1081,19 @@ struct ResidL {
     static std::pair<int, int> launch(sbd_ctx *ctx, int nb, const double *V, const double *W, int k, i64 ldv, i64 n,
                                       const double *Y, const double *theta, int m, int jp, const double *diag,
                                       double delta, double *T, i64 ldt) {
+        if (vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_tma()) {
+            constexpr int TTA = (8192 / (2 * K + 1)) & ~1;
+            const size_t smem = 128 + sizeof(double) * (2 * (size_t)(2 * K + 1) * TTA + TTA);
+            const int nt = std::max(1, std::min<int>((int)((n + TTA - 1) / TTA), ctx->num_sms));
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(residual_tma<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                attr = true;
+            }
+            residual_tma<K, M><<<nt, kBlock, smem, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T,
+                                                                 ldt, ctx->red.as<double>());
+            return {nt, K + 1 + M};
+        }
         if (vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0) {
             constexpr int TT = 512 / M;
             const int nt = tile_blocks(ctx, n, TT);
@@ -859,18 +1130,34 @@ struct ResidL {
 template <int K>
 struct GsL {
     static int run(sbd_ctx *ctx, const double *V, int k, i64 ldv, i64 n, const double *c, int kdot, double *t,
-                   double *out) {
+                   double *out, double *out_vec = nullptr, const double *scale = nullptr) {
         int nb = red_blocks(ctx, n);
         if (int rc = ensure_red(ctx, nb, K + 1)) return rc;
-        if (vec_ok(V, ldv, t)) {
-            const int nt = tile_blocks(ctx, n, 512);
-            gs_tile<K><<<nt, kBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, ctx->red.as<double>());
+        double *dst = out_vec ? out_vec : t;
+        if (vec_ok(V, ldv, t) && use_tma()) {
+            constexpr int TTA = (8192 / (K + 1)) & ~1;
+            const size_t smem = 128 + sizeof(double) * 2 * (size_t)(K + 1) * TTA;
+            const int nt = std::max(1, std::min<int>((int)((n + TTA - 1) / TTA), ctx->num_sms));
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(gs_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                attr = true;
+            }
+            gs_tma<K><<<nt, kBlock, smem, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale, ctx->red.as<double>());
             finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
             SBD_LAUNCHED(ctx, "gs_update");
             return SBD_OK;
         }
-        gs_kernel<K, false><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, ctx->red.as<double>());
-        finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nb, K + 1, kdot, K, kdot + 1, out);
+        // non-TMA paths update t in place (the finalize form may clobber t), then scale into out_vec
+        if (vec_ok(V, ldv, t)) {
+            const int nt = tile_blocks(ctx, n, 512);
+            gs_tile<K><<<nt, kBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, ctx->red.as<double>());
+            finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
+        } else {
+            gs_kernel<K, false><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, ctx->red.as<double>());
+            finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nb, K + 1, kdot, K, kdot + 1, out);
+        }
+        if (out_vec) scale_copy_kernel<<<nb * 2, kBlock, 0, ctx->stream>>>(t, out_vec, n, scale);
         SBD_LAUNCHED(ctx, "gs_update");
         return SBD_OK;
     }
@@ -943,11 +1230,16 @@ int sbd_gs_update(sbd_ctx *ctx, const double *V, int k, int64_t ldv, int64_t n, 
                   double *out2) {
     SBD_CHECK_CTX(ctx);
     if (int rc = check_k(ctx, k)) return rc;
-    if (k == 0) {
-        // only |t|^2
-        return GsL<8>::run(ctx, V, 0, (i64)ldv, (i64)n, c, 0, t, out2);
-    }
-    return dispatch_k<GsL>(k, ctx, V, k, (i64)ldv, (i64)n, c, k, t, out2);
+    if (k == 0) return GsL<8>::run(ctx, V, 0, (i64)ldv, (i64)n, c, 0, t, out2);
+    return dispatch_k<GsL>(k, ctx, V, k, (i64)ldv, (i64)n, c, k, t, out2, (double *)nullptr, (const double *)nullptr);
+}
+
+int sbd_gs_finalize(sbd_ctx *ctx, const double *V, int k, int64_t ldv, int64_t n, const double *c, const double *t,
+                    double *v_out, const double *scale, double *out_norm2) {
+    SBD_CHECK_CTX(ctx);
+    if (int rc = check_k(ctx, k)) return rc;
+    if (k == 0) return GsL<8>::run(ctx, V, 0, (i64)ldv, (i64)n, c, 0, const_cast<double *>(t), out_norm2, v_out, scale);
+    return dispatch_k<GsL>(k, ctx, V, k, (i64)ldv, (i64)n, c, 0, const_cast<double *>(t), out_norm2, v_out, scale);
 }
 
 int sbd_gs_update_nodots(sbd_ctx *ctx, const double *V, int k, int64_t ldv, int64_t n, const double *c, double *t,
@@ -955,7 +1247,8 @@ int sbd_gs_update_nodots(sbd_ctx *ctx, const double *V, int k, int64_t ldv, int6
     SBD_CHECK_CTX(ctx);
     if (int rc = check_k(ctx, k)) return rc;
     if (k == 0) return GsL<8>::run(ctx, V, 0, (i64)ldv, (i64)n, c, 0, t, out_norm2);
-    return dispatch_k<GsL>(k, ctx, V, k, (i64)ldv, (i64)n, c, 0, t, out_norm2);
+    return dispatch_k<GsL>(k, ctx, V, k, (i64)ldv, (i64)n, c, 0, t, out_norm2, (double *)nullptr,
+                           (const double *)nullptr);
 }
 
 int sbd_scale_copy(sbd_ctx *ctx, const double *src, double *dst, int64_t n, const double *scale) {

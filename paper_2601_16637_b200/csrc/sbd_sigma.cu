@@ -46,7 +46,7 @@ struct SideArgs {
     const double *diag;            // [n_rows][ldy]
     const double *YT;              // beta-side result, [n_cols][ldyt]
     i64 ldyt;
-    const int64_t *a_s_off;        // rows with alpha singles carry task 0 in Y (cross_kernel)
+    const int64_t *a_s_off;        // rows with alpha singles carry task 0 in Y (cross_kernel); null: no task 0
 };
 
 template <bool VEC>
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[j] = fma(dv[j], xo[j], acc[j]);
             // task 0, already in Y for rows with alpha singles (cross_kernel)
-            if (a.a_s_off[g + 1] != a.a_s_off[g]) {
+            if (a.a_s_off != nullptr && a.a_s_off[g + 1] != a.a_s_off[g]) {
                 double pv[4];
                 load4<VEC, false>(a.Y + r * a.ldy, c0, lane, ok, pv);
 #pragma unroll
@@ -458,7 +458,8 @@ int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full, double *y) {
     a.YT = ctx->yt.as<double>();
     a.ldyt = ctx->ld_t;
     a.diag = ctx->diag.as<double>();
-    a.a_s_off = A.s_off.as<int64_t>();
+    // task 0 exists only when both sectors have in-set singles
+    a.a_s_off = (A.ns > 0 && B.ns > 0) ? A.s_off.as<int64_t>() : nullptr;
     if (A.ns > 0 && B.ns > 0) {
         const size_t smem = 128 + sizeof(double) * 2 * (size_t)(nb + ctx->ld_vpp);
         const bool staged = (nb % 2 == 0) && aligned16(x_full) && smem <= 220 * 1024;

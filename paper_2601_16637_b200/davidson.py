@@ -469,7 +469,11 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
 
 
 def _orthogonalize_device(eng, V, k, ld, n_loc, t, proj, t_norm2, opts, small, scale, reduce) -> bool:
-    """CGS2 of t against V[:k] given c = V^T t; writes V[k] on success."""
+    """CGS2 of t against V[:k] given c = V^T t; writes the normalised V[k] on success.
+
+    Rejection rule of the reference orthogonalize (davidson.py:166-185): the
+    remainder norm must stay >= 1e-12 of the input norm.
+    """
     import torch
 
     norm0 = float(np.sqrt(max(t_norm2, 0.0)))
@@ -478,10 +482,21 @@ def _orthogonalize_device(eng, V, k, ld, n_loc, t, proj, t_norm2, opts, small, s
     dev = V.device
     c = torch.from_numpy(np.ascontiguousarray(proj, dtype=np.float64)).to(dev)
     if opts.reorthogonalize:
+        # CGS pass 1: t' = t - V c ; c2 = V^T t' ; |t'|^2
         eng("sbd_gs_update", _p(V), k, ld, n_loc, _p(c), _p(t), _p(small))
         reduce(small[: k + 1])
-        c2 = small[:k].clone()
-        eng("sbd_gs_update_nodots", _p(V), k, ld, n_loc, _p(c2), _p(t), _p(small))
+        host = small[: k + 1].cpu().numpy()
+        c2, n2p = host[:k], float(host[k])
+        n2 = n2p - float(c2 @ c2)  # |t' - V c2|^2 for orthonormal V
+        c2d = small[:k].clone()
+        if n2p > 0.0 and n2 > 0.5 * n2p:
+            # pass 2 fused with the normalisation, written straight into V[k]
+            if np.sqrt(n2) < 1e-12 * norm0:
+                return False
+            scale.fill_(1.0 / np.sqrt(n2))
+            eng("sbd_gs_finalize", _p(V), k, ld, n_loc, _p(c2d), _p(t), _p(V[k]), _p(scale), _p(small))
+            return True
+        eng("sbd_gs_update_nodots", _p(V), k, ld, n_loc, _p(c2d), _p(t), _p(small))
     else:
         eng("sbd_gs_update_nodots", _p(V), k, ld, n_loc, _p(c), _p(t), _p(small))
     reduce(small[:1])

@@ -84,11 +84,17 @@ class Comm:
         if self.world == 1:
             views[0].copy_(local)
             return None
-        if self._staged(local) or self.backend == "gloo":
-            hv = [v.new_empty(v.shape, device="cpu") for v in views]
-            self.dist.all_gather(hv, local.cpu(), group=self.group)
-            for v, h in zip(views, hv):
-                v.copy_(h)
+        if self.backend == "gloo":
+            # gloo all_gather needs equal sizes: pad every block to the longest
+            import torch
+
+            mx = max(v.numel() for v in views)
+            send = torch.zeros(mx, dtype=local.dtype)
+            send[: local.numel()] = local.cpu()
+            recv = [torch.empty(mx, dtype=local.dtype) for _ in views]
+            self.dist.all_gather(recv, send, group=self.group)
+            for v, h in zip(views, recv):
+                v.copy_(h[: v.numel()])
             return None
         return self.dist.all_gather(views, local, group=self.group, async_op=True)
 
