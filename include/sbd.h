@@ -147,7 +147,8 @@ int sbd_gs_update_nodots(sbd_ctx *ctx, const double *V_dev, int k, int64_t ldv, 
 
 /* Last CGS pass fused with normalisation: v_out = (t - sum_i c[i] V_i) * (*scale_dev),
  * t untouched; out_norm2_dev[0] = |t - V c|^2 (before scaling).  The caller
- * takes scale = 1/sqrt(|t|^2 - |c|^2), exact for orthonormal V. */
+ * takes scale = 1/sqrt(|t|^2 - |c|^2), exact for orthonormal V.  On the non-TMA
+ * fallback path t is overwritten with t - V c. */
 int sbd_gs_finalize(sbd_ctx *ctx, const double *V_dev, int k, int64_t ldv, int64_t n, const double *c_dev,
                     const double *t_dev, double *v_out_dev, const double *scale_dev, double *out_norm2_dev);
 
