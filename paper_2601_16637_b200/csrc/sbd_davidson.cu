@@ -729,7 +729,11 @@ gs_tma(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__rest
     }
 }
 
-// Ritz residual + preconditioner + projections, TMA-fed (stage: k V + k W + diag slices)
+// Ritz residual + preconditioner + projections, TMA-fed (stage: k V + k W + diag
+// slices).  Phase 1 is split over all 8 warps (warp w sums its vectors
+// i = w, w+8, ... for every element; lanes stride the tile), partial sums are
+// combined through shared memory, then the element-wise residual /
+// preconditioner, then the warp-split projections V_i . t_jp.
 template <int K, int M>
 __global__ void __launch_bounds__(kBlock)
 residual_tma(const double *__restrict__ V, const double *__restrict__ W, int k, i64 ldv, i64 n,
@@ -737,11 +741,14 @@ residual_tma(const double *__restrict__ V, const double *__restrict__ W, int k, 
              const double *__restrict__ diag, double delta, double *__restrict__ T, i64 ldt,
              double *__restrict__ partial) {
     constexpr int TT0 = 8192 / (2 * K + 1), TTA = TT0 & ~1, KW = (K + kWarpsT - 1) / kWarpsT;
+    constexpr int EPL = (TTA + 31) / 32;  // elements per lane in the warp-split phases
     extern __shared__ __align__(128) unsigned char rsm2[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(rsm2);
     double *stage0 = reinterpret_cast<double *>(rsm2 + 128);
     const i64 sstride = (i64)(2 * K + 1) * TTA;
-    double *ts = stage0 + 2 * sstride;  // [TTA]: the target root's correction
+    double *ts = stage0 + 2 * sstride;                 // [TTA] correction of the target root
+    double *pu = ts + TTA;                             // [kWarpsT][M][TTA]
+    double *pw = pu + (size_t)kWarpsT * M * TTA;       // [kWarpsT][M][TTA]
     __shared__ double ys[64 * 8];
     __shared__ double th[8];
     __shared__ double red[kWarpsT][M + 1];
@@ -793,28 +800,65 @@ residual_tma(const double *__restrict__ V, const double *__restrict__ W, int k, 
             }
             __syncthreads();
         }
-        for (i64 e = threadIdx.x; e < cnt; e += blockDim.x) {
-            double u[M], wy[M];
+        // phase 1: per-warp partial Y^T V and Y^T W over the warp's vectors
+        {
+            double u[EPL][M], wy[EPL][M];
 #pragma unroll
-            for (int j = 0; j < M; ++j) u[j] = wy[j] = 0.0;
-            for (int i = 0; i < k; ++i) {
-                const double v = st[(i64)i * TTA + e], w = st[(i64)(K + i) * TTA + e];
+            for (int q = 0; q < EPL; ++q)
 #pragma unroll
-                for (int j = 0; j < M; ++j)
-                    if (j < m) {
-                        u[j] = fma(ys[i * m + j], v, u[j]);
-                        wy[j] = fma(ys[i * m + j], w, wy[j]);
+                for (int j = 0; j < M; ++j) u[q][j] = wy[q][j] = 0.0;
+#pragma unroll
+            for (int a = 0; a < KW; ++a) {
+                const int i = warp + kWarpsT * a;
+                if (i < k) {
+                    const double *vi = st + (i64)i * TTA, *wi = st + (i64)(K + i) * TTA;
+                    double yv[M];
+#pragma unroll
+                    for (int j = 0; j < M; ++j) yv[j] = j < m ? ys[i * m + j] : 0.0;
+#pragma unroll
+                    for (int q = 0; q < EPL; ++q) {
+                        const int e = lane + 32 * q;
+                        if (e < TTA) {
+                            const double v = vi[e], w = wi[e];
+#pragma unroll
+                            for (int j = 0; j < M; ++j) {
+                                u[q][j] = fma(yv[j], v, u[q][j]);
+                                wy[q][j] = fma(yv[j], w, wy[q][j]);
+                            }
+                        }
                     }
+                }
             }
+#pragma unroll
+            for (int q = 0; q < EPL; ++q) {
+                const int e = lane + 32 * q;
+                if (e < TTA) {
+#pragma unroll
+                    for (int j = 0; j < M; ++j) {
+                        pu[((size_t)warp * M + j) * TTA + e] = u[q][j];
+                        pw[((size_t)warp * M + j) * TTA + e] = wy[q][j];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // phase 1b: combine, residual, preconditioner (davidson.py:159-163,257)
+        for (i64 e = threadIdx.x; e < cnt; e += blockDim.x) {
             const double d = st[(i64)(2 * K) * TTA + e];
             double tj = 0.0;
 #pragma unroll
             for (int j = 0; j < M; ++j) {
                 if (j < m) {
-                    const double r = wy[j] - th[j] * u[j];
+                    double uu = 0.0, ww = 0.0;
+#pragma unroll
+                    for (int w2 = 0; w2 < kWarpsT; ++w2) {
+                        uu += pu[((size_t)w2 * M + j) * TTA + e];
+                        ww += pw[((size_t)w2 * M + j) * TTA + e];
+                    }
+                    const double r = ww - th[j] * uu;
                     rn2[j] = fma(r, r, rn2[j]);
                     const double g = d - th[j];
-                    const double t = r / ((g >= 0.0 ? 1.0 : -1.0) * fmax(fabs(g), delta));  // davidson.py:159-163
+                    const double t = r / ((g >= 0.0 ? 1.0 : -1.0) * fmax(fabs(g), delta));
                     T[j * ldt + base + e] = t;
                     if (j == jp) tj = t;
                 }
@@ -823,13 +867,18 @@ residual_tma(const double *__restrict__ V, const double *__restrict__ W, int k, 
             tn2 = fma(tj, tj, tn2);
         }
         __syncthreads();
+        // phase 2: projections V_i . t_jp (warp-split)
 #pragma unroll
         for (int a = 0; a < KW; ++a) {
             const int i = warp + kWarpsT * a;
             if (i < k) {
                 const double *vi = st + (i64)i * TTA;
                 double sacc = 0.0;
-                for (i64 e = lane; e < cnt; e += 32) sacc = fma(vi[e], ts[e], sacc);
+#pragma unroll
+                for (int q = 0; q < EPL; ++q) {
+                    const int e = lane + 32 * q;
+                    if (e < cnt) sacc = fma(vi[e], ts[e], sacc);
+                }
                 acc[a] += sacc;
             }
         }
@@ -1081,9 +1130,10 @@ struct ResidL {
     static std::pair<int, int> launch(sbd_ctx *ctx, int nb, const double *V, const double *W, int k, i64 ldv, i64 n,
                                       const double *Y, const double *theta, int m, int jp, const double *diag,
                                       double delta, double *T, i64 ldt) {
-        if (vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_tma()) {
-            constexpr int TTA = (8192 / (2 * K + 1)) & ~1;
-            const size_t smem = 128 + sizeof(double) * (2 * (size_t)(2 * K + 1) * TTA + TTA);
+        constexpr int TTA = (8192 / (2 * K + 1)) & ~1;
+        constexpr size_t smem_tma = 128 + sizeof(double) * (2 * (size_t)(2 * K + 1) * TTA + TTA + 2 * 8 * M * TTA);
+        if (vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_tma() && smem_tma <= 220 * 1024) {
+            const size_t smem = smem_tma;
             const int nt = std::max(1, std::min<int>((int)((n + TTA - 1) / TTA), ctx->num_sms));
             static bool attr = false;
             if (!attr) {
