@@ -620,6 +620,15 @@ residual_tile(const double *__restrict__ V, const double *__restrict__ W, int k,
 // entirely out of shared memory (no second global touch, no register
 // staging).  Stage size is ~64 KB, i.e. TT = 8192 / (#vectors per tile).
 
+// even tile length so that nvec slices of one stage take ~64 KB (<= 1024 elements)
+__host__ __device__ constexpr int tma_tile(int nvec) {
+    return ((8192 / nvec) < 1024 ? (8192 / nvec) : 1024) & ~1;
+}
+// elements per lane needed by residual_tma<K> over the k range dispatch_k maps to K
+__host__ __device__ constexpr int resid_epl(int K) {
+    return (tma_tile(2 * (K <= 8 ? 1 : K / 2 + 1) + 1) + 31) / 32;
+}
+
 struct TmaPipe {
     uint64_t *bar;  // [2]
     __device__ void init() {
@@ -641,12 +650,12 @@ template <int K>
 __global__ void __launch_bounds__(kBlock)
 gs_tma(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__restrict__ c, int kdot,
        const double *t, double *out, const double *__restrict__ scale, double *__restrict__ partial) {
-    constexpr int TT = 8192 / (K + 1), KW = (K + kWarpsT - 1) / kWarpsT;
-    constexpr int TTA = TT & ~1;  // keep tiles an even number of elements
+    constexpr int KW = (K + kWarpsT - 1) / kWarpsT;
+    const int TTA = tma_tile(k + 1);  // ~64 KB of slices per stage, even length
     extern __shared__ __align__(128) unsigned char gsm[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(gsm);
     double *stage0 = reinterpret_cast<double *>(gsm + 128);
-    const i64 sstride = (i64)(K + 1) * TTA;  // doubles per stage: k V slices + t slice
+    const i64 sstride = (i64)(k + 1) * TTA;  // doubles per stage: k V slices + t slice
     __shared__ double cs[K];
     __shared__ double nrm[kWarpsT];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -662,7 +671,7 @@ gs_tma(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__rest
         if (b) {
             mbar_arrive_expect_tx(&bar[s], b * (uint32_t)(k + 1));
             for (int i = 0; i < k; ++i) tma_load_1d(st + (i64)i * TTA, V + i * ldv + base, b, &bar[s]);
-            tma_load_1d(st + (i64)K * TTA, t + base, b, &bar[s]);
+            tma_load_1d(st + (i64)k * TTA, t + base, b, &bar[s]);
         } else {
             mbar_arrive_expect_tx(&bar[s], 0);
         }
@@ -685,11 +694,11 @@ gs_tma(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__rest
             const i64 e = cnt - 1;
             if (threadIdx.x == 0) {
                 for (int i = 0; i < k; ++i) st[(i64)i * TTA + e] = V[i * ldv + base + e];
-                st[(i64)K * TTA + e] = t[base + e];
+                st[(i64)k * TTA + e] = t[base + e];
             }
             __syncthreads();
         }
-        double *ts = st + (i64)K * TTA;
+        double *ts = st + (i64)k * TTA;
         for (i64 e = threadIdx.x; e < cnt; e += blockDim.x) {
             double v = ts[e];
             for (int i = 0; i < k; ++i) v = fma(-cs[i], st[(i64)i * TTA + e], v);
@@ -740,12 +749,13 @@ residual_tma(const double *__restrict__ V, const double *__restrict__ W, int k, 
              const double *__restrict__ Y, const double *__restrict__ theta, int m, int jp,
              const double *__restrict__ diag, double delta, double *__restrict__ T, i64 ldt,
              double *__restrict__ partial) {
-    constexpr int TT0 = 8192 / (2 * K + 1), TTA = TT0 & ~1, KW = (K + kWarpsT - 1) / kWarpsT;
-    constexpr int EPL = (TTA + 31) / 32;  // elements per lane in the warp-split phases
+    constexpr int KW = (K + kWarpsT - 1) / kWarpsT;
+    constexpr int EPL = resid_epl(K);  // elements per lane in the warp-split phases (max over k)
+    const int TTA = tma_tile(2 * k + 1);
     extern __shared__ __align__(128) unsigned char rsm2[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(rsm2);
     double *stage0 = reinterpret_cast<double *>(rsm2 + 128);
-    const i64 sstride = (i64)(2 * K + 1) * TTA;
+    const i64 sstride = (i64)(2 * k + 1) * TTA;
     double *ts = stage0 + 2 * sstride;                 // [TTA] correction of the target root
     double *pu = ts + TTA;                             // [kWarpsT][M][TTA]
     double *pw = pu + (size_t)kWarpsT * M * TTA;       // [kWarpsT][M][TTA]
@@ -766,9 +776,9 @@ residual_tma(const double *__restrict__ V, const double *__restrict__ W, int k, 
             mbar_arrive_expect_tx(&bar[s], b * (uint32_t)(2 * k + 1));
             for (int i = 0; i < k; ++i) {
                 tma_load_1d(st + (i64)i * TTA, V + i * ldv + base, b, &bar[s]);
-                tma_load_1d(st + (i64)(K + i) * TTA, W + i * ldv + base, b, &bar[s]);
+                tma_load_1d(st + (i64)(k + i) * TTA, W + i * ldv + base, b, &bar[s]);
             }
-            tma_load_1d(st + (i64)(2 * K) * TTA, diag + base, b, &bar[s]);
+            tma_load_1d(st + (i64)(2 * k) * TTA, diag + base, b, &bar[s]);
         } else {
             mbar_arrive_expect_tx(&bar[s], 0);
         }
@@ -794,9 +804,9 @@ residual_tma(const double *__restrict__ V, const double *__restrict__ W, int k, 
             if (threadIdx.x == 0) {
                 for (int i = 0; i < k; ++i) {
                     st[(i64)i * TTA + e] = V[i * ldv + base + e];
-                    st[(i64)(K + i) * TTA + e] = W[i * ldv + base + e];
+                    st[(i64)(k + i) * TTA + e] = W[i * ldv + base + e];
                 }
-                st[(i64)(2 * K) * TTA + e] = diag[base + e];
+                st[(i64)(2 * k) * TTA + e] = diag[base + e];
             }
             __syncthreads();
         }
@@ -811,7 +821,7 @@ residual_tma(const double *__restrict__ V, const double *__restrict__ W, int k, 
             for (int a = 0; a < KW; ++a) {
                 const int i = warp + kWarpsT * a;
                 if (i < k) {
-                    const double *vi = st + (i64)i * TTA, *wi = st + (i64)(K + i) * TTA;
+                    const double *vi = st + (i64)i * TTA, *wi = st + (i64)(k + i) * TTA;
                     double yv[M];
 #pragma unroll
                     for (int j = 0; j < M; ++j) yv[j] = j < m ? ys[i * m + j] : 0.0;
@@ -844,7 +854,7 @@ residual_tma(const double *__restrict__ V, const double *__restrict__ W, int k, 
         __syncthreads();
         // phase 1b: combine, residual, preconditioner (davidson.py:159-163,257)
         for (i64 e = threadIdx.x; e < cnt; e += blockDim.x) {
-            const double d = st[(i64)(2 * K) * TTA + e];
+            const double d = st[(i64)(2 * k) * TTA + e];
             double tj = 0.0;
 #pragma unroll
             for (int j = 0; j < M; ++j) {
@@ -1130,14 +1140,15 @@ struct ResidL {
     static std::pair<int, int> launch(sbd_ctx *ctx, int nb, const double *V, const double *W, int k, i64 ldv, i64 n,
                                       const double *Y, const double *theta, int m, int jp, const double *diag,
                                       double delta, double *T, i64 ldt) {
-        constexpr int TTA = (8192 / (2 * K + 1)) & ~1;
-        constexpr size_t smem_tma = 128 + sizeof(double) * (2 * (size_t)(2 * K + 1) * TTA + TTA + 2 * 8 * M * TTA);
-        if (vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_tma() && smem_tma <= 220 * 1024) {
+        const int TTA = tma_tile(2 * k + 1);
+        const size_t smem_tma = 128 + sizeof(double) * (2 * (size_t)(2 * k + 1) * TTA + TTA + 2 * 8 * M * (size_t)TTA);
+        if (vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_tma() && smem_tma <= 220 * 1024 &&
+            TTA <= 32 * resid_epl(K)) {
             const size_t smem = smem_tma;
             const int nt = std::max(1, std::min<int>((int)((n + TTA - 1) / TTA), ctx->num_sms));
             static bool attr = false;
             if (!attr) {
-                cudaFuncSetAttribute(residual_tma<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                cudaFuncSetAttribute(residual_tma<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
                 attr = true;
             }
             residual_tma<K, M><<<nt, kBlock, smem, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T,
@@ -1185,12 +1196,12 @@ struct GsL {
         if (int rc = ensure_red(ctx, nb, K + 1)) return rc;
         double *dst = out_vec ? out_vec : t;
         if (vec_ok(V, ldv, t) && use_tma()) {
-            constexpr int TTA = (8192 / (K + 1)) & ~1;
-            const size_t smem = 128 + sizeof(double) * 2 * (size_t)(K + 1) * TTA;
+            const int TTA = tma_tile(k + 1);
+            const size_t smem = 128 + sizeof(double) * 2 * (size_t)(k + 1) * TTA;
             const int nt = std::max(1, std::min<int>((int)((n + TTA - 1) / TTA), ctx->num_sms));
             static bool attr = false;
             if (!attr) {
-                cudaFuncSetAttribute(gs_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                cudaFuncSetAttribute(gs_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
                 attr = true;
             }
             gs_tma<K><<<nt, kBlock, smem, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale, ctx->red.as<double>());
