@@ -324,7 +324,9 @@ def run_ours(args):
 
     # ---- end to end through the public API -----------------------------------------------
     e2e = None
-    if world == 1:
+    if args.no_e2e:
+        pass
+    elif world == 1:
         xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
         yh = torch.empty(n, dtype=torch.float64, pin_memory=True)
         xh.copy_(x_own.cpu())
@@ -386,7 +388,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(table, a, b)
 
-    launches_per_step = 3
+    launches_per_step = 4  # transpose, beta side, task-0 cross, alpha side
     line = {
         "metric": METRIC, "value": value, "unit": "dets/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": t_step * 1e3, "higher_is_better": True,
@@ -424,6 +426,7 @@ def main():
     ap.add_argument("--no-davidson", action="store_true")
     ap.add_argument("--davidson-iters", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
