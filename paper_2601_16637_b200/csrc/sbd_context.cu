@@ -114,9 +114,15 @@ int sbd_set_integrals(sbd_ctx *ctx, int norb, const double *h_host, const double
     SBD_CUDA(ctx, cudaMemcpy(ctx->dpq.p, dpq.data(), sizeof(double) * norb * norb, cudaMemcpyHostToDevice));
     ctx->ld_vpp = (npair + 1) / 2 * 2;
     {
-        std::vector<double> vpp((size_t)npair * ctx->ld_vpp, 0.0);
+        const i64 ld = ctx->ld_vpp;
+        std::vector<double> vpp((size_t)npair * 4 * ld, 0.0);
         for (i64 P = 0; P < npair; ++P)
-            for (i64 Q = 0; Q < npair; ++Q) vpp[(size_t)P * ctx->ld_vpp + Q] = eri_host[tri_idx(P, Q)];
+            for (int sa = 0; sa < 2; ++sa)
+                for (i64 Q = 0; Q < npair; ++Q) {
+                    const double v = eri_host[tri_idx(P, Q)];
+                    vpp[(size_t)(2 * P + sa) * 2 * ld + Q] = sa ? -v : v;
+                    vpp[(size_t)(2 * P + sa) * 2 * ld + ld + Q] = sa ? v : -v;
+                }
         SBD_CUDA(ctx, ctx->vpp.ensure(sizeof(double) * vpp.size()));
         SBD_CUDA(ctx, cudaMemcpy(ctx->vpp.p, vpp.data(), sizeof(double) * vpp.size(), cudaMemcpyHostToDevice));
     }

@@ -969,68 +969,137 @@ __global__ void __launch_bounds__(kBlock) combine_kernel(const double *__restric
     }
 }
 
-// Cyclic Jacobi (davidson.py:86-148) by one warp; lanes own matrix rows.
+// Jacobi eigensolver of the projected matrix (davidson.py:86-148): same
+// rotation formulas, symmetrisation, stopping rule (off-norm <= 1e-14 ||A||_F
+// at a sweep start) and stable ascending output order as the reference, but
+// with the parallel (round-robin tournament) ordering: each step rotates
+// kk/2 disjoint pairs at once (rows, then columns, of one CTA), so a sweep is
+// kk-1 steps instead of k(k-1)/2 sequential rotations.  Eigenvalues agree
+// with the cyclic order to rounding; eigenvector signs are arbitrary in both.
 constexpr int kJacMax = 64;
-__global__ void jacobi_kernel(const double *__restrict__ Ain, int k, int lda, double *__restrict__ evals,
-                              double *__restrict__ evecs, int max_sweeps, int *__restrict__ info) {
+constexpr int kJacThreads = 256;
+__global__ void __launch_bounds__(kJacThreads) jacobi_kernel(const double *__restrict__ Ain, int k, int lda,
+                                                             double *__restrict__ evals, double *__restrict__ evecs,
+                                                             int max_sweeps, int *__restrict__ info) {
     extern __shared__ double jsm[];
     double(*a)[kJacMax + 1] = reinterpret_cast<double(*)[kJacMax + 1]>(jsm);
     double(*v)[kJacMax + 1] = reinterpret_cast<double(*)[kJacMax + 1]>(jsm + kJacMax * (kJacMax + 1));
-    int *order = reinterpret_cast<int *>(jsm + 2 * kJacMax * (kJacMax + 1));
-    const int lane = threadIdx.x;
-    // symmetrise: a = (M + M^T) / 2 ; v = I
-    for (int idx = lane; idx < k * k; idx += 32) {
-        int p = idx / k, q = idx % k;
+    double *rc = jsm + 2 * kJacMax * (kJacMax + 1);  // per pair: c, s, new a_pp, new a_qq  [4][kJacMax/2]
+    int *order = reinterpret_cast<int *>(rc + 4 * (kJacMax / 2));
+    int *pp = order + kJacMax;                       // pair members [2][kJacMax/2]
+    __shared__ double red[kJacThreads / 32];
+    __shared__ int stop;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int kk = (k + 1) & ~1, np = kk / 2;  // even size (index k is a phantom when k is odd)
+    for (int idx = tid; idx < k * k; idx += kJacThreads) {
+        const int p = idx / k, q = idx % k;
         a[p][q] = (Ain[p * lda + q] + Ain[q * lda + p]) / 2.0;
         v[p][q] = p == q ? 1.0 : 0.0;
     }
-    __syncwarp();
+    __syncthreads();
     double fro = 0.0;
-    for (int idx = lane; idx < k * k; idx += 32) fro = fma(a[idx / k][idx % k], a[idx / k][idx % k], fro);
+    for (int idx = tid; idx < k * k; idx += kJacThreads) fro = fma(a[idx / k][idx % k], a[idx / k][idx % k], fro);
     fro = warp_sum(fro);
-    const double tol = 1e-14 * sqrt(fro);
+    if (lane == 0) red[warp] = fro;
+    __syncthreads();
+    if (tid == 0) {
+        double f = 0.0;
+        for (int w = 0; w < kJacThreads / 32; ++w) f += red[w];
+        red[0] = f;
+    }
+    __syncthreads();
+    const double tol = 1e-14 * sqrt(red[0]);
+    __syncthreads();
     int sweep = 0;
     for (; sweep < max_sweeps; ++sweep) {
         double off = 0.0;
-        for (int p = lane; p < k - 1; p += 32)
-            for (int q = p + 1; q < k; ++q) off += 2.0 * a[p][q] * a[p][q];
+        for (int idx = tid; idx < k * k; idx += kJacThreads) {
+            const int p = idx / k, q = idx % k;
+            if (q > p) off += 2.0 * a[p][q] * a[p][q];
+        }
         off = warp_sum(off);
-        if (sqrt(off) <= tol) break;
-        for (int p = 0; p < k - 1; ++p) {
-            for (int q = p + 1; q < k; ++q) {
-                const double apq = a[p][q];
-                if (apq == 0.0) continue;
-                const double app = a[p][p], aqq = a[q][q];
-                const double theta = (aqq - app) / (2.0 * apq);
-                double t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
-                if (theta < 0.0) t = -t;
-                const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
-                __syncwarp();
-                for (int r = lane; r < k; r += 32) {
-                    if (r != p && r != q) {
-                        const double arp = a[r][p], arq = a[r][q];
-                        const double np = c * arp - s * arq, nq = s * arp + c * arq;
-                        a[r][p] = np;
-                        a[p][r] = np;
-                        a[r][q] = nq;
-                        a[q][r] = nq;
+        if (lane == 0) red[warp] = off;
+        __syncthreads();
+        if (tid == 0) {
+            double f = 0.0;
+            for (int w = 0; w < kJacThreads / 32; ++w) f += red[w];
+            stop = sqrt(f) <= tol;
+        }
+        __syncthreads();
+        if (stop) break;
+        for (int step = 0; step < kk - 1; ++step) {
+            // round robin: position 0 fixed, positions 1..kk-1 rotate by `step`
+            if (tid < np) {
+                auto at = [&](int pos) { return pos == 0 ? 0 : 1 + (pos - 1 + step) % (kk - 1); };
+                int p = at(tid), q = at(kk - 1 - tid);
+                if (p > q) { const int t = p; p = q; q = t; }
+                pp[tid] = p;
+                pp[np + tid] = q;
+                double c = 1.0, sn = 0.0, npp = 0.0, nqq = 0.0;
+                int act = 0;
+                if (q < k) {
+                    const double apq = a[p][q];
+                    if (apq != 0.0) {
+                        act = 1;
+                        const double app = a[p][p], aqq = a[q][q];
+                        const double theta = (aqq - app) / (2.0 * apq);
+                        double t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
+                        if (theta < 0.0) t = -t;
+                        c = 1.0 / sqrt(t * t + 1.0);
+                        sn = t * c;
+                        npp = app - t * apq;
+                        nqq = aqq + t * apq;
                     }
-                    const double vrp = v[r][p], vrq = v[r][q];
-                    v[r][p] = c * vrp - s * vrq;
-                    v[r][q] = s * vrp + c * vrq;
                 }
-                if (lane == 0) {
-                    a[p][p] = app - t * apq;
-                    a[q][q] = aqq + t * apq;
+                rc[tid] = c;
+                rc[kJacMax / 2 + tid] = sn;
+                rc[kJacMax + tid] = npp;
+                rc[3 * (kJacMax / 2) + tid] = nqq;
+                pp[2 * np + tid] = act;
+            }
+            __syncthreads();
+            // rows: J^T A
+            for (int idx = tid; idx < np * k; idx += kJacThreads) {
+                const int i = idx / k, col = idx % k;
+                const int p = pp[i], q = pp[np + i];
+                const double sn = rc[kJacMax / 2 + i];
+                if (pp[2 * np + i]) {
+                    const double c = rc[i], ap = a[p][col], aq = a[q][col];
+                    a[p][col] = c * ap - sn * aq;
+                    a[q][col] = sn * ap + c * aq;
+                }
+            }
+            __syncthreads();
+            // columns: (J^T A) J and V J
+            for (int idx = tid; idx < np * k; idx += kJacThreads) {
+                const int i = idx / k, r = idx % k;
+                const int p = pp[i], q = pp[np + i];
+                const double sn = rc[kJacMax / 2 + i];
+                if (pp[2 * np + i]) {
+                    const double c = rc[i];
+                    const double ap = a[r][p], aq = a[r][q];
+                    a[r][p] = c * ap - sn * aq;
+                    a[r][q] = sn * ap + c * aq;
+                    const double vp = v[r][p], vq = v[r][q];
+                    v[r][p] = c * vp - sn * vq;
+                    v[r][q] = sn * vp + c * vq;
+                }
+            }
+            __syncthreads();
+            // the rotated 2x2 block exactly as the reference writes it
+            if (tid < np) {
+                const int p = pp[tid], q = pp[np + tid];
+                if (pp[2 * np + tid]) {
+                    a[p][p] = rc[kJacMax + tid];
+                    a[q][q] = rc[3 * (kJacMax / 2) + tid];
                     a[p][q] = 0.0;
                     a[q][p] = 0.0;
                 }
-                __syncwarp();
             }
+            __syncthreads();
         }
     }
-    __syncwarp();
-    if (lane == 0) {
+    if (tid == 0) {
         // stable ascending order of the diagonal (np.argsort kind="stable")
         for (int i = 0; i < k; ++i) order[i] = i;
         for (int i = 1; i < k; ++i) {
@@ -1045,9 +1114,9 @@ __global__ void jacobi_kernel(const double *__restrict__ Ain, int k, int lda, do
         }
         info[0] = sweep;
     }
-    __syncwarp();
-    for (int i = lane; i < k; i += 32) evals[i] = a[order[i]][order[i]];
-    for (int idx = lane; idx < k * k; idx += 32) {
+    __syncthreads();
+    for (int i = tid; i < k; i += kJacThreads) evals[i] = a[order[i]][order[i]];
+    for (int idx = tid; idx < k * k; idx += kJacThreads) {
         int r = idx / k, cidx = idx % k;
         evecs[r * k + cidx] = v[r][order[cidx]];
     }
@@ -1338,13 +1407,14 @@ int sbd_jacobi(sbd_ctx *ctx, const double *A, int k, int lda, double *evals, dou
                int *info) {
     SBD_CHECK_CTX(ctx);
     if (k < 1 || k > kJacMax) return sbd_fail(ctx, SBD_EINVAL, "jacobi size must be in [1, 64]");
-    const int smem = (int)(sizeof(double) * 2 * kJacMax * (kJacMax + 1) + sizeof(int) * kJacMax);
+    const int smem = (int)(sizeof(double) * (2 * kJacMax * (kJacMax + 1) + 4 * (kJacMax / 2)) +
+                           sizeof(int) * 3 * kJacMax);
     static bool attr_set = false;
     if (!attr_set) {
         SBD_CUDA(ctx, cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr_set = true;
     }
-    jacobi_kernel<<<1, 32, smem, ctx->stream>>>(A, k, lda, evals, evecs, max_sweeps, info);
+    jacobi_kernel<<<1, kJacThreads, smem, ctx->stream>>>(A, k, lda, evals, evecs, max_sweeps, info);
     SBD_LAUNCHED(ctx, "jacobi");
     return SBD_OK;
 }

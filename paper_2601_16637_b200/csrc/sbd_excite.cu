@@ -15,6 +15,7 @@
 // the reference's entry order; targets are mapped back to caller indices
 // through the sort permutation.
 #include <algorithm>
+#include <vector>
 
 #include "sbd_internal.cuh"
 
@@ -262,24 +263,94 @@ __global__ void jtable_kernel(const u64 *__restrict__ str, i64 n, i64 npair, con
     J[P * n + i] = acc;
 }
 
-// Slot-major ELL of the singles: ell[slot * ld + i] for slot < count(i), then empty.
-__global__ void ell_kernel(i64 n, const int64_t *__restrict__ s_off, const SConn *__restrict__ sconn, int w, i64 ld,
-                           uint32_t *__restrict__ ell) {
-    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= ld) return;
-    const i64 m0 = i < n ? s_off[i] : 0, cnt = i < n ? s_off[i + 1] - m0 : 0;
-    for (int s = 0; s < w; ++s) {
-        uint32_t v = kEllEmpty;
-        if (s < cnt) {
-            const SConn e = sconn[m0 + s];
-            const uint32_t P = (uint32_t)(abs(e.info) - 1);
-            v = ((uint32_t)e.tgt << (kEllPairBits + 1)) | (P << 1) | (e.info < 0 ? 1u : 0u);
-        }
-        ell[s * ld + i] = v;
-    }
-}
-
 }  // namespace
+
+// Sliced-ELL layout of the singles for the opposite-spin (task 0) kernel
+// (host side: O(n log n) on tables that are already final; the layout only
+// balances work, it never changes which terms are summed).
+//
+// Strings are sorted by single count (descending, stable) into groups of 32
+// positions.  The target index space [0, n) is cut into H chunks of
+// sell_chunk strings; for chunk h, group g holds W_{h,g} slots (the widest
+// position of the group), slot-major: entry q of position l at
+// ent[goff[h][g] + 32 q + l].  An entry is packed as
+//   (tgt - h * chunk) << sell_pbits | (P + neg * ld_vpp)
+// i.e. the chunk-local target and the column of the sign-folded ERI row
+// (sbd_context.cu: row (Pa, s_a) = [s_a (Pa|.), -s_a (Pa|.)]).  Unused slots
+// point at local target `chunk`, a zero slot the kernel keeps after the
+// staged chunk, so padding adds exactly 0.0 with no branch.
+static int build_sell(sbd_ctx *ctx, Sector &s) {
+    const i64 n = s.n;
+    cudaStream_t st = ctx->stream;
+    std::vector<int64_t> off(n + 1);
+    std::vector<SConn> sc(s.ns + 1);
+    SBD_CUDA(ctx, cudaMemcpyAsync(off.data(), s.s_off.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
+    if (s.ns) SBD_CUDA(ctx, cudaMemcpyAsync(sc.data(), s.sconn.p, sizeof(SConn) * s.ns, cudaMemcpyDeviceToHost, st));
+    SBD_CUDA(ctx, cudaStreamSynchronize(st));
+    const i64 H = std::max<i64>(1, (n + kSellChunk - 1) / kSellChunk);
+    const i64 chunk = std::max<i64>(2, ((n + H - 1) / H + 1) & ~(i64)1);  // even: 16-byte TMA rows
+    int pbits = 1;
+    while (((i64)1 << pbits) < 2 * ctx->ld_vpp) ++pbits;
+    int cbits = 1;
+    while (((i64)1 << cbits) <= chunk) ++cbits;
+    if (pbits + cbits > 32) return sbd_fail(ctx, SBD_EINVAL, "sector too large for the packed single-excitation table");
+    // per-string, per-chunk counts; sort by (total, count in chunk 0, 1, ...)
+    // descending, so the 32 positions of a group have (nearly) equal counts in
+    // every chunk and padding stays small
+    std::vector<int32_t> cc((size_t)n * H, 0);
+    for (i64 i = 0; i < n; ++i)
+        for (i64 k = off[i]; k < off[i + 1]; ++k) ++cc[(size_t)i * H + sc[k].tgt / chunk];
+    std::vector<int32_t> order(n);
+    for (i64 i = 0; i < n; ++i) order[i] = (int32_t)i;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+        const i64 ta = off[a + 1] - off[a], tb = off[b + 1] - off[b];
+        if (ta != tb) return ta > tb;
+        for (i64 h = 0; h < H; ++h)
+            if (cc[(size_t)a * H + h] != cc[(size_t)b * H + h]) return cc[(size_t)a * H + h] > cc[(size_t)b * H + h];
+        return false;
+    });
+    const i64 groups = (n + 31) / 32;
+    std::vector<int64_t> goff((size_t)H * (groups + 1), 0);
+    i64 total = 0;
+    for (i64 h = 0; h < H; ++h) {
+        for (i64 g = 0; g < groups; ++g) {
+            i64 w = 0;
+            for (i64 l = 0; l < 32 && g * 32 + l < n; ++l) w = std::max<i64>(w, cc[(size_t)order[g * 32 + l] * H + h]);
+            goff[h * (groups + 1) + g] = total;
+            total += 32 * w;
+        }
+        goff[h * (groups + 1) + groups] = total;
+    }
+    if (total >= (int64_t)INT32_MAX) return sbd_fail(ctx, SBD_EINVAL, "singles table too large");
+    const uint32_t null_ent = (uint32_t)chunk << pbits;
+    std::vector<uint32_t> ent((size_t)total + 4, null_ent);
+    std::vector<int32_t> col((size_t)groups * 32 + 1, -1), go((size_t)H * (groups + 1));
+    for (i64 p = 0; p < n; ++p) {
+        const i64 g = p / 32, l = p % 32;
+        const int32_t c = order[p];
+        std::vector<i64> fill(H, 0);
+        for (i64 k = off[c]; k < off[c + 1]; ++k) {
+            const i64 h = sc[k].tgt / chunk, jl = sc[k].tgt - h * chunk;
+            const i64 P = std::abs(sc[k].info) - 1, neg = sc[k].info < 0;
+            ent[goff[h * (groups + 1) + g] + 32 * fill[h] + l] = ((uint32_t)jl << pbits) | (uint32_t)(P + neg * ctx->ld_vpp);
+            ++fill[h];
+        }
+        col[p] = c;
+    }
+    for (size_t i = 0; i < go.size(); ++i) go[i] = (int32_t)goff[i];
+    s.sell_groups = groups;
+    s.sell_nent = total;
+    s.sell_h = H;
+    s.sell_chunk = chunk;
+    s.sell_pbits = pbits;
+    SBD_CUDA(ctx, s.sell_ent.ensure(sizeof(uint32_t) * ent.size()));
+    SBD_CUDA(ctx, s.sell_goff.ensure(sizeof(int32_t) * go.size()));
+    SBD_CUDA(ctx, s.sell_col.ensure(sizeof(int32_t) * col.size()));
+    SBD_CUDA(ctx, cudaMemcpy(s.sell_ent.p, ent.data(), sizeof(uint32_t) * ent.size(), cudaMemcpyHostToDevice));
+    SBD_CUDA(ctx, cudaMemcpy(s.sell_goff.p, go.data(), sizeof(int32_t) * go.size(), cudaMemcpyHostToDevice));
+    SBD_CUDA(ctx, cudaMemcpy(s.sell_col.p, col.data(), sizeof(int32_t) * col.size(), cudaMemcpyHostToDevice));
+    return SBD_OK;
+}
 
 int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s) {
     const i64 n = s.n;
@@ -360,21 +431,9 @@ int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other) {
     dim3 g(grid_for(n, 128), (unsigned)ctx->npair);
     jtable_kernel<<<g, 128, 0, st>>>(s.str.as<u64>(), n, ctx->npair, ctx->eri.as<double>(), s.J.as<double>());
     SBD_LAUNCHED(ctx, "jtable");
-    // ELL of the singles for the opposite-spin (task 0) kernel
-    std::vector<int64_t> off(n + 1);
-    SBD_CUDA(ctx, cudaMemcpyAsync(off.data(), s.s_off.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
-    SBD_CUDA(ctx, cudaStreamSynchronize(st));
-    int w = 0;
-    for (i64 i = 0; i < n; ++i) w = std::max<int>(w, (int)(off[i + 1] - off[i]));
-    if (n >= kEllMaxStrings || ctx->npair >= ((i64)1 << kEllPairBits))
+    // packed singles for the opposite-spin (task 0) kernel
+    if (n >= kPackMaxStrings || ctx->npair >= ((i64)1 << kPackPairBits))
         return sbd_fail(ctx, SBD_EINVAL, "sector too large for the packed single-excitation table");
-    s.ell_w = w;
-    s.ell_ld = (n + 3) / 4 * 4;
-    SBD_CUDA(ctx, s.ell.ensure(sizeof(uint32_t) * ((size_t)std::max(w, 1) * s.ell_ld + 4)));
-    if (w > 0) {
-        ell_kernel<<<grid_for(s.ell_ld, 256), 256, 0, st>>>(n, s.s_off.as<int64_t>(), s.sconn.as<SConn>(), w, s.ell_ld,
-                                                            s.ell.as<uint32_t>());
-        SBD_LAUNCHED(ctx, "ell");
-    }
+    return build_sell(ctx, s);
     return SBD_OK;
 }

@@ -55,9 +55,13 @@ struct Sector {
     DevBuf s_row;            // int32[ns]: source string of each single
     DevBuf energy;           // f64[n]: same-spin diagonal energy per string
     DevBuf J;                // f64[npair][n]: J[P][i] = sum_{q in string i} (P|qq)
-    DevBuf ell;              // u32[ell_w][ell_ld]: singles, slot-major, packed (tgt<<13 | P<<1 | neg)
-    int ell_w = 0;
-    i64 ell_ld = 0;
+    // singles for the opposite-spin (task 0) kernel: chunked sliced ELL, see
+    // build_sell (sbd_excite.cu) for the layout
+    DevBuf sell_ent;         // u32[sell_nent]
+    DevBuf sell_goff;        // int32[sell_h][groups+1]
+    DevBuf sell_col;         // int32[groups*32]: string at each position (-1: padding)
+    i64 sell_groups = 0, sell_nent = 0, sell_h = 1, sell_chunk = 0;
+    int sell_pbits = 1;
     bool built = false;
 };
 
@@ -70,7 +74,8 @@ struct sbd_ctx {
     double e_core = 0.0;
     bool have_integrals = false;
     DevBuf h, eri, dpq;  // h[norb*norb], eri, dpq[norb*norb] = (pp|qq)
-    DevBuf vpp;          // vpp[P * ld_vpp + Q] = (P|Q) over orbital pairs (rows 16-byte aligned)
+    DevBuf vpp;          // sign-folded pair-pair ERI rows: row (P, sa) at (2P + sa) * 2 ld_vpp holds
+                         //   [ (-1)^sa (P|Q) for Q < ld_vpp | -(-1)^sa (P|Q) for Q < ld_vpp ]
     i64 ld_vpp = 0;
     Sector sec[2];
     i64 row_lo = 0, row_hi = -1;  // owned alpha rows (row_hi < 0: all)
@@ -116,9 +121,9 @@ int sbd_sort_strings(sbd_ctx *ctx, Sector &s);              // sbd_strings.cu
 int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s);       // sbd_excite.cu
 int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other);  // sbd_excite.cu
 
-constexpr uint32_t kEllEmpty = 0xFFFFFFFFu;
-constexpr int kEllPairBits = 12;   // orbital pair index < 4096 (norb <= 64 gives 2080)
-constexpr i64 kEllMaxStrings = (i64)1 << 19;
+constexpr i64 kSellChunk = 3584;  // strings per staged chunk of an x row (28 KB)
+constexpr int kPackPairBits = 12;   // orbital pair index < 4096 (norb <= 64 gives 2080)
+constexpr i64 kPackMaxStrings = (i64)1 << 19;  // target index in the remaining 19 bits
 
 __host__ __device__ inline i64 tri_idx(i64 a, i64 b) {
     return a >= b ? a * (a + 1) / 2 + b : b * (b + 1) / 2 + a;

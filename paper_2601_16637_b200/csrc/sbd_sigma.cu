@@ -22,6 +22,7 @@
 // Grid order keeps all SMs on one column tile of X at a time, so the ~c-bar
 // re-reads of each X row segment are served from L2.
 #include <algorithm>
+#include <cstdlib>
 
 #include "sbd_internal.cuh"
 #include "sbd_ptx.cuh"
@@ -199,15 +200,24 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
 // written for rows that have alpha singles (the streaming kernel adds it).
 //
 // Work list: the flat list of alpha-single entries of the owned rows, split
-// over CTAs at row boundaries (a row's entries stay in one CTA, so its Y row
-// is read-modify-written by one thread per column, no atomics).  For each
-// entry the gathers X[ja_k, jb] hit arbitrary columns of row ja_k: the whole
-// row and the pair-pair ERI row (Pa_k | *) are brought into shared memory by
-// TMA bulk copies (cp.async.bulk + mbarrier), double-buffered so entry e+1's
-// copy overlaps entry e's gathers.  The beta singles come from a slot-major
-// packed ELL table: each thread owns 4 consecutive columns and reads one
-// 128-bit word per slot.
-constexpr int kCrossThreads = 512;
+// over CTAs at row boundaries, so a row's entries stay in one CTA.  The beta
+// singles are a chunked sliced ELL (sbd_excite.cu build_sell): beta strings
+// sorted by single count into groups of 32 positions; per chunk of targets
+// each group is slot-major and padded to its widest position with entries
+// that read a zero slot.  Lane l of warp w owns position l of groups
+// w + 32 j (j < CPT) and keeps their sums in registers across all entries of
+// a row; the row is written once (no atomics, no read-back).  An entry packs
+// the chunk-local target and the column of a sign-folded ERI row, so the
+// inner loop is: shared load, shift, mask, two shared gathers, one FMA.
+//
+// Staged variant: per (entry, chunk) item, the x row chunk ja_k[h*C, h*C+C)
+// and the ERI row (Pa_k, s_k) are TMA bulk-copied (cp.async.bulk + mbarrier)
+// into one of two shared-memory stages; full[s] counts the bytes, empty[s]
+// counts warps done with it, so a fast warp runs ahead into the other stage
+// and thread 0 refills a stage as soon as every warp released it.  The SELL
+// itself is also resident in shared memory when it fits.
+constexpr int kCrossThreads = 1024;      // staged: one CTA per SM
+constexpr int kCrossThreadsFlat = 256;   // flat: group tiles x entry ranges
 
 __device__ __forceinline__ i64 snap_entry(i64 t, i64 e_end, const int64_t *__restrict__ a_s_off,
                                           const int32_t *__restrict__ a_row) {
@@ -216,99 +226,195 @@ __device__ __forceinline__ i64 snap_entry(i64 t, i64 e_end, const int64_t *__res
     return t == a_s_off[g] ? t : a_s_off[g + 1];
 }
 
-template <bool STAGED>
-__device__ __forceinline__ void cross_entry(const double *xrow, const double *vrow, double sga, bool first, double *yr,
-                                            i64 nb, const uint32_t *__restrict__ ell, int ell_w, i64 ell_ld) {
-    for (i64 ib = (i64)threadIdx.x * 4; ib < nb; ib += (i64)blockDim.x * 4) {
-        double acc[4];
+struct CrossArgs {
+    i64 n_rows, row_base, nb;
+    const double *X;
+    double *Y;
+    const int64_t *a_s_off;
+    const SConn *a_sconn;
+    const int32_t *a_row;
+    const int32_t *goff;     // beta SELL group offsets [H][groups+1]
+    const int32_t *col;      // beta SELL position -> beta string
+    const uint32_t *ent;     // beta SELL entries
+    i64 groups, H, chunk;
+    int pbits;
+    const double *vsg;       // sign-folded ERI rows, row (P, s) at (2P + s) * 2 ld
+    i64 ld;
+};
+
+__device__ __forceinline__ const double *vrow(const CrossArgs &a, const SConn &sa) {
+    return a.vsg + (i64)(2 * (abs(sa.info) - 1) + (sa.info < 0)) * 2 * a.ld;
+}
+
+// acc[j] += sum over the item's entries of position (g_lo + warp + j*nw, lane)
+template <int CPT, bool CHECK>
+__device__ __forceinline__ void cross_accumulate(double (&acc)[CPT], const CrossArgs &a, const int32_t *goff_h,
+                                                 const uint32_t *ent, const double *xr, const double *vr, i64 g_lo,
+                                                 int nw) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t pmask = (1u << a.pbits) - 1u, nul = (uint32_t)a.chunk;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j] = (first || ib + j >= nb) ? 0.0 : yr[ib + j];
-        for (int slot0 = 0; slot0 < ell_w; slot0 += 4) {
-            uint4 e4[4];
-            bool any = false;
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-                e4[s] = slot0 + s < ell_w ? __ldg(reinterpret_cast<const uint4 *>(ell + (i64)(slot0 + s) * ell_ld + ib))
-                                          : make_uint4(kEllEmpty, kEllEmpty, kEllEmpty, kEllEmpty);
-            }
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-                const uint32_t ev[4] = {e4[s].x, e4[s].y, e4[s].z, e4[s].w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint32_t e = ev[j];
-                    if (e == kEllEmpty) continue;
-                    any = true;
-                    const i64 jb = (i64)(e >> (kEllPairBits + 1));
-                    const int Pb = (int)((e >> 1) & ((1u << kEllPairBits) - 1));
-                    const double v = STAGED ? vrow[Pb] : __ldg(vrow + Pb);
-                    const double x = STAGED ? xrow[jb] : __ldg(xrow + jb);
-                    const double t = sga * v * x;
-                    acc[j] = (e & 1u) ? acc[j] - t : acc[j] + t;
+    for (int j = 0; j < CPT; ++j) {
+        const i64 g = g_lo + warp + (i64)j * nw;
+        if (g < a.groups) {
+            const int o0 = goff_h[g], w = (goff_h[g + 1] - o0) >> 5;
+            const uint32_t *ep = ent + o0 + lane;
+            int q = 0;
+            for (; q + 2 <= w; q += 2) {
+                const uint32_t p0 = ep[32 * q], p1 = ep[32 * q + 32];
+                if (CHECK) {
+                    if ((p0 >> a.pbits) != nul) acc[j] = fma(vr[p0 & pmask], xr[p0 >> a.pbits], acc[j]);
+                    if ((p1 >> a.pbits) != nul) acc[j] = fma(vr[p1 & pmask], xr[p1 >> a.pbits], acc[j]);
+                } else {
+                    const double t0 = vr[p0 & pmask] * xr[p0 >> a.pbits];
+                    acc[j] = fma(vr[p1 & pmask], xr[p1 >> a.pbits], acc[j] + t0);
                 }
             }
-            if (!any) break;  // slots fill in order: an all-empty group ends the row
+            if (q < w) {
+                const uint32_t p0 = ep[32 * q];
+                if (!CHECK || (p0 >> a.pbits) != nul) acc[j] = fma(vr[p0 & pmask], xr[p0 >> a.pbits], acc[j]);
+            }
         }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (ib + j < nb) yr[ib + j] = acc[j];
     }
 }
 
-template <bool STAGED>
-__global__ void __launch_bounds__(kCrossThreads)
-cross_kernel(i64 n_rows, i64 row_base, i64 nb, const double *__restrict__ X, double *__restrict__ Y,
-             const int64_t *__restrict__ a_s_off, const SConn *__restrict__ a_sconn, const int32_t *__restrict__ a_row,
-             const uint32_t *__restrict__ ell, int ell_w, i64 ell_ld, const double *__restrict__ vpp, i64 ld_vpp) {
+template <int CPT>
+__device__ __forceinline__ void cross_store(double (&acc)[CPT], const CrossArgs &a, double *yr, i64 g_lo, int nw) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int c[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {  // all column loads first: one round trip, not CPT
+        const i64 g = g_lo + warp + (i64)j * nw;
+        c[j] = g < a.groups ? __ldg(a.col + g * 32 + lane) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+        if (c[j] >= 0) yr[c[j]] = acc[j];
+        acc[j] = 0.0;
+    }
+}
+
+__host__ __device__ inline i64 cross_stage_doubles(i64 chunk, i64 ld) { return chunk + 2 + 2 * ld; }
+constexpr int kCrossStages = 3;
+
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Warp-specialised pipeline: the last warp produces (TMA into kCrossStages
+// stages, L2 prefetch two items further ahead), the other warps consume.
+template <int CPT, bool SENT>
+__global__ void __launch_bounds__(kCrossThreads, 1) cross_kernel_tma(CrossArgs a) {
     extern __shared__ __align__(128) unsigned char csm[];
-    uint64_t *bar = reinterpret_cast<uint64_t *>(csm);
-    double *xs0 = reinterpret_cast<double *>(csm + 128);
-    const i64 stage = nb + ld_vpp;  // doubles per stage: X row then ERI row
-    const i64 E0 = a_s_off[row_base], E1 = a_s_off[row_base + n_rows];
+    uint64_t *full = reinterpret_cast<uint64_t *>(csm);
+    uint64_t *empty = full + kCrossStages;
+    double *st0 = reinterpret_cast<double *>(csm + 128);
+    const i64 sdbl = cross_stage_doubles(a.chunk, a.ld);
+    int32_t *sgoff = reinterpret_cast<int32_t *>(st0 + kCrossStages * sdbl);
+    const i64 ngoff = a.H * (a.groups + 1);
+    uint32_t *sent = reinterpret_cast<uint32_t *>(sgoff + ((ngoff + 3) & ~(i64)3));
+    constexpr int kC = kCrossThreads / 32 - 1;  // consumer warps
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const i64 E0 = a.a_s_off[a.row_base], E1 = a.a_s_off[a.row_base + a.n_rows];
     const i64 tot = E1 - E0;
-    const i64 e0 = snap_entry(E0 + tot * blockIdx.x / gridDim.x, E1, a_s_off, a_row);
-    const i64 e1 = snap_entry(E0 + tot * (blockIdx.x + 1) / gridDim.x, E1, a_s_off, a_row);
+    const i64 e0 = snap_entry(E0 + tot * blockIdx.x / gridDim.x, E1, a.a_s_off, a.a_row);
+    const i64 e1 = snap_entry(E0 + tot * (blockIdx.x + 1) / gridDim.x, E1, a.a_s_off, a.a_row);
     if (e0 >= e1) return;
-    if (!STAGED) {
-        for (i64 e = e0; e < e1; ++e) {
-            const SConn sa = a_sconn[e];
-            const i64 g = a_row[e];
-            const double sga = sa.info > 0 ? 1.0 : -1.0;
-            cross_entry<false>(X + (i64)sa.tgt * nb, vpp + (i64)(abs(sa.info) - 1) * ld_vpp, sga, e == a_s_off[g],
-                               Y + (g - row_base) * nb, nb, ell, ell_w, ell_ld);
-            __syncthreads();
+    const i64 nitems = (e1 - e0) * a.H;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kCrossStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kC);
+        }
+        mbar_fence_init();
+    }
+    if (threadIdx.x < kCrossStages) {  // zero slots read by padding entries
+        st0[threadIdx.x * sdbl + a.chunk] = 0.0;
+        st0[threadIdx.x * sdbl + a.chunk + 1] = 0.0;
+    }
+    for (i64 i = threadIdx.x; i < ngoff; i += kCrossThreads) sgoff[i] = a.goff[i];
+    if (SENT) {
+        const i64 nent = a.goff[ngoff - 1];
+        for (i64 i = threadIdx.x; i < nent / 4; i += kCrossThreads)
+            reinterpret_cast<uint4 *>(sent)[i] = __ldg(reinterpret_cast<const uint4 *>(a.ent) + i);
+        for (i64 i = (nent & ~(i64)3) + threadIdx.x; i < nent; i += kCrossThreads) sent[i] = a.ent[i];
+    }
+    __syncthreads();
+    if (warp == kC) {
+        if (lane != 0) return;
+        const uint32_t bv = (uint32_t)(2 * a.ld * sizeof(double));
+        i64 e = e0, h = 0, pe = e0, ph_ = 0;  // item being issued; item being prefetched
+        auto advance = [&](i64 &ee, i64 &hh) {
+            if (++hh == a.H) { hh = 0; ++ee; }
+        };
+        for (int k = 0; k < 2 && pe < e1; ++k) {  // prefetch window
+            prefetch_l2(a.X + (i64)a.a_sconn[pe].tgt * a.nb + ph_ * a.chunk,
+                        (uint32_t)(min(a.chunk, a.nb - ph_ * a.chunk) * sizeof(double)));
+            advance(pe, ph_);
+        }
+        for (i64 item = 0; item < nitems; ++item) {
+            const int s = (int)(item % kCrossStages);
+            if (item >= kCrossStages) mbar_wait(&empty[s], (uint32_t)(((item / kCrossStages) - 1) & 1));
+            const SConn sa = a.a_sconn[e];
+            const i64 c0 = h * a.chunk, cols = min(a.chunk, a.nb - c0);
+            double *dst = st0 + s * sdbl;
+            const uint32_t bx = (uint32_t)(cols * sizeof(double));
+            mbar_arrive_expect_tx(&full[s], bx + bv);
+            tma_load_1d(dst, a.X + (i64)sa.tgt * a.nb + c0, bx, &full[s]);
+            tma_load_1d(dst + a.chunk + 2, vrow(a, sa), bv, &full[s]);
+            advance(e, h);
+            if (pe < e1) {
+                prefetch_l2(a.X + (i64)a.a_sconn[pe].tgt * a.nb + ph_ * a.chunk,
+                            (uint32_t)(min(a.chunk, a.nb - ph_ * a.chunk) * sizeof(double)));
+                advance(pe, ph_);
+            }
         }
         return;
     }
-    const uint32_t bx = (uint32_t)(nb * sizeof(double)), bv = (uint32_t)(ld_vpp * sizeof(double));
-    auto issue = [&](i64 e, int s) {
-        const SConn sa = a_sconn[e];
-        double *dst = xs0 + s * stage;
-        mbar_arrive_expect_tx(&bar[s], bx + bv);
-        tma_load_1d(dst, X + (i64)sa.tgt * nb, bx, &bar[s]);
-        tma_load_1d(dst + nb, vpp + (i64)(abs(sa.info) - 1) * ld_vpp, bv, &bar[s]);
-    };
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_fence_init();
+    double acc[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) acc[j] = 0.0;
+    i64 e = e0, h = 0;
+    int s = 0;
+    uint32_t ph = 0;
+    for (i64 item = 0; item < nitems; ++item) {
+        mbar_wait(&full[s], ph);
+        const double *xr = st0 + s * sdbl;
+        cross_accumulate<CPT, false>(acc, a, sgoff + h * (a.groups + 1), SENT ? sent : a.ent, xr, xr + a.chunk + 2, 0,
+                                     kC);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == kCrossStages) { s = 0; ph ^= 1u; }
+        if (++h == a.H) {
+            h = 0;
+            const i64 g = a.a_row[e];
+            if (e + 1 == e1 || a.a_row[e + 1] != g) cross_store<CPT>(acc, a, a.Y + (g - a.row_base) * a.nb, 0, kC);
+            ++e;
+        }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        issue(e0, 0);
-        if (e0 + 1 < e1) issue(e0 + 1, 1);
-    }
-    int it = 0;
-    for (i64 e = e0; e < e1; ++e, ++it) {
-        const int s = it & 1;
-        mbar_wait(&bar[s], (uint32_t)((it >> 1) & 1));
-        const SConn sa = a_sconn[e];
-        const i64 g = a_row[e];
-        const double *xr = xs0 + s * stage;
-        cross_entry<true>(xr, xr + nb, sa.info > 0 ? 1.0 : -1.0, e == a_s_off[g], Y + (g - row_base) * nb, nb, ell,
-                          ell_w, ell_ld);
-        __syncthreads();  // stage s fully consumed
-        if (threadIdx.x == 0 && e + 2 < e1) issue(e + 2, s);
+}
+
+// Flat (x rows not 16-byte aligned, or too many groups for one CTA):
+// grid.x = entry ranges, grid.y = tiles of (warps * CPT) groups; gathers and
+// the SELL go through L1/L2.
+template <int CPT>
+__global__ void __launch_bounds__(kCrossThreadsFlat) cross_kernel_flat(CrossArgs a) {
+    constexpr int kW = kCrossThreadsFlat / 32;
+    const i64 g_lo = (i64)blockIdx.y * kW * CPT;
+    const i64 E0 = a.a_s_off[a.row_base], E1 = a.a_s_off[a.row_base + a.n_rows];
+    const i64 tot = E1 - E0;
+    const i64 e0 = snap_entry(E0 + tot * blockIdx.x / gridDim.x, E1, a.a_s_off, a.a_row);
+    const i64 e1 = snap_entry(E0 + tot * (blockIdx.x + 1) / gridDim.x, E1, a.a_s_off, a.a_row);
+    double acc[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) acc[j] = 0.0;
+    for (i64 e = e0; e < e1; ++e) {
+        const SConn sa = a.a_sconn[e];
+        const i64 g = a.a_row[e];
+        for (i64 h = 0; h < a.H; ++h)
+            cross_accumulate<CPT, true>(acc, a, a.goff + h * (a.groups + 1), a.ent, a.X + (i64)sa.tgt * a.nb + h * a.chunk,
+                                        vrow(a, sa), g_lo, kW);
+        if (e + 1 == e1 || a.a_row[e + 1] != g) cross_store<CPT>(acc, a, a.Y + (g - a.row_base) * a.nb, g_lo, kW);
     }
 }
 
@@ -382,6 +488,69 @@ int ensure_scratch(sbd_ctx *ctx) {
     size_t bytes = sizeof(double) * (size_t)std::max<i64>(nb, 1) * ctx->ld_t;
     SBD_CUDA(ctx, ctx->xt.ensure(bytes));
     SBD_CUDA(ctx, ctx->yt.ensure(bytes));
+    return SBD_OK;
+}
+
+template <int CPT, bool SENT>
+int launch_cross_tma(sbd_ctx *ctx, const CrossArgs &ca, size_t smem) {
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        SBD_CUDA(ctx, cudaFuncSetAttribute(cross_kernel_tma<CPT, SENT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+        smem_set = smem;
+    }
+    cross_kernel_tma<CPT, SENT><<<(unsigned)ctx->num_sms, kCrossThreads, smem, ctx->stream>>>(ca);
+    SBD_LAUNCHED(ctx, "cross_kernel_tma");
+    return SBD_OK;
+}
+
+template <bool SENT>
+int launch_cross_tma_cpt(sbd_ctx *ctx, const CrossArgs &ca, size_t smem, i64 cpt) {
+    if (cpt <= 2) return launch_cross_tma<2, SENT>(ctx, ca, smem);
+    if (cpt <= 4) return launch_cross_tma<4, SENT>(ctx, ca, smem);
+    if (cpt <= 8) return launch_cross_tma<8, SENT>(ctx, ca, smem);
+    if (cpt <= 10) return launch_cross_tma<10, SENT>(ctx, ca, smem);
+    if (cpt <= 12) return launch_cross_tma<12, SENT>(ctx, ca, smem);
+    return launch_cross_tma<14, SENT>(ctx, ca, smem);
+}
+
+int launch_cross(sbd_ctx *ctx, const double *x_full, double *y) {
+    const Sector &A = ctx->sec[0], &B = ctx->sec[1];
+    CrossArgs ca{};
+    ca.n_rows = ctx->own_rows();
+    ca.row_base = ctx->own_lo();
+    ca.nb = B.n;
+    ca.X = x_full;
+    ca.Y = y;
+    ca.a_s_off = A.s_off.as<int64_t>();
+    ca.a_sconn = A.sconn.as<SConn>();
+    ca.a_row = A.s_row.as<int32_t>();
+    ca.goff = B.sell_goff.as<int32_t>();
+    ca.col = B.sell_col.as<int32_t>();
+    ca.ent = B.sell_ent.as<uint32_t>();
+    ca.groups = B.sell_groups;
+    ca.H = B.sell_h;
+    ca.chunk = B.sell_chunk;
+    ca.pbits = B.sell_pbits;
+    ca.vsg = ctx->vpp.as<double>();
+    ca.ld = ctx->ld_vpp;
+    constexpr size_t kSmemMax = 227 * 1024;
+    const i64 ngoff = ca.H * (ca.groups + 1);
+    const size_t base = 128 + sizeof(double) * kCrossStages * (size_t)cross_stage_doubles(ca.chunk, ca.ld) +
+                        sizeof(int32_t) * (size_t)((ngoff + 3) & ~(i64)3);
+    const size_t with_ent = base + sizeof(uint32_t) * (size_t)B.sell_nent;
+    const i64 cpt = (ca.groups + kCrossThreads / 32 - 2) / (kCrossThreads / 32 - 1);
+    const char *force = getenv("SBD_CROSS_UNSTAGED");  // test knob: exercise the flat variant
+    const bool staged_ok = !(force && force[0] == '1') && (B.n % 2 == 0) && aligned16(x_full) && cpt <= 14;
+    if (staged_ok && with_ent <= kSmemMax) return launch_cross_tma_cpt<true>(ctx, ca, with_ent, cpt);
+    if (staged_ok && base <= kSmemMax) return launch_cross_tma_cpt<false>(ctx, ca, base, cpt);
+    constexpr int kCpt = 8;
+    const i64 gpt = (i64)(kCrossThreadsFlat / 32) * kCpt;
+    const i64 tiles = std::max<i64>(1, (ca.groups + gpt - 1) / gpt);
+    const unsigned gx = (unsigned)std::max<i64>(1, std::min<i64>((i64)ctx->num_sms * 8 / tiles + 1, ctx->own_rows()));
+    dim3 grid(gx, (unsigned)tiles);
+    cross_kernel_flat<kCpt><<<grid, kCrossThreadsFlat, 0, ctx->stream>>>(ca);
+    SBD_LAUNCHED(ctx, "cross_kernel_flat");
     return SBD_OK;
 }
 
@@ -461,25 +630,8 @@ int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full, double *y) {
     // task 0 exists only when both sectors have in-set singles
     a.a_s_off = (A.ns > 0 && B.ns > 0) ? A.s_off.as<int64_t>() : nullptr;
     if (A.ns > 0 && B.ns > 0) {
-        const size_t smem = 128 + sizeof(double) * 2 * (size_t)(nb + ctx->ld_vpp);
-        const bool staged = (nb % 2 == 0) && aligned16(x_full) && smem <= 220 * 1024;
-        const unsigned grid = (unsigned)ctx->num_sms;
-        if (staged) {
-            static size_t smem_set = 0;
-            if (smem > smem_set) {
-                SBD_CUDA(ctx, cudaFuncSetAttribute(cross_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)smem));
-                smem_set = smem;
-            }
-            cross_kernel<true><<<grid, kCrossThreads, smem, ctx->stream>>>(
-                rows, ctx->own_lo(), nb, x_full, y, A.s_off.as<int64_t>(), A.sconn.as<SConn>(),
-                A.s_row.as<int32_t>(), B.ell.as<uint32_t>(), B.ell_w, B.ell_ld, ctx->vpp.as<double>(), ctx->ld_vpp);
-        } else {
-            cross_kernel<false><<<grid * 2, kCrossThreads, 0, ctx->stream>>>(
-                rows, ctx->own_lo(), nb, x_full, y, A.s_off.as<int64_t>(), A.sconn.as<SConn>(),
-                A.s_row.as<int32_t>(), B.ell.as<uint32_t>(), B.ell_w, B.ell_ld, ctx->vpp.as<double>(), ctx->ld_vpp);
-        }
-        SBD_LAUNCHED(ctx, "cross_kernel");
+        rc = launch_cross(ctx, x_full, y);
+        if (rc) return rc;
     }
     dim3 g((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kColsPerWarp - 1) / kColsPerWarp));
     const bool vec = (nb % 2 == 0) && aligned16(x_full) && aligned16(y);

@@ -156,13 +156,21 @@ def test_cfg2_full_size_properties():
     assert np.array_equal(ys, hx.cpu().numpy())
 
 
-def test_random_instances_vs_oracle():
-    """Ragged random sets across shapes, incl. odd n_beta (scalar path) and 1-string sectors."""
+@pytest.mark.parametrize("unstaged", [False, True])
+def test_random_instances_vs_oracle(unstaged, monkeypatch):
+    """Ragged random sets across shapes, incl. odd n_beta (scalar path) and 1-string sectors.
+
+    ``unstaged`` forces the task-0 kernel variant that gathers through L1/L2
+    (used when an x row does not fit shared memory); the (14, 2, 7) case has
+    3432 beta strings, i.e. two column tiles of that variant.
+    """
     from paper_2601_16637_b200 import HamiltonianApplier, SelectedBasis
     from paper_2601_16637_b200.synth import random_integrals, random_product_strings
 
+    if unstaged:
+        monkeypatch.setenv("SBD_CROSS_UNSTAGED", "1")
     cases = [(10, 5, 4, 77, 131, 1), (14, 3, 4, 301, 257, 2), (16, 8, 8, 500, 1, 3), (16, 8, 8, 1, 499, 4),
-             (12, 6, 6, 924, 129, 5), (20, 2, 9, 190, 600, 6)]
+             (12, 6, 6, 924, 129, 5), (20, 2, 9, 190, 600, 6), (14, 2, 7, 40, 3432, 7)]
     for norb, na, nb, nsa, nsb, seed in cases:
         a, _ = random_product_strings(norb, na, na, nsa, 1, seed)
         _, b = random_product_strings(norb, nb, nb, 1, nsb, seed + 100)
