@@ -1122,6 +1122,184 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(const double *__res
     }
 }
 
+// ---------------------------------------------------------------------------
+// Register-streaming passes (16-byte aligned operands, K <= 32).  A thread owns
+// element pairs (128-bit loads) and walks all k vectors of the pair itself, so
+// no cross-warp reduction or barrier sits inside the stream and each thread
+// keeps up to 2k independent loads in flight.  The dot-product phase re-reads
+// the k V pairs the same thread just loaded (L2 hits: only the first touch
+// costs HBM).  Per-thread accumulators are reduced once at the end.
+constexpr int kRegBlock = 256;
+
+template <int K, int NA>
+__device__ __forceinline__ void block_store_partials(double (&acc)[NA], double *__restrict__ partial, int stride) {
+    __shared__ double red[kRegBlock / 32][NA];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+        const double v = warp_sum(acc[i]);
+        if (lane == 0) red[warp][i] = v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < NA; i += blockDim.x) {
+        double sum = 0.0;
+        for (int w = 0; w < kRegBlock / 32; ++w) sum += red[w][i];
+        partial[(i64)blockIdx.x * stride + i] = sum;
+    }
+}
+
+__device__ __forceinline__ double precond_div(double r, double d, double th, double delta) {
+    const double g = d - th;
+    return r / ((g >= 0.0 ? 1.0 : -1.0) * fmax(fabs(g), delta));
+}
+
+// Residuals, preconditioned corrections and V^T t_jp (davidson.py:252-258,159-163).
+// partial per block (stride K+1+M): [0,K) dots | K: |t_jp|^2 | K+1+j: |r_j|^2
+template <int K, int M>
+__global__ void __launch_bounds__(kRegBlock, 2)
+residual_reg(const double *__restrict__ V, const double *__restrict__ W, int k, i64 ldv, i64 n,
+             const double *__restrict__ Y, const double *__restrict__ theta, int m, int jp,
+             const double *__restrict__ diag, double delta, double *__restrict__ T, i64 ldt,
+             double *__restrict__ partial) {
+    __shared__ double ys[K * M];
+    __shared__ double th[M];
+    for (int idx = threadIdx.x; idx < K * M; idx += blockDim.x) {
+        const int i = idx / M, j = idx % M;
+        ys[idx] = (i < k && j < m) ? Y[i * m + j] : 0.0;
+    }
+    if (threadIdx.x < M) th[threadIdx.x] = threadIdx.x < m ? theta[threadIdx.x] : 0.0;
+    __syncthreads();
+    constexpr int NA = K + 1 + M;
+    double acc[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) acc[i] = 0.0;
+    const i64 np = n / 2;
+    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (i64)gridDim.x * blockDim.x) {
+        double2 u[M], wy[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) u[j] = wy[j] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            if (i < k) {
+                const double2 v = reinterpret_cast<const double2 *>(V + i * ldv)[p];
+                const double2 w = __ldcs(reinterpret_cast<const double2 *>(W + i * ldv) + p);
+#pragma unroll
+                for (int j = 0; j < M; ++j) {
+                    const double y = ys[i * M + j];
+                    u[j].x = fma(y, v.x, u[j].x);
+                    u[j].y = fma(y, v.y, u[j].y);
+                    wy[j].x = fma(y, w.x, wy[j].x);
+                    wy[j].y = fma(y, w.y, wy[j].y);
+                }
+            }
+        }
+        const double2 d = __ldcs(reinterpret_cast<const double2 *>(diag) + p);
+        double2 tj = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            if (j < m) {
+                const double rx = wy[j].x - th[j] * u[j].x, ry = wy[j].y - th[j] * u[j].y;
+                const double2 t = make_double2(precond_div(rx, d.x, th[j], delta), precond_div(ry, d.y, th[j], delta));
+                __stcs(reinterpret_cast<double2 *>(T + j * ldt) + p, t);
+                acc[K + 1 + j] = fma(rx, rx, fma(ry, ry, acc[K + 1 + j]));
+                if (j == jp) tj = t;
+            }
+        }
+        acc[K] = fma(tj.x, tj.x, fma(tj.y, tj.y, acc[K]));
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            if (i < k) {
+                const double2 v = __ldcs(reinterpret_cast<const double2 *>(V + i * ldv) + p);
+                acc[i] = fma(v.x, tj.x, fma(v.y, tj.y, acc[i]));
+            }
+        }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail element
+        const i64 e = n - 1;
+        double u[M], wy[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) u[j] = wy[j] = 0.0;
+        for (int i = 0; i < k; ++i)
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+                u[j] = fma(ys[i * M + j], V[i * ldv + e], u[j]);
+                wy[j] = fma(ys[i * M + j], W[i * ldv + e], wy[j]);
+            }
+        double tj = 0.0;
+#pragma unroll
+        for (int j = 0; j < M; ++j)
+            if (j < m) {
+                const double r = wy[j] - th[j] * u[j];
+                const double t = precond_div(r, diag[e], th[j], delta);
+                T[j * ldt + e] = t;
+                acc[K + 1 + j] = fma(r, r, acc[K + 1 + j]);
+                if (j == jp) tj = t;
+            }
+        acc[K] = fma(tj, tj, acc[K]);
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (i < k) acc[i] = fma(V[i * ldv + e], tj, acc[i]);
+    }
+    block_store_partials<K, NA>(acc, partial, NA);
+}
+
+// t_new = t - V c ; out = scale * t_new (out may alias t) ; dots V_i . t_new (i < kdot) ; |t_new|^2
+// partial per block (stride K+1): [0,K) dots | K: |t_new|^2
+template <int K, bool DOTS>
+__global__ void __launch_bounds__(kRegBlock, 2)
+gs_reg(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__restrict__ c, int kdot, const double *t,
+       double *out, const double *__restrict__ scale, double *__restrict__ partial) {
+    __shared__ double cs[K];
+    for (int i = threadIdx.x; i < K; i += blockDim.x) cs[i] = i < k ? c[i] : 0.0;
+    __syncthreads();
+    const double sc = scale ? *scale : 1.0;
+    constexpr int NA = K + 1;
+    double acc[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) acc[i] = 0.0;
+    const i64 np = n / 2;
+    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (i64)gridDim.x * blockDim.x) {
+        double2 tv = reinterpret_cast<const double2 *>(t)[p];
+#pragma unroll
+        for (int i0 = 0; i0 < K; i0 += 8) {  // 8 independent loads ahead of each FMA chain
+            double2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (i0 + u < k)
+                    v[u] = DOTS ? reinterpret_cast<const double2 *>(V + (i0 + u) * ldv)[p]
+                                : __ldcs(reinterpret_cast<const double2 *>(V + (i0 + u) * ldv) + p);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (i0 + u < k) {
+                    tv.x = fma(-cs[i0 + u], v[u].x, tv.x);
+                    tv.y = fma(-cs[i0 + u], v[u].y, tv.y);
+                }
+        }
+        reinterpret_cast<double2 *>(out)[p] = make_double2(tv.x * sc, tv.y * sc);
+        acc[K] = fma(tv.x, tv.x, fma(tv.y, tv.y, acc[K]));
+        if (DOTS) {
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                if (i < kdot) {
+                    const double2 v = __ldcs(reinterpret_cast<const double2 *>(V + i * ldv) + p);  // L2 hit
+                    acc[i] = fma(v.x, tv.x, fma(v.y, tv.y, acc[i]));
+                }
+            }
+        }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const i64 e = n - 1;
+        double x = t[e];
+        for (int i = 0; i < k; ++i) x = fma(-cs[i], V[i * ldv + e], x);
+        out[e] = x * sc;
+        acc[K] = fma(x, x, acc[K]);
+#pragma unroll
+        for (int i = 0; i < K; ++i)
+            if (i < kdot) acc[i] = fma(V[i * ldv + e], x, acc[i]);
+    }
+    block_store_partials<K, NA>(acc, partial, NA);
+}
+
 inline bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 inline bool vec_ok(const double *V, i64 ldv) { return al16(V) && ldv % 2 == 0; }
 template <class... P>
@@ -1134,6 +1312,15 @@ inline bool use_tma() {
     if (v < 0) {
         const char *e = getenv("SBD_NO_TMA");
         v = (e && *e && *e != '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+inline bool use_reg() {  // SBD_DAV_TMA=1 selects the TMA-staged passes (A/B measurements)
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SBD_DAV_TMA");
+        v = (e && *e == '1') ? 0 : 1;
     }
     return v == 1;
 }
@@ -1209,6 +1396,12 @@ struct ResidL {
     static std::pair<int, int> launch(sbd_ctx *ctx, int nb, const double *V, const double *W, int k, i64 ldv, i64 n,
                                       const double *Y, const double *theta, int m, int jp, const double *diag,
                                       double delta, double *T, i64 ldt) {
+        if (K <= 32 && M <= 2 && vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_reg()) {
+            const int nt = ctx->num_sms * 2;
+            residual_reg<(K <= 32 ? K : 32), M><<<nt, kRegBlock, 0, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp,
+                                                                                 diag, delta, T, ldt, ctx->red.as<double>());
+            return {nt, K + 1 + M};
+        }
         const int TTA = tma_tile(2 * k + 1);
         const size_t smem_tma = 128 + sizeof(double) * (2 * (size_t)(2 * k + 1) * TTA + TTA + 2 * 8 * M * (size_t)TTA);
         if (vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_tma() && smem_tma <= 220 * 1024 &&
@@ -1264,6 +1457,18 @@ struct GsL {
         int nb = red_blocks(ctx, n);
         if (int rc = ensure_red(ctx, nb, K + 1)) return rc;
         double *dst = out_vec ? out_vec : t;
+        if (K <= 32 && vec_ok(V, ldv, t) && al16(dst) && use_reg()) {
+            const int nt = ctx->num_sms * 2;
+            if (kdot > 0)
+                gs_reg<(K <= 32 ? K : 32), true><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale,
+                                                                                  ctx->red.as<double>());
+            else
+                gs_reg<(K <= 32 ? K : 32), false><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst,
+                                                                                   scale, ctx->red.as<double>());
+            finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
+            SBD_LAUNCHED(ctx, "gs_update");
+            return SBD_OK;
+        }
         if (vec_ok(V, ldv, t) && use_tma()) {
             const int TTA = tma_tile(k + 1);
             const size_t smem = 128 + sizeof(double) * 2 * (size_t)(k + 1) * TTA;

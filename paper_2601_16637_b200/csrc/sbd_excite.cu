@@ -287,7 +287,7 @@ static int build_sell(sbd_ctx *ctx, Sector &s) {
     SBD_CUDA(ctx, cudaMemcpyAsync(off.data(), s.s_off.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
     if (s.ns) SBD_CUDA(ctx, cudaMemcpyAsync(sc.data(), s.sconn.p, sizeof(SConn) * s.ns, cudaMemcpyDeviceToHost, st));
     SBD_CUDA(ctx, cudaStreamSynchronize(st));
-    const i64 H = std::max<i64>(1, (n + kSellChunk - 1) / kSellChunk);
+    const i64 H = n <= kSellWhole ? 1 : (n + kSellChunk - 1) / kSellChunk;
     const i64 chunk = std::max<i64>(2, ((n + H - 1) / H + 1) & ~(i64)1);  // even: 16-byte TMA rows
     int pbits = 1;
     while (((i64)1 << pbits) < 2 * ctx->ld_vpp) ++pbits;
@@ -339,6 +339,7 @@ static int build_sell(sbd_ctx *ctx, Sector &s) {
     }
     for (size_t i = 0; i < go.size(); ++i) go[i] = (int32_t)goff[i];
     s.sell_groups = groups;
+    s.sell_goff_host = go;
     s.sell_nent = total;
     s.sell_h = H;
     s.sell_chunk = chunk;

@@ -61,6 +61,7 @@ struct Sector {
     DevBuf sell_goff;        // int32[sell_h][groups+1]
     DevBuf sell_col;         // int32[groups*32]: string at each position (-1: padding)
     i64 sell_groups = 0, sell_nent = 0, sell_h = 1, sell_chunk = 0;
+    std::vector<int32_t> sell_goff_host;  // host copy of sell_goff
     int sell_pbits = 1;
     bool built = false;
 };
@@ -121,7 +122,10 @@ int sbd_sort_strings(sbd_ctx *ctx, Sector &s);              // sbd_strings.cu
 int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s);       // sbd_excite.cu
 int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other);  // sbd_excite.cu
 
-constexpr i64 kSellChunk = 3584;  // strings per staged chunk of an x row (28 KB)
+// x rows of up to kSellWhole strings are staged whole (H = 1, cluster kernel);
+// longer rows in chunks of at most kSellChunk strings (28 KB)
+constexpr i64 kSellWhole = 12288;
+constexpr i64 kSellChunk = 3584;
 constexpr int kPackPairBits = 12;   // orbital pair index < 4096 (norb <= 64 gives 2080)
 constexpr i64 kPackMaxStrings = (i64)1 << 19;  // target index in the remaining 19 bits
 

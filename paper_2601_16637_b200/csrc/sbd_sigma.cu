@@ -195,6 +195,150 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
     }
 }
 
+// Asynchronous-copy variant of side_kernel (16-byte aligned rows).  A warp
+// owns one output row and a tile of kTW = 256 columns; each lane streams its
+// own 8 columns of every connection's x row segment with cp.async (16-byte
+// LDGSTS, L1 bypass) into a private ring of kRing shared-memory slots, so
+// kRing segments per lane are in flight without holding registers -- the
+// register-staged version is latency-bound at ~100 KB in flight per SM.  A
+// lane only ever reads back the bytes it copied itself, so cp.async.wait_group
+// is the only synchronisation (no barriers in the stream).
+constexpr int kTW = 256;
+
+template <bool ALPHA>
+struct SideAsync {
+    static constexpr int kRing = ALPHA ? 3 : 4;
+    static constexpr size_t smem() { return sizeof(double) * (size_t)kRowsPerCta * kRing * kTW; }
+};
+
+__device__ __forceinline__ void cp_async16(void *dst_smem, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <bool ALPHA>
+__global__ void __launch_bounds__(kRowsPerCta * 32, 3) side_kernel_async(SideArgs a) {
+    constexpr int R = SideAsync<ALPHA>::kRing;
+    extern __shared__ __align__(128) unsigned char ssm[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *ring = reinterpret_cast<double *>(ssm) + (size_t)w * R * kTW;
+    const i64 r = (i64)blockIdx.x * kRowsPerCta + w;
+    const i64 c0 = (i64)blockIdx.y * kTW;
+    const i64 ncol = min((i64)kTW, a.n_cols - c0);
+    const bool row_ok = r < a.n_rows;
+    bool ok[8], pair[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        ok[2 * h] = 2 * lane + 64 * h < ncol;
+        ok[2 * h + 1] = 2 * lane + 64 * h + 1 < ncol;
+        pair[h] = ok[2 * h];  // rows are padded to even length: the pair is readable
+    }
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    if (row_ok) {
+        const i64 g = a.row_base + r;
+        const i64 e0 = a.conn_off[g], n = a.conn_off[g + 1] - e0;
+        auto issue = [&](i64 i, int slot) {
+            if (i < n) {
+                const double *src = a.X + (i64)a.conn[e0 + i].tgt * a.ldx + c0;
+                double *dst = ring + (size_t)slot * kTW;
+#pragma unroll
+                for (int h = 0; h < 4; ++h)
+                    if (pair[h]) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
+            }
+            cp_async_commit();
+        };
+#pragma unroll
+        for (int i = 0; i < R - 1; ++i) issue(i, i);
+        int slot = 0;
+        for (i64 i = 0; i < n; ++i) {
+            issue(i + R - 1, slot == 0 ? R - 1 : slot - 1);
+            const Conn cn = a.conn[e0 + i];
+            cp_async_wait<R - 1>();
+            const double *src = ring + (size_t)slot * kTW;
+            double2 v[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) v[h] = *reinterpret_cast<const double2 *>(src + 2 * lane + 64 * h);
+            if (cn.info == 0) {
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    acc[2 * h] = fma(cn.c, v[h].x, acc[2 * h]);
+                    acc[2 * h + 1] = fma(cn.c, v[h].y, acc[2 * h + 1]);
+                }
+            } else {
+                const int P = abs(cn.info) - 1;
+                const double sg = cn.info > 0 ? 1.0 : -1.0;
+                const double *jr = a.J + (i64)P * a.ldj + a.col_base + c0;
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int cc = 2 * lane + 64 * h;
+                    const double j0 = ok[2 * h] ? __ldg(jr + cc) : 0.0, j1 = ok[2 * h + 1] ? __ldg(jr + cc + 1) : 0.0;
+                    acc[2 * h] = fma(fma(sg, j0, cn.c), v[h].x, acc[2 * h]);
+                    acc[2 * h + 1] = fma(fma(sg, j1, cn.c), v[h].y, acc[2 * h + 1]);
+                }
+            }
+            if (++slot == R) slot = 0;
+        }
+        cp_async_wait<0>();
+    }
+
+    if (ALPHA) {
+        // + (B X^T)^T : tile YT[c0:c0+256, r0:r0+8] through shared memory
+        __shared__ double tile[kTW][kRowsPerCta + 1];
+        const i64 r0 = (i64)blockIdx.x * kRowsPerCta;
+        {
+            const int i = threadIdx.x;  // one column of the tile per thread
+            if (i < ncol) {
+                const double2 *srcp = reinterpret_cast<const double2 *>(a.YT + (c0 + i) * a.ldyt + r0);
+#pragma unroll
+                for (int q = 0; q < kRowsPerCta / 2; ++q) {
+                    const double2 u = srcp[q];
+                    tile[i][2 * q] = u.x;
+                    tile[i][2 * q + 1] = u.y;
+                }
+            }
+        }
+        __syncthreads();
+        if (row_ok) {
+            const i64 g = a.row_base + r;
+            const double *drow = a.diag + r * a.ldy + c0, *xrow = a.X + g * a.ldx + c0;
+            const bool t0 = a.a_s_off != nullptr && a.a_s_off[g + 1] != a.a_s_off[g];
+            const double *yrow = a.Y + r * a.ldy + c0;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int cc = 2 * lane + 64 * h;
+                if (ok[2 * h + 1]) {
+                    const double2 d = __ldcs(reinterpret_cast<const double2 *>(drow + cc));
+                    const double2 x = __ldg(reinterpret_cast<const double2 *>(xrow + cc));
+                    acc[2 * h] = fma(d.x, x.x, acc[2 * h] + tile[cc][w]);
+                    acc[2 * h + 1] = fma(d.y, x.y, acc[2 * h + 1] + tile[cc + 1][w]);
+                    if (t0) {
+                        const double2 p = *reinterpret_cast<const double2 *>(yrow + cc);
+                        acc[2 * h] += p.x;
+                        acc[2 * h + 1] += p.y;
+                    }
+                } else if (ok[2 * h]) {
+                    acc[2 * h] = fma(drow[cc], xrow[cc], acc[2 * h] + tile[cc][w]);
+                    if (t0) acc[2 * h] += yrow[cc];
+                }
+            }
+        }
+    }
+
+    if (row_ok) {
+        double *yr = a.Y + r * a.ldy + c0;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int cc = 2 * lane + 64 * h;
+            if (ok[2 * h + 1]) __stcs(reinterpret_cast<double2 *>(yr + cc), make_double2(acc[2 * h], acc[2 * h + 1]));
+            else if (ok[2 * h]) yr[cc] = acc[2 * h];
+        }
+    }
+}
+
 // Task 0, the alpha-single x beta-single opposite-spin doubles (apply.py:235-238):
 //   Y[r, ib] = sum_{k in aS(g)} s_k sum_{m in bS(ib)} s_m (Pa_k | Pb_m) X[ja_k, jb_m]
 // written for rows that have alpha singles (the streaming kernel adds it).
@@ -394,6 +538,135 @@ __global__ void __launch_bounds__(kCrossThreads, 1) cross_kernel_tma(CrossArgs a
     }
 }
 
+// Cluster variant (H = 1, whole x rows): a pair of CTAs on two SMs shares
+// every entry's x row and ERI row through one TMA multicast (one L2/HBM read
+// feeds both shared memories); CTA rank r owns the SELL groups g = 2 gl + r,
+// so each CTA keeps only half of the SELL resident and each lane half as
+// many accumulators.  Stage release spans the pair: rank 1's producer arms
+// its own full barrier and then arrives on rank 0's `peer` barrier; rank 0's
+// producer issues the multicast once both CTAs released the stage.
+constexpr int kMcStages = 2;
+
+__host__ __device__ inline i64 mc_local_groups(i64 groups, int rank) { return (groups - rank + 1) / 2; }
+
+template <int CPT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrossThreads, 1) cross_kernel_mc(CrossArgs a) {
+    extern __shared__ __align__(128) unsigned char csm[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(csm);
+    uint64_t *empty = full + kMcStages;
+    uint64_t *peer = empty + kMcStages;
+    double *st0 = reinterpret_cast<double *>(csm + 128);
+    const i64 sdbl = cross_stage_doubles(a.chunk, a.ld);
+    const int rank = (int)cluster_ctarank();
+    const i64 ngl = mc_local_groups(a.groups, rank);
+    int32_t *lgoff = reinterpret_cast<int32_t *>(st0 + kMcStages * sdbl);
+    uint32_t *sent = reinterpret_cast<uint32_t *>(lgoff + ((ngl + 4) & ~(i64)3));
+    constexpr int kC = kCrossThreads / 32 - 1;  // consumer warps
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const i64 cl = blockIdx.x / 2, ncl = gridDim.x / 2;
+    const i64 E0 = a.a_s_off[a.row_base], E1 = a.a_s_off[a.row_base + a.n_rows];
+    const i64 tot = E1 - E0;
+    const i64 e0 = snap_entry(E0 + tot * cl / ncl, E1, a.a_s_off, a.a_row);
+    const i64 e1 = snap_entry(E0 + tot * (cl + 1) / ncl, E1, a.a_s_off, a.a_row);
+    const i64 nitems = e1 - e0;  // both CTAs of the pair see the same range
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kMcStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kC);
+            mbar_init(&peer[i], 1);
+        }
+        mbar_fence_init();
+        // local group offsets (prefix over this rank's groups)
+        int32_t o = 0;
+        for (i64 gl = 0; gl < ngl; ++gl) {
+            const i64 g = 2 * gl + rank;
+            lgoff[gl] = o;
+            o += a.goff[g + 1] - a.goff[g];
+        }
+        lgoff[ngl] = o;
+    }
+    if (threadIdx.x < kMcStages) {  // zero slots read by padding entries
+        st0[threadIdx.x * sdbl + a.chunk] = 0.0;
+        st0[threadIdx.x * sdbl + a.chunk + 1] = 0.0;
+    }
+    __syncthreads();
+    for (i64 gl = warp; gl < ngl; gl += kCrossThreads / 32) {  // this rank's SELL into shared memory
+        const i64 g = 2 * gl + rank;
+        const int src = a.goff[g], cnt = a.goff[g + 1] - src, dst = lgoff[gl];
+        for (int i = lane; i < cnt; i += 32) sent[dst + i] = __ldg(a.ent + src + i);
+    }
+    cluster_sync_all();  // barriers of both CTAs initialised before any remote traffic
+    if (warp == kC) {
+        if (lane == 0 && nitems > 0) {
+            const uint32_t bv = (uint32_t)(2 * a.ld * sizeof(double));
+            const uint32_t bx = (uint32_t)(a.nb * sizeof(double));
+            const uint32_t peer0 = cluster_map(&peer[0], 0);
+            for (i64 item = 0; item < nitems; ++item) {
+                const int s = (int)(item & 1);
+                const uint32_t use = (uint32_t)(item >> 1);
+                if (item >= kMcStages) mbar_wait(&empty[s], (use - 1) & 1);
+                mbar_arrive_expect_tx(&full[s], bx + bv);
+                if (rank == 1) {
+                    mbar_arrive_remote(peer0 + (uint32_t)(s * sizeof(uint64_t)));
+                } else {
+                    mbar_wait_cluster(&peer[s], use & 1);
+                    const SConn sa = a.a_sconn[e0 + item];
+                    double *dst = st0 + s * sdbl;
+                    tma_load_1d_multicast(dst, a.X + (i64)sa.tgt * a.nb, bx, &full[s], 0x3);
+                    tma_load_1d_multicast(dst + a.chunk + 2, vrow(a, sa), bv, &full[s], 0x3);
+                }
+            }
+        }
+    } else {
+        double acc[CPT];
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) acc[j] = 0.0;
+        for (i64 item = 0; item < nitems; ++item) {
+            const int s = (int)(item & 1);
+            mbar_wait(&full[s], (uint32_t)((item >> 1) & 1));
+            const double *xr = st0 + s * sdbl;
+            const double *vr = xr + a.chunk + 2;
+            const uint32_t pmask = (1u << a.pbits) - 1u;
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) {
+                const i64 gl = warp + (i64)j * kC;
+                if (gl < ngl) {
+                    const int o0 = lgoff[gl], w = (lgoff[gl + 1] - o0) >> 5;
+                    const uint32_t *ep = sent + o0 + lane;
+                    int q = 0;
+                    for (; q + 2 <= w; q += 2) {
+                        const uint32_t p0 = ep[32 * q], p1 = ep[32 * q + 32];
+                        const double t0 = vr[p0 & pmask] * xr[p0 >> a.pbits];
+                        acc[j] = fma(vr[p1 & pmask], xr[p1 >> a.pbits], acc[j] + t0);
+                    }
+                    if (q < w) {
+                        const uint32_t p0 = ep[32 * q];
+                        acc[j] = fma(vr[p0 & pmask], xr[p0 >> a.pbits], acc[j]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            const i64 e = e0 + item, g = a.a_row[e];
+            if (e + 1 == e1 || a.a_row[e + 1] != g) {
+                double *yr = a.Y + (g - a.row_base) * a.nb;
+                int c[CPT];
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) {
+                    const i64 gl = warp + (i64)j * kC;
+                    c[j] = gl < ngl ? __ldg(a.col + (2 * gl + rank) * 32 + lane) : -1;
+                }
+#pragma unroll
+                for (int j = 0; j < CPT; ++j) {
+                    if (c[j] >= 0) yr[c[j]] = acc[j];
+                    acc[j] = 0.0;
+                }
+            }
+        }
+    }
+    cluster_sync_all();  // no CTA leaves while its pair may still signal it
+}
+
 // Flat (x rows not 16-byte aligned, or too many groups for one CTA):
 // grid.x = entry ranges, grid.y = tiles of (warps * CPT) groups; gathers and
 // the SELL go through L1/L2.
@@ -459,6 +732,11 @@ __global__ void diag_kernel(i64 n_rows, i64 row_base, i64 nb, const u64 *__restr
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+bool use_side_tma() {  // SBD_SIDE_LDG=1 selects the register-staged stream (A/B measurements)
+    const char *e = getenv("SBD_SIDE_LDG");
+    return !(e && e[0] == '1');
+}
+
 int require_ready(sbd_ctx *ctx) {
     if (!ctx->sec[0].built || !ctx->sec[1].built)
         return sbd_fail(ctx, SBD_EINVAL, "tables not built (call sbd_build_tables)");
@@ -504,6 +782,18 @@ int launch_cross_tma(sbd_ctx *ctx, const CrossArgs &ca, size_t smem) {
     return SBD_OK;
 }
 
+template <int CPT>
+int launch_cross_mc(sbd_ctx *ctx, const CrossArgs &ca, size_t smem) {
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        SBD_CUDA(ctx, cudaFuncSetAttribute(cross_kernel_mc<CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set = smem;
+    }
+    cross_kernel_mc<CPT><<<(unsigned)ctx->num_sms, kCrossThreads, smem, ctx->stream>>>(ca);
+    SBD_LAUNCHED(ctx, "cross_kernel_mc");
+    return SBD_OK;
+}
+
 template <bool SENT>
 int launch_cross_tma_cpt(sbd_ctx *ctx, const CrossArgs &ca, size_t smem, i64 cpt) {
     if (cpt <= 2) return launch_cross_tma<2, SENT>(ctx, ca, smem);
@@ -541,6 +831,23 @@ int launch_cross(sbd_ctx *ctx, const double *x_full, double *y) {
     const size_t with_ent = base + sizeof(uint32_t) * (size_t)B.sell_nent;
     const i64 cpt = (ca.groups + kCrossThreads / 32 - 2) / (kCrossThreads / 32 - 1);
     const char *force = getenv("SBD_CROSS_UNSTAGED");  // test knob: exercise the flat variant
+    const char *nomc = getenv("SBD_CROSS_NO_CLUSTER");  // test knob: exercise the single-CTA pipeline
+    if (!(force && force[0] == '1') && !(nomc && nomc[0] == '1') && ca.H == 1 && (B.n % 2 == 0) &&
+        aligned16(x_full) && (ctx->num_sms % 2 == 0)) {
+        const i64 ngl = mc_local_groups(ca.groups, 0);
+        i64 ent0 = 0, ent1 = 0;  // SELL entries per rank (host copy of the offsets)
+        for (i64 g = 0; g < ca.groups; ++g) (g % 2 ? ent1 : ent0) += B.sell_goff_host[g + 1] - B.sell_goff_host[g];
+        const size_t smem_mc = 128 + sizeof(double) * kMcStages * (size_t)cross_stage_doubles(ca.chunk, ca.ld) +
+                               sizeof(int32_t) * (size_t)((ngl + 4) & ~(i64)3) +
+                               sizeof(uint32_t) * (size_t)std::max(ent0, ent1);
+        const i64 cpt_mc = (ngl + kCrossThreads / 32 - 2) / (kCrossThreads / 32 - 1);
+        if (smem_mc <= kSmemMax && cpt_mc <= 8) {
+            if (cpt_mc <= 2) return launch_cross_mc<2>(ctx, ca, smem_mc);
+            if (cpt_mc <= 4) return launch_cross_mc<4>(ctx, ca, smem_mc);
+            if (cpt_mc <= 6) return launch_cross_mc<6>(ctx, ca, smem_mc);
+            return launch_cross_mc<8>(ctx, ca, smem_mc);
+        }
+    }
     const bool staged_ok = !(force && force[0] == '1') && (B.n % 2 == 0) && aligned16(x_full) && cpt <= 14;
     if (staged_ok && with_ent <= kSmemMax) return launch_cross_tma_cpt<true>(ctx, ca, with_ent, cpt);
     if (staged_ok && base <= kSmemMax) return launch_cross_tma_cpt<false>(ctx, ca, base, cpt);
@@ -596,8 +903,19 @@ int sbd_sigma_local(sbd_ctx *ctx, const double *x_own) {
     a.conn = B.conn.as<Conn>();
     a.J = A.J.as<double>();
     a.ldj = A.n;
-    dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((rows + kColsPerWarp - 1) / kColsPerWarp));
-    side_kernel<true, false><<<g, kRowsPerCta * 32, 0, st>>>(a);
+    if (use_side_tma() && aligned16(a.X) && a.ldx % 2 == 0) {
+        static bool attr = false;
+        if (!attr) {
+            SBD_CUDA(ctx, cudaFuncSetAttribute(side_kernel_async<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)SideAsync<false>::smem()));
+            attr = true;
+        }
+        dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((rows + kTW - 1) / kTW));
+        side_kernel_async<false><<<g, kRowsPerCta * 32, SideAsync<false>::smem(), st>>>(a);
+    } else {
+        dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((rows + kColsPerWarp - 1) / kColsPerWarp));
+        side_kernel<true, false><<<g, kRowsPerCta * 32, 0, st>>>(a);
+    }
     SBD_LAUNCHED(ctx, "side_kernel<beta>");
     return SBD_OK;
 }
@@ -635,8 +953,20 @@ int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full, double *y) {
     }
     dim3 g((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kColsPerWarp - 1) / kColsPerWarp));
     const bool vec = (nb % 2 == 0) && aligned16(x_full) && aligned16(y);
-    if (vec) side_kernel<true, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
-    else side_kernel<false, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
+    if (vec && use_side_tma()) {
+        static bool attr = false;
+        if (!attr) {
+            SBD_CUDA(ctx, cudaFuncSetAttribute(side_kernel_async<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)SideAsync<true>::smem()));
+            attr = true;
+        }
+        dim3 gt((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kTW - 1) / kTW));
+        side_kernel_async<true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
+    } else if (vec) {
+        side_kernel<true, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
+    } else {
+        side_kernel<false, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
+    }
     SBD_LAUNCHED(ctx, "side_kernel<alpha>");
     return SBD_OK;
 }
