@@ -80,6 +80,11 @@ int sbd_destroy(sbd_ctx *ctx) {
     if (!ctx) return SBD_OK;
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+    }
+    for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
     delete ctx;
     return SBD_OK;
 }

@@ -1148,6 +1148,19 @@ __device__ __forceinline__ void block_store_partials(double (&acc)[NA], double *
     }
 }
 
+// Lane 0 of each warp bulk-prefetches, into L2, the 32 element pairs (512 B)
+// the warp touches kPfDist grid-stride iterations ahead in vector v.  With
+// kPfDist = 0 the whole iteration's slices of all k vectors are requested at
+// once, so the thread's register-staged loads (8 vectors at a time) find them
+// in L2 instead of paying one HBM latency per group of 8.
+constexpr int kPfDist = 0;
+__device__ __forceinline__ void warp_prefetch(const double *v, i64 p_warp_next, i64 np) {
+    if (p_warp_next < np) {
+        const i64 cnt = min((i64)32, np - p_warp_next);
+        prefetch_l2(v + 2 * p_warp_next, (uint32_t)(cnt * 16));
+    }
+}
+
 __device__ __forceinline__ double precond_div(double r, double d, double th, double delta) {
     const double g = d - th;
     return r / ((g >= 0.0 ? 1.0 : -1.0) * fmax(fabs(g), delta));
@@ -1174,7 +1187,16 @@ residual_reg(const double *__restrict__ V, const double *__restrict__ W, int k, 
 #pragma unroll
     for (int i = 0; i < NA; ++i) acc[i] = 0.0;
     const i64 np = n / 2;
-    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (i64)gridDim.x * blockDim.x) {
+    const i64 stride = (i64)gridDim.x * blockDim.x;
+    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += stride) {
+        if ((threadIdx.x & 31) == 0) {
+            const i64 pn = p + kPfDist * stride;
+            for (int i = 0; i < k; ++i) {
+                warp_prefetch(V + i * ldv, pn, np);
+                warp_prefetch(W + i * ldv, pn, np);
+            }
+            warp_prefetch(diag, pn, np);
+        }
         double2 u[M], wy[M];
 #pragma unroll
         for (int j = 0; j < M; ++j) u[j] = wy[j] = make_double2(0.0, 0.0);
@@ -1258,7 +1280,13 @@ gs_reg(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__rest
 #pragma unroll
     for (int i = 0; i < NA; ++i) acc[i] = 0.0;
     const i64 np = n / 2;
-    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += (i64)gridDim.x * blockDim.x) {
+    const i64 stride = (i64)gridDim.x * blockDim.x;
+    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += stride) {
+        if ((threadIdx.x & 31) == 0) {
+            const i64 pn = p + kPfDist * stride;
+            for (int i = 0; i < k; ++i) warp_prefetch(V + i * ldv, pn, np);
+            warp_prefetch(t, pn, np);
+        }
         double2 tv = reinterpret_cast<const double2 *>(t)[p];
 #pragma unroll
         for (int i0 = 0; i0 < K; i0 += 8) {  // 8 independent loads ahead of each FMA chain
@@ -1298,6 +1326,58 @@ gs_reg(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__rest
             if (i < kdot) acc[i] = fma(V[i * ldv + e], x, acc[i]);
     }
     block_store_partials<K, NA>(acc, partial, NA);
+}
+
+// Thick restart in place: V[j] <- sum_i Y[i, j] V[i] for j < keep <= 8
+// (davidson.py:280-289).  Thread per element pair; the whole pair column of
+// V is read (L2-prefetched in bulk, then 8 vectors at a time) before any of
+// the keep outputs is written, so the in-place update is safe.
+template <int K>
+__global__ void __launch_bounds__(kRegBlock, 2)
+rotate_reg(double *__restrict__ V, int k, i64 ldv, i64 n, const double *__restrict__ Y, int keep) {
+    __shared__ double ys[K * 8];
+    for (int idx = threadIdx.x; idx < K * 8; idx += blockDim.x) {
+        const int i = idx / 8, j = idx % 8;
+        ys[idx] = (i < k && j < keep) ? Y[i * keep + j] : 0.0;
+    }
+    __syncthreads();
+    const i64 np = n / 2, stride = (i64)gridDim.x * blockDim.x;
+    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += stride) {
+        if ((threadIdx.x & 31) == 0)
+            for (int i = 0; i < k; ++i) warp_prefetch(V + i * ldv, p, np);
+        double2 u[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u[j] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i0 = 0; i0 < K; i0 += 8) {
+            double2 v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (i0 + q < k) v[q] = __ldcs(reinterpret_cast<const double2 *>(V + (i0 + q) * ldv) + p);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (i0 + q < k)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const double y = ys[(i0 + q) * 8 + j];
+                        u[j].x = fma(y, v[q].x, u[j].x);
+                        u[j].y = fma(y, v[q].y, u[j].y);
+                    }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (j < keep) reinterpret_cast<double2 *>(V + j * ldv)[p] = u[j];
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const i64 e = n - 1;
+        double u[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i = 0; i < k; ++i) {
+            const double v = V[i * ldv + e];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) u[j] = fma(ys[i * 8 + j], v, u[j]);
+        }
+        for (int j = 0; j < keep; ++j) V[j * ldv + e] = u[j];
+    }
 }
 
 inline bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -1501,6 +1581,11 @@ struct GsL {
 template <int K>
 struct RotL {
     static int run(sbd_ctx *ctx, double *V, int k, i64 ldv, i64 n, const double *Y, int keep) {
+        if (K <= 32 && keep <= 8 && vec_ok(V, ldv) && use_reg()) {
+            rotate_reg<(K <= 32 ? K : 32)><<<ctx->num_sms * 2, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, Y, keep);
+            SBD_LAUNCHED(ctx, "rotate");
+            return SBD_OK;
+        }
         rotate_kernel<K><<<red_blocks(ctx, n) * 2, kBlock, 0, ctx->stream>>>(V, k, ldv, n, Y, keep);
         SBD_LAUNCHED(ctx, "rotate");
         return SBD_OK;

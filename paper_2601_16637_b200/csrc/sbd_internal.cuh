@@ -87,6 +87,8 @@ struct sbd_ctx {
     bool diag_valid = false;
     DevBuf red;                  // reduction scratch
     DevBuf hx, hy;               // device staging for sbd_sigma_host
+    cudaStream_t copy_stream = nullptr;  // sbd_sigma_host: H2D/D2H overlapped with the kernels
+    std::vector<cudaEvent_t> events;
     int num_sms = 148;
 
     i64 own_lo() const { return row_lo; }

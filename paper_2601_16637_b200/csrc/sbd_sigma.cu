@@ -48,6 +48,7 @@ struct SideArgs {
     const double *YT;              // beta-side result, [n_cols][ldyt]
     i64 ldyt;
     const int64_t *a_s_off;        // rows with alpha singles carry task 0 in Y (cross_kernel); null: no task 0
+    i64 tile0;                     // first column tile (pipelined host path launches tile ranges)
 };
 
 template <bool VEC>
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, 3) side_kernel_async(SideArg
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *ring = reinterpret_cast<double *>(ssm) + (size_t)w * R * kTW;
     const i64 r = (i64)blockIdx.x * kRowsPerCta + w;
-    const i64 c0 = (i64)blockIdx.y * kTW;
+    const i64 c0 = ((i64)blockIdx.y + a.tile0) * kTW;
     const i64 ncol = min((i64)kTW, a.n_cols - c0);
     const bool row_ok = r < a.n_rows;
     bool ok[8], pair[4];
@@ -441,9 +442,6 @@ __device__ __forceinline__ void cross_store(double (&acc)[CPT], const CrossArgs 
 __host__ __device__ inline i64 cross_stage_doubles(i64 chunk, i64 ld) { return chunk + 2 + 2 * ld; }
 constexpr int kCrossStages = 3;
 
-__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 // Warp-specialised pipeline: the last warp produces (TMA into kCrossStages
 // stages, L2 prefetch two items further ahead), the other warps consume.
@@ -546,6 +544,7 @@ __global__ void __launch_bounds__(kCrossThreads, 1) cross_kernel_tma(CrossArgs a
 // its own full barrier and then arrives on rank 0's `peer` barrier; rank 0's
 // producer issues the multicast once both CTAs released the stage.
 constexpr int kMcStages = 2;
+constexpr int kMcPrefetch = 2;
 
 __host__ __device__ inline i64 mc_local_groups(i64 groups, int rank) { return (groups - rank + 1) / 2; }
 
@@ -611,6 +610,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrossThreads, 1) cr
                 } else {
                     mbar_wait_cluster(&peer[s], use & 1);
                     const SConn sa = a.a_sconn[e0 + item];
+                    if (item + kMcPrefetch < nitems)  // next-but-one rows: L2 hits for the TMA
+                        prefetch_l2(a.X + (i64)a.a_sconn[e0 + item + kMcPrefetch].tgt * a.nb, bx);
                     double *dst = st0 + s * sdbl;
                     tma_load_1d_multicast(dst, a.X + (i64)sa.tgt * a.nb, bx, &full[s], 0x3);
                     tma_load_1d_multicast(dst + a.chunk + 2, vrow(a, sa), bv, &full[s], 0x3);
@@ -618,31 +619,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrossThreads, 1) cr
             }
         }
     } else {
+        // per-group slot ranges never change across items: keep them in registers
+        uint32_t gptr[CPT];  // index (in sent) of slot 0 of this lane in group j
+        int gw[CPT];         // slots in group j (warp-uniform)
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+            const i64 gl = warp + (i64)j * kC;
+            gw[j] = gl < ngl ? (lgoff[gl + 1] - lgoff[gl]) >> 5 : 0;
+            gptr[j] = (uint32_t)(gl < ngl ? lgoff[gl] : 0) + lane;
+        }
+        const uint32_t pmask = (1u << a.pbits) - 1u, pb = (uint32_t)a.pbits;
         double acc[CPT];
 #pragma unroll
         for (int j = 0; j < CPT; ++j) acc[j] = 0.0;
         for (i64 item = 0; item < nitems; ++item) {
             const int s = (int)(item & 1);
             mbar_wait(&full[s], (uint32_t)((item >> 1) & 1));
-            const double *xr = st0 + s * sdbl;
-            const double *vr = xr + a.chunk + 2;
-            const uint32_t pmask = (1u << a.pbits) - 1u;
+            const uint32_t xa = smem_u32(st0 + s * sdbl), va = xa + (uint32_t)((a.chunk + 2) * sizeof(double));
+            auto term = [&](uint32_t e) {
+                return lds_f64(va + ((e & pmask) << 3)) * lds_f64(xa + ((e >> pb) << 3));
+            };
 #pragma unroll
             for (int j = 0; j < CPT; ++j) {
-                const i64 gl = warp + (i64)j * kC;
-                if (gl < ngl) {
-                    const int o0 = lgoff[gl], w = (lgoff[gl + 1] - o0) >> 5;
-                    const uint32_t *ep = sent + o0 + lane;
-                    int q = 0;
-                    for (; q + 2 <= w; q += 2) {
-                        const uint32_t p0 = ep[32 * q], p1 = ep[32 * q + 32];
-                        const double t0 = vr[p0 & pmask] * xr[p0 >> a.pbits];
-                        acc[j] = fma(vr[p1 & pmask], xr[p1 >> a.pbits], acc[j] + t0);
+                const int w = gw[j];
+                if (w > 0) {
+                    const uint32_t ep = smem_u32(sent + gptr[j]);
+                    double t = term(lds_u32(ep));
+                    if (w > 1) t += term(lds_u32(ep + 128));
+                    if (w > 2) {
+                        t += term(lds_u32(ep + 256));
+                        for (int q = 3; q < w; ++q) t += term(lds_u32(ep + 128 * q));
                     }
-                    if (q < w) {
-                        const uint32_t p0 = ep[32 * q];
-                        acc[j] = fma(vr[p0 & pmask], xr[p0 >> a.pbits], acc[j]);
-                    }
+                    acc[j] += t;
                 }
             }
             __syncwarp();
@@ -861,6 +869,101 @@ int launch_cross(sbd_ctx *ctx, const double *x_full, double *y) {
     return SBD_OK;
 }
 
+// Beta side for own alpha rows [r0, r1) (local): transpose those rows of x into
+// X^T columns, then stream Y^T's column tiles covering them.  r0 is a
+// multiple of kTW unless the whole range is launched.
+int launch_beta_side(sbd_ctx *ctx, const double *x_own, i64 r0, i64 r1) {
+    const Sector &A = ctx->sec[0], &B = ctx->sec[1];
+    const i64 rows = ctx->own_rows(), nb = B.n;
+    if (r1 <= r0 || nb == 0) return SBD_OK;
+    cudaStream_t st = ctx->stream;
+    dim3 tg((unsigned)((nb + 31) / 32), (unsigned)((r1 - r0 + 31) / 32));
+    transpose_kernel<<<tg, dim3(32, 8), 0, st>>>(x_own + r0 * nb, r1 - r0, nb, nb, ctx->xt.as<double>() + r0, ctx->ld_t);
+    SBD_LAUNCHED(ctx, "transpose_kernel");
+    SideArgs a{};
+    a.n_rows = nb;
+    a.row_base = 0;
+    a.n_cols = rows;
+    a.col_base = ctx->own_lo();
+    a.X = ctx->xt.as<double>();
+    a.ldx = ctx->ld_t;
+    a.Y = ctx->yt.as<double>();
+    a.ldy = ctx->ld_t;
+    a.conn_off = B.conn_off.as<int64_t>();
+    a.conn = B.conn.as<Conn>();
+    a.J = A.J.as<double>();
+    a.ldj = A.n;
+    if (use_side_tma() && aligned16(a.X) && a.ldx % 2 == 0) {
+        static bool attr = false;
+        if (!attr) {
+            SBD_CUDA(ctx, cudaFuncSetAttribute(side_kernel_async<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)SideAsync<false>::smem()));
+            attr = true;
+        }
+        a.tile0 = r0 / kTW;
+        const i64 t1 = (r1 + kTW - 1) / kTW;
+        dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)(t1 - a.tile0));
+        side_kernel_async<false><<<g, kRowsPerCta * 32, SideAsync<false>::smem(), st>>>(a);
+    } else {
+        if (r0 != 0 || r1 != rows) return sbd_fail(ctx, SBD_EINVAL, "row-range beta side needs the aligned path");
+        dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((rows + kColsPerWarp - 1) / kColsPerWarp));
+        side_kernel<true, false><<<g, kRowsPerCta * 32, 0, st>>>(a);
+    }
+    SBD_LAUNCHED(ctx, "side_kernel<beta>");
+    return SBD_OK;
+}
+
+// Alpha side (+ diagonal, task 0, beta side fold-in) for own rows [r0, r1) (local).
+int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64 r1) {
+    const Sector &A = ctx->sec[0], &B = ctx->sec[1];
+    const i64 nb = B.n, rows = r1 - r0;
+    if (rows <= 0 || nb == 0) return SBD_OK;
+    SideArgs a{};
+    a.n_rows = rows;
+    a.row_base = ctx->own_lo() + r0;
+    a.n_cols = nb;
+    a.col_base = 0;
+    a.X = x_full;
+    a.ldx = nb;
+    a.Y = y + r0 * nb;
+    a.ldy = nb;
+    a.conn_off = A.conn_off.as<int64_t>();
+    a.conn = A.conn.as<Conn>();
+    a.J = B.J.as<double>();
+    a.ldj = nb;
+    a.YT = ctx->yt.as<double>() + r0;
+    a.ldyt = ctx->ld_t;
+    a.diag = ctx->diag.as<double>() + r0 * nb;
+    a.a_s_off = (A.ns > 0 && B.ns > 0) ? A.s_off.as<int64_t>() : nullptr;
+    const bool vec = (nb % 2 == 0) && aligned16(x_full) && aligned16(y) && (r0 % 2 == 0);
+    if (vec && use_side_tma()) {
+        static bool attr = false;
+        if (!attr) {
+            SBD_CUDA(ctx, cudaFuncSetAttribute(side_kernel_async<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)SideAsync<true>::smem()));
+            attr = true;
+        }
+        dim3 gt((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kTW - 1) / kTW));
+        side_kernel_async<true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
+    } else {
+        dim3 g((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kColsPerWarp - 1) / kColsPerWarp));
+        if (vec) side_kernel<true, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
+        else side_kernel<false, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
+    }
+    SBD_LAUNCHED(ctx, "side_kernel<alpha>");
+    return SBD_OK;
+}
+
+int ensure_events(sbd_ctx *ctx, size_t n) {
+    if (!ctx->copy_stream) SBD_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    while (ctx->events.size() < n) {
+        cudaEvent_t e;
+        SBD_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->events.push_back(e);
+    }
+    return SBD_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -883,41 +986,7 @@ int sbd_sigma_local(sbd_ctx *ctx, const double *x_own) {
     if (rc) return rc;
     rc = ensure_scratch(ctx);
     if (rc) return rc;
-    const Sector &A = ctx->sec[0], &B = ctx->sec[1];
-    const i64 rows = ctx->own_rows(), nb = B.n;
-    if (rows == 0 || nb == 0) return SBD_OK;
-    cudaStream_t st = ctx->stream;
-    dim3 tg((unsigned)((nb + 31) / 32), (unsigned)((rows + 31) / 32));
-    transpose_kernel<<<tg, dim3(32, 8), 0, st>>>(x_own, rows, nb, nb, ctx->xt.as<double>(), ctx->ld_t);
-    SBD_LAUNCHED(ctx, "transpose_kernel");
-    SideArgs a{};
-    a.n_rows = nb;
-    a.row_base = 0;
-    a.n_cols = rows;
-    a.col_base = ctx->own_lo();
-    a.X = ctx->xt.as<double>();
-    a.ldx = ctx->ld_t;
-    a.Y = ctx->yt.as<double>();
-    a.ldy = ctx->ld_t;
-    a.conn_off = B.conn_off.as<int64_t>();
-    a.conn = B.conn.as<Conn>();
-    a.J = A.J.as<double>();
-    a.ldj = A.n;
-    if (use_side_tma() && aligned16(a.X) && a.ldx % 2 == 0) {
-        static bool attr = false;
-        if (!attr) {
-            SBD_CUDA(ctx, cudaFuncSetAttribute(side_kernel_async<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)SideAsync<false>::smem()));
-            attr = true;
-        }
-        dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((rows + kTW - 1) / kTW));
-        side_kernel_async<false><<<g, kRowsPerCta * 32, SideAsync<false>::smem(), st>>>(a);
-    } else {
-        dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((rows + kColsPerWarp - 1) / kColsPerWarp));
-        side_kernel<true, false><<<g, kRowsPerCta * 32, 0, st>>>(a);
-    }
-    SBD_LAUNCHED(ctx, "side_kernel<beta>");
-    return SBD_OK;
+    return launch_beta_side(ctx, x_own, 0, ctx->own_rows());
 }
 
 int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full, double *y) {
@@ -927,48 +996,12 @@ int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full, double *y) {
     rc = ensure_diag(ctx);
     if (rc) return rc;
     const Sector &A = ctx->sec[0], &B = ctx->sec[1];
-    const i64 rows = ctx->own_rows(), nb = B.n;
-    if (rows == 0 || nb == 0) return SBD_OK;
-    SideArgs a{};
-    a.n_rows = rows;
-    a.row_base = ctx->own_lo();
-    a.n_cols = nb;
-    a.col_base = 0;
-    a.X = x_full;
-    a.ldx = nb;
-    a.Y = y;
-    a.ldy = nb;
-    a.conn_off = A.conn_off.as<int64_t>();
-    a.conn = A.conn.as<Conn>();
-    a.J = B.J.as<double>();
-    a.ldj = nb;
-    a.YT = ctx->yt.as<double>();
-    a.ldyt = ctx->ld_t;
-    a.diag = ctx->diag.as<double>();
-    // task 0 exists only when both sectors have in-set singles
-    a.a_s_off = (A.ns > 0 && B.ns > 0) ? A.s_off.as<int64_t>() : nullptr;
-    if (A.ns > 0 && B.ns > 0) {
+    if (ctx->own_rows() == 0 || B.n == 0) return SBD_OK;
+    if (A.ns > 0 && B.ns > 0) {  // task 0 exists only when both sectors have in-set singles
         rc = launch_cross(ctx, x_full, y);
         if (rc) return rc;
     }
-    dim3 g((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kColsPerWarp - 1) / kColsPerWarp));
-    const bool vec = (nb % 2 == 0) && aligned16(x_full) && aligned16(y);
-    if (vec && use_side_tma()) {
-        static bool attr = false;
-        if (!attr) {
-            SBD_CUDA(ctx, cudaFuncSetAttribute(side_kernel_async<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)SideAsync<true>::smem()));
-            attr = true;
-        }
-        dim3 gt((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kTW - 1) / kTW));
-        side_kernel_async<true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
-    } else if (vec) {
-        side_kernel<true, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
-    } else {
-        side_kernel<false, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
-    }
-    SBD_LAUNCHED(ctx, "side_kernel<alpha>");
-    return SBD_OK;
+    return launch_alpha_side(ctx, x_full, y, 0, ctx->own_rows());
 }
 
 int sbd_sigma(sbd_ctx *ctx, const double *x_full, double *y) {
@@ -981,19 +1014,70 @@ int sbd_sigma(sbd_ctx *ctx, const double *x_full, double *y) {
     return sbd_sigma_remote(ctx, x_full, y);
 }
 
+// Host buffers in and out.  With one owner of all rows and the aligned
+// kernels, the copies are pipelined with the kernels in kTW-aligned alpha-row
+// chunks on a second stream: the beta side of chunk c (it only reads x rows
+// of its own column tiles) runs while chunk c+1 is uploaded; after the last
+// chunk, task 0 and the alpha side run chunk by chunk, each chunk's y going
+// back to the host while the next chunk computes.  The host pointers should
+// be pinned for the copies to be asynchronous.
 int sbd_sigma_host(sbd_ctx *ctx, const double *x_host, double *y_host) {
     SBD_CHECK_CTX(ctx);
     int rc = require_ready(ctx);
     if (rc) return rc;
-    const i64 nfull = ctx->sec[0].n * ctx->sec[1].n, nown = ctx->own_rows() * ctx->sec[1].n;
+    const Sector &A = ctx->sec[0], &B = ctx->sec[1];
+    const i64 nb = B.n, nfull = A.n * nb, rows = ctx->own_rows(), nown = rows * nb;
     SBD_CUDA(ctx, ctx->hx.ensure(sizeof(double) * (nfull + 2)));
     SBD_CUDA(ctx, ctx->hy.ensure(sizeof(double) * (nown + 2)));
-    if (nfull)
-        SBD_CUDA(ctx, cudaMemcpyAsync(ctx->hx.p, x_host, sizeof(double) * nfull, cudaMemcpyHostToDevice, ctx->stream));
-    rc = sbd_sigma(ctx, ctx->hx.as<double>(), ctx->hy.as<double>());
+    double *dx = ctx->hx.as<double>(), *dy = ctx->hy.as<double>();
+    const bool pipelined = rows == A.n && nb % 2 == 0 && use_side_tma() && rows > 2 * kTW;
+    if (!pipelined) {
+        if (nfull) SBD_CUDA(ctx, cudaMemcpyAsync(dx, x_host, sizeof(double) * nfull, cudaMemcpyHostToDevice, ctx->stream));
+        rc = sbd_sigma(ctx, dx, dy);
+        if (rc) return rc;
+        if (nown) SBD_CUDA(ctx, cudaMemcpyAsync(y_host, dy, sizeof(double) * nown, cudaMemcpyDeviceToHost, ctx->stream));
+        SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        return SBD_OK;
+    }
+    rc = ensure_scratch(ctx);
     if (rc) return rc;
-    if (nown)
-        SBD_CUDA(ctx, cudaMemcpyAsync(y_host, ctx->hy.p, sizeof(double) * nown, cudaMemcpyDeviceToHost, ctx->stream));
+    rc = ensure_diag(ctx);
+    if (rc) return rc;
+    const i64 nch = 8;
+    const i64 step = std::max<i64>(kTW, (rows / nch + kTW - 1) / kTW * kTW);
+    std::vector<i64> cut{0};
+    while (cut.back() < rows) cut.push_back(std::min(rows, cut.back() + step));
+    const size_t nc = cut.size() - 1;
+    rc = ensure_events(ctx, 2 * nc + 1);
+    if (rc) return rc;
+    cudaStream_t cs = ctx->copy_stream;
+    cudaEvent_t *ev = ctx->events.data();
+    // the copy stream must not overwrite dx/dy while earlier work on the compute stream uses them
+    SBD_CUDA(ctx, cudaEventRecord(ev[2 * nc], ctx->stream));
+    SBD_CUDA(ctx, cudaStreamWaitEvent(cs, ev[2 * nc], 0));
+    for (size_t c = 0; c < nc; ++c) {
+        const i64 r0 = cut[c], r1 = cut[c + 1];
+        SBD_CUDA(ctx, cudaMemcpyAsync(dx + r0 * nb, x_host + r0 * nb, sizeof(double) * (r1 - r0) * nb,
+                                      cudaMemcpyHostToDevice, cs));
+        SBD_CUDA(ctx, cudaEventRecord(ev[c], cs));
+        SBD_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ev[c], 0));
+        rc = launch_beta_side(ctx, dx, r0, r1);
+        if (rc) return rc;
+    }
+    if (A.ns > 0 && B.ns > 0) {
+        rc = launch_cross(ctx, dx, dy);
+        if (rc) return rc;
+    }
+    for (size_t c = 0; c < nc; ++c) {
+        const i64 r0 = cut[c], r1 = cut[c + 1];
+        rc = launch_alpha_side(ctx, dx, dy, r0, r1);
+        if (rc) return rc;
+        SBD_CUDA(ctx, cudaEventRecord(ev[nc + c], ctx->stream));
+        SBD_CUDA(ctx, cudaStreamWaitEvent(cs, ev[nc + c], 0));
+        SBD_CUDA(ctx, cudaMemcpyAsync(y_host + r0 * nb, dy + r0 * nb, sizeof(double) * (r1 - r0) * nb,
+                                      cudaMemcpyDeviceToHost, cs));
+    }
+    SBD_CUDA(ctx, cudaStreamSynchronize(cs));
     SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SBD_OK;
 }
