@@ -208,8 +208,9 @@ constexpr int kTW = 256;
 
 template <bool ALPHA>
 struct SideAsync {
-    static constexpr int kRing = ALPHA ? 3 : 4;
+    static constexpr int kRing = 4;  // the alpha side's epilogue tile reuses the ring after the stream
     static constexpr size_t smem() { return sizeof(double) * (size_t)kRowsPerCta * kRing * kTW; }
+    static_assert(sizeof(double) * kTW * (kRowsPerCta + 1) <= smem(), "epilogue tile must fit the ring");
 };
 
 __device__ __forceinline__ void cp_async16(void *dst_smem, const void *src) {
@@ -287,8 +288,10 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, 3) side_kernel_async(SideArg
     }
 
     if (ALPHA) {
-        // + (B X^T)^T : tile YT[c0:c0+256, r0:r0+8] through shared memory
-        __shared__ double tile[kTW][kRowsPerCta + 1];
+        // + (B X^T)^T : tile YT[c0:c0+256, r0:r0+8] through shared memory (the
+        // rings are drained: every warp waited for its last copy group)
+        __syncthreads();
+        double(*tile)[kRowsPerCta + 1] = reinterpret_cast<double(*)[kRowsPerCta + 1]>(ssm);
         const i64 r0 = (i64)blockIdx.x * kRowsPerCta;
         {
             const int i = threadIdx.x;  // one column of the tile per thread

@@ -273,6 +273,11 @@ def davidson_solve(apply_h: Callable, diag, x0=None, opts: Optional[DavidsonOpti
 
 
 def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce, rank_offset, ctx):
+    """Driver loop.  The projected matrix T = V^T H V and the Gram matrix G stay
+    on the device next to V and W; the Rayleigh-Ritz eigensolve reads T in
+    place.  The host sees one packed read-back per iteration (Ritz values,
+    residual norms, |t|^2, Jacobi sweep count, orthogonality loss) for the
+    control decisions, plus one for the CGS2 branch test."""
     import torch
 
     f64 = dict(dtype=torch.float64, device=dev)
@@ -284,6 +289,7 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
         apply_fn = apply_h
     eng = _Engine(dev.index, ctx, profile=opts.profile)
     reduce = allreduce if allreduce is not None else (lambda t: None)
+    stream = torch.cuda.current_stream(dev)
 
     m = opts.n_roots
     k_max = min(opts.max_subspace, n)
@@ -292,13 +298,26 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
     rng = np.random.default_rng(0x5BD1A6)
 
     # leading dimension padded to a multiple of 32 doubles: 16-byte aligned rows
-    # for the 128-bit tile kernels; vectors are the [:n_loc] views
+    # for the 128-bit kernels; vectors are the [:n_loc] views
     ld = max(32, (n_loc + 31) // 32 * 32)
     V = torch.zeros((k_max, ld), **f64)[:, :n_loc]
     W = torch.zeros((k_max, ld), **f64)[:, :n_loc]
     Tv = torch.zeros((m, ld), **f64)[:, :n_loc]   # preconditioned residuals (one per root)
     small = torch.zeros(2 * 64 + 16, **f64)       # device scratch for dot products
+    small2 = torch.zeros(2 * 64 + 16, **f64)      # CGS outputs (never aliases its input c)
     scale = torch.zeros(1, **f64)
+    T = torch.zeros((k_max, k_max), **f64)        # projected matrix, device-resident
+    G = torch.zeros((k_max, k_max), **f64)        # Gram matrix of V (orthogonality stats)
+    eye = torch.eye(k_max, **f64)
+    Y_dev = torch.zeros((k_max * 8,), **f64)
+    Yk_dev = torch.zeros((k_max * 8,), **f64)
+    th_dev = torch.zeros(8, **f64)
+    jac_w = torch.zeros(k_max, **f64)
+    jac_v = torch.zeros((k_max * k_max,), **f64)
+    jac_info = torch.zeros(1, dtype=torch.int32, device=dev)
+    c_dev = torch.zeros(64, **f64)
+    pack = torch.zeros(64 + 8, **f64)
+    host = torch.zeros(64 + 8, dtype=torch.float64, pin_memory=True)
 
     # start vector (davidson.py:219-227)
     if x0 is None:
@@ -320,74 +339,87 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
             raise ValueError("x0 must be nonzero")
         V[0].copy_(v0 / norm)
 
-    T = np.zeros((k_max, k_max))
-    G = np.zeros((k_max, k_max))  # Gram matrix of V (orthogonality stats)
     k = 1
     theta = np.zeros(m)
-    Y = np.zeros((1, m))
+    mk = 1
     res_norms = np.full(m, np.inf)
     prev_theta0 = None
     jp = 0  # root whose correction the fused kernel projects
-    evals = evecs = None
-    Y_dev = torch.zeros((k_max * 8,), **f64)
-    th_dev = torch.zeros(8, **f64)
-    jac_in = torch.zeros((k_max, k_max), **f64)
-    jac_w = torch.zeros(k_max, **f64)
-    jac_v = torch.zeros((k_max, k_max), **f64)
-    jac_info = torch.zeros(1, dtype=torch.int32, device=dev)
     ritz_rotated = False
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+
+    host_ms = {}
+    _tick = [time.perf_counter()]
+
+    def hp(name):  # host-side time per section (profile mode only)
+        if opts.profile:
+            t = time.perf_counter()
+            host_ms[name] = host_ms.get(name, 0.0) + (t - _tick[0]) * 1e3
+            _tick[0] = t
+
+    def readback(t_dev, cnt):
+        host[:cnt].copy_(t_dev[:cnt], non_blocking=True)
+        hp("enqueue")
+        stream.synchronize()
+        hp("sync_wait")
+        return host[:cnt].numpy().copy()
 
     for iteration in range(1, opts.max_iters + 1):
         t_iter = time.perf_counter()
         stats.iterations = iteration
         # image of the newest direction (davidson.py:241-245)
-        tic = time.perf_counter()
+        ev0.record(stream)
         with eng.phase("sigma"):
             apply_fn(V[k - 1], W[k - 1])
-        torch.cuda.current_stream(dev).synchronize()
-        stats.apply_seconds.append(time.perf_counter() - tic)
+        ev1.record(stream)
         stats.n_applies += 1
 
         # T[:, k-1] = V^T w and the Gram row of v_{k-1}: one pass over V
         eng("sbd_vdots2", _p(V), k, ld, n_loc, _p(W[k - 1]), _p(V[k - 1]), _p(small))
         reduce(small[: 2 * k])
-        sm = small[: 2 * k].cpu().numpy()
-        T[:k, k - 1] = T[k - 1, :k] = sm[:k]
-        G[:k, k - 1] = G[k - 1, :k] = sm[k:2 * k]
+        T[:k, k - 1] = small[:k]
+        T[k - 1, :k] = small[:k]
+        G[:k, k - 1] = small[k:2 * k]
+        G[k - 1, :k] = small[k:2 * k]
 
-        # Rayleigh-Ritz on the device (davidson.py:251)
-        jac_in[:k, :k].copy_(torch.from_numpy(T[:k, :k]))
-        jin = jac_in[:k, :k].contiguous()
-        eng("sbd_jacobi", _p(jin), k, k, _p(jac_w), _p(jac_v), 64, _p(jac_info))
-        jw = jac_w[:k].cpu().numpy()
-        jv = jac_v.reshape(-1)[: k * k].reshape(k, k)
-        if int(jac_info.item()) >= 64:
-            raise RuntimeError("Jacobi sweep limit 64 reached without convergence")
-        evals, evecs = jw.copy(), jv.cpu().numpy().copy()
+        # Rayleigh-Ritz on the device, in place on T (davidson.py:251)
+        eng("sbd_jacobi", _p(T), k, k_max, _p(jac_w), _p(jac_v), 64, _p(jac_info))
         # numpy slicing in the reference keeps min(m, k) roots while k < m
         mk = min(m, k)
-        theta = evals[:mk].copy()
-        Y = np.ascontiguousarray(evecs[:, :mk])
+        evecs = jac_v[: k * k].view(k, k)
+        Y_dev[: k * mk].copy_(evecs[:, :mk].reshape(-1))
+        th_dev[:mk].copy_(jac_w[:mk])
         ritz_rotated = False
 
         # residuals, preconditioned corrections and V^T t in one pass
-        Y_dev[: k * mk].copy_(torch.from_numpy(Y.reshape(-1)))
-        th_dev[:mk].copy_(torch.from_numpy(theta))
         jp = min(jp, mk - 1)
         eng("sbd_residual_precond_target", _p(V), _p(W), k, ld, n_loc, _p(Y_dev), _p(th_dev), mk, jp,
             _p(diag_dev), float(opts.precond_delta), _p(Tv), ld, _p(small))
         reduce(small[: k + 1 + mk])
-        out = small[: k + 1 + mk].cpu().numpy()
-        res_norms = np.sqrt(np.maximum(out[k + 1:k + 1 + mk], 0.0))
-        proj = out[:k].copy()
-        t_norm2 = float(out[k])
+        c_dev[:k].copy_(small[:k])
 
-        stats.ortho_history.append(float(np.linalg.norm(G[:k, :k] - np.eye(k))) if opts.track_orthogonality
-                                   else float("nan"))
+        # one packed read-back: theta | residual^2 | |t|^2 | sweeps | ortho
+        pack[:mk].copy_(jac_w[:mk])
+        pack[mk:2 * mk].copy_(small[k + 1:k + 1 + mk])
+        pack[2 * mk] = small[k]
+        pack[2 * mk + 1] = jac_info[0].to(torch.float64)
+        if opts.track_orthogonality:
+            pack[2 * mk + 2] = torch.linalg.norm(G[:k, :k] - eye[:k, :k])
+        hv = readback(pack, 2 * mk + 3)
+        stats.apply_seconds.append(ev0.elapsed_time(ev1) / 1e3)
+        if hv[2 * mk + 1] >= 64:
+            raise RuntimeError("Jacobi sweep limit 64 reached without convergence")
+        theta = hv[:mk].copy()
+        res_norms = np.sqrt(np.maximum(hv[mk:2 * mk], 0.0))
+        t_norm2 = float(hv[2 * mk])
+
+        stats.ortho_history.append(float(hv[2 * mk + 2]) if opts.track_orthogonality else float("nan"))
         stats.theta_history.append(theta.copy())
         stats.residual_history.append(res_norms.copy())
         stats.theta_deltas.append(abs(theta[0] - prev_theta0) if prev_theta0 is not None else np.inf)
         prev_theta0 = theta[0]
+        hp("control")
 
         if bool(np.all(res_norms <= opts.tol_residual)):
             stats.converged = True
@@ -403,7 +435,7 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
             # the fused projection used another root: one extra pass
             eng("sbd_vdots2", _p(V), k, ld, n_loc, _p(t_vec), _p(t_vec), _p(small))
             reduce(small[: 2 * k])
-            proj = small[:k].cpu().numpy().copy()
+            c_dev[:k].copy_(small[:k])
             nn = (t_vec @ t_vec).reshape(1)
             reduce(nn)
             t_norm2 = float(nn.item())
@@ -411,22 +443,26 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
 
         if k == k_max:
             # thick restart (davidson.py:280-289): rotate V and W in place
-            yk = np.ascontiguousarray(evecs[:, :keep])
-            Y_dev[: k * keep].copy_(torch.from_numpy(yk.reshape(-1)))
-            eng("sbd_rotate", _p(V), k, ld, n_loc, _p(Y_dev), keep)
-            eng("sbd_rotate", _p(W), k, ld, n_loc, _p(Y_dev), keep)
-            T[:, :] = 0.0
-            T[:keep, :keep] = np.diag(evals[:keep])
-            G_new = yk.T @ G[:k, :k] @ yk
-            G[:, :] = 0.0
-            G[:keep, :keep] = G_new
-            proj = yk.T @ proj
+            yk = evecs[:, :keep]
+            Yk_dev[: k * keep].copy_(yk.reshape(-1))
+            eng("sbd_rotate", _p(V), k, ld, n_loc, _p(Yk_dev), keep)
+            eng("sbd_rotate", _p(W), k, ld, n_loc, _p(Yk_dev), keep)
+            # the k x k bookkeeping on the host (a few microseconds; no cuBLAS on the path)
+            yk_h = yk.cpu().numpy()
+            G_new = yk_h.T @ G[:k, :k].cpu().numpy() @ yk_h
+            c_new = yk_h.T @ c_dev[:k].cpu().numpy()
+            T.zero_()
+            T[:keep, :keep] = torch.diag(jac_w[:keep])
+            G.zero_()
+            G[:keep, :keep] = torch.from_numpy(G_new).to(dev)
+            c_dev[:keep].copy_(torch.from_numpy(c_new).to(dev))
             stats.restarts += 1
             stats.restart_iters.append(iteration)
             k = keep
             ritz_rotated = True
 
-        v_ok = _orthogonalize_device(eng, V, k, ld, n_loc, t_vec, proj, t_norm2, opts, small, scale, reduce)
+        v_ok = _orthogonalize_device(eng, V, k, ld, n_loc, t_vec, c_dev, t_norm2, opts, small2, scale, reduce,
+                                     readback)
         attempts = 0
         while not v_ok and attempts < 3:
             stats.breakdowns += 1
@@ -435,11 +471,11 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
             t_vec.copy_(torch.from_numpy(rv[lo:lo + n_loc]))
             eng("sbd_vdots2", _p(V), k, ld, n_loc, _p(t_vec), _p(t_vec), _p(small))
             reduce(small[: 2 * k])
-            proj = small[:k].cpu().numpy().copy()
+            c_dev[:k].copy_(small[:k])
             nn = (t_vec @ t_vec).reshape(1)
             reduce(nn)
-            v_ok = _orthogonalize_device(eng, V, k, ld, n_loc, t_vec, proj, float(nn.item()), opts, small, scale,
-                                         reduce)
+            v_ok = _orthogonalize_device(eng, V, k, ld, n_loc, t_vec, c_dev, float(nn.item()), opts, small2, scale,
+                                         reduce, readback)
             attempts += 1
         if not v_ok:
             stats.iter_seconds.append(time.perf_counter() - t_iter)
@@ -448,45 +484,41 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
         stats.iter_seconds.append(time.perf_counter() - t_iter)
 
     # Ritz vectors of the last Rayleigh-Ritz (davidson.py:256), computed once
-    mk = Y.shape[1]
     if ritz_rotated:
-        Yr = np.zeros((k, mk))
-        Yr[:mk, :mk] = np.eye(mk)
+        Yr = torch.zeros((k, mk), **f64)
+        Yr[:mk, :mk] = torch.eye(mk, **f64)
     else:
-        Yr = Y
+        Yr = jac_v[: k * k].view(k, k)[:, :mk]
     kk = Yr.shape[0]
-    Y_dev[: kk * mk].copy_(torch.from_numpy(np.ascontiguousarray(Yr).reshape(-1)))
+    Y_dev[: kk * mk].copy_(Yr.reshape(-1))
     U = torch.empty((mk, n_loc), **f64)
     eng("sbd_combine", _p(V), kk, ld, n_loc, _p(Y_dev), mk, _p(U), n_loc)
     del V, W, Tv
     torch.cuda.current_stream(dev).synchronize()
     if opts.profile:
         stats.phase_ms = eng.summary()
+        stats.phase_ms.update({"host:" + k_: v for k_, v in host_ms.items()})
     vectors = U if return_device else U.cpu().numpy()
     if eng.own_ctx:
         eng.ctx.close()
     return DavidsonResult(energies=theta.copy(), vectors=vectors, residual_norms=res_norms.copy(), stats=stats)
 
 
-def _orthogonalize_device(eng, V, k, ld, n_loc, t, proj, t_norm2, opts, small, scale, reduce) -> bool:
-    """CGS2 of t against V[:k] given c = V^T t; writes the normalised V[k] on success.
+def _orthogonalize_device(eng, V, k, ld, n_loc, t, c, t_norm2, opts, small, scale, reduce, readback) -> bool:
+    """CGS2 of t against V[:k] given c = V^T t (device); writes the normalised V[k] on success.
 
     Rejection rule of the reference orthogonalize (davidson.py:166-185): the
     remainder norm must stay >= 1e-12 of the input norm.
     """
-    import torch
-
     norm0 = float(np.sqrt(max(t_norm2, 0.0)))
     if norm0 == 0.0:
         return False
-    dev = V.device
-    c = torch.from_numpy(np.ascontiguousarray(proj, dtype=np.float64)).to(dev)
     if opts.reorthogonalize:
         # CGS pass 1: t' = t - V c ; c2 = V^T t' ; |t'|^2
         eng("sbd_gs_update", _p(V), k, ld, n_loc, _p(c), _p(t), _p(small))
         reduce(small[: k + 1])
-        host = small[: k + 1].cpu().numpy()
-        c2, n2p = host[:k], float(host[k])
+        hv = readback(small, k + 1)
+        c2, n2p = hv[:k], float(hv[k])
         n2 = n2p - float(c2 @ c2)  # |t' - V c2|^2 for orthonormal V
         c2d = small[:k].clone()
         if n2p > 0.0 and n2 > 0.5 * n2p:
@@ -500,7 +532,7 @@ def _orthogonalize_device(eng, V, k, ld, n_loc, t, proj, t_norm2, opts, small, s
     else:
         eng("sbd_gs_update_nodots", _p(V), k, ld, n_loc, _p(c), _p(t), _p(small))
     reduce(small[:1])
-    norm = float(np.sqrt(max(float(small[0].item()), 0.0)))
+    norm = float(np.sqrt(max(float(readback(small, 1)[0]), 0.0)))
     if norm < 1e-12 * norm0 or norm == 0.0:
         return False
     scale.fill_(1.0 / norm)

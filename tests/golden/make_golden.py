@@ -186,8 +186,47 @@ def make_cfg4():
     _big("cfg4", 36, 27, 27, 30000, [(0, 1)])
 
 
+EXPLICIT_CASES = [
+    # name, norb, na, nb, n_dets, integral seed, basis seed
+    ("expl_4_2_2_all", 4, 2, 2, 36, 0, 3),
+    ("expl_5_2_3_some", 5, 2, 3, 40, 9, 1),
+    ("expl_6_3_3", 6, 3, 3, 150, 21, 5),
+    ("expl_8_4_3", 8, 4, 3, 900, 7, 11),
+    ("expl_single", 3, 2, 2, 1, 42, 0),
+    ("expl_10_5_5", 10, 5, 5, 4000, 13, 17),
+    ("expl_12_6_6", 12, 6, 6, 20000, 1, 2),
+]
+
+
+def make_explicit():
+    """Explicit (full-bitstring) bases: the reference's _explicit_kernel (apply.py:320-458)."""
+    out, meta = {}, {}
+    for name, norb, na, nb, nd, iseed, bseed in EXPLICIT_CASES:
+        table = synth.random_integrals(norb, seed=iseed)
+        basis = synth.random_explicit_basis(norb, na, nb, nd, seed=bseed)
+        app = HamiltonianApplier(basis, table, exec_policy="deterministic")
+        rng = np.random.default_rng(2000 + iseed)
+        xs = rng.standard_normal((2, basis.dimension))
+        ys = np.stack([app(x) for x in xs])
+        n = basis.dimension
+        opts = DavidsonOptions(n_roots=min(2, n), restart_keep=min(4, n), max_subspace=min(32, n))
+        res = davidson_solve(app, app.diag, opts=opts)
+        out[f"{name}/det_a"] = np.array([d.alpha for d in basis.dets], dtype=np.uint64)
+        out[f"{name}/det_b"] = np.array([d.beta for d in basis.dets], dtype=np.uint64)
+        out[f"{name}/diag"] = app.diag
+        out[f"{name}/x"] = xs
+        out[f"{name}/y"] = ys
+        out[f"{name}/energies"] = res.energies
+        meta[name] = dict(norb=norb, na=na, nb=nb, n_dets=nd, iseed=iseed, bseed=bseed,
+                          iterations=res.stats.iterations, converged=res.stats.converged, n_roots=opts.n_roots)
+        print(name, n, res.energies, res.stats.iterations)
+    np.savez_compressed(os.path.join(HERE, "explicit.npz"), **out)
+    with open(os.path.join(HERE, "explicit_meta.json"), "w") as f:
+        json.dump(meta, f, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
-    jobs = dict(small=make_small, cfg1=make_cfg1, cfg2=make_cfg2, cfg4=make_cfg4,
+    jobs = dict(small=make_small, cfg1=make_cfg1, cfg2=make_cfg2, cfg4=make_cfg4, explicit=make_explicit,
                 **{"cfg1-davidson": make_cfg1_davidson})
     for arg in sys.argv[1:]:
         jobs[arg]()

@@ -97,9 +97,13 @@ def test_empty_and_single_string_sectors():
     assert t.s_off.tolist() == [0, 0] and t.d_off.tolist() == [0, 0]
 
 
-@pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg4"])
 def test_big_config_tables_diag_sigma_windows(cfg):
-    """Reference tables (SHA-256 of every column) and reference sigma on alpha-row windows."""
+    """Reference tables (SHA-256 of every column) and reference sigma on alpha-row windows.
+
+    cfg4 is the 9e8-determinant Fe-S-like system (36 orbitals, 3e4 x 3e4 strings): its x rows (240 KB)
+    exceed shared memory, so task 0 runs on the chunked sliced-ELL pipeline.
+    """
     from paper_2601_16637_b200 import HamiltonianApplier, SelectedBasis
 
     rec, arrays = load_big(cfg)

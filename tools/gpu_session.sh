@@ -20,4 +20,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:'side_kernel|cross_kernel|transpose_kernel' -s 12 -c 4 -o "$OUT/sigma" \
     python bench.py --steps 1 --warmup 3 --no-davidson --no-cpu --no-e2e > "$OUT/ncu_full.log" 2>&1
+# Davidson: per-phase device/host time, then one ncu capture of each vector pass
+timeout 600 python tools/profile_davidson.py > "$OUT/dav_profile.json" 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:'residual|gs_|vdots2|rotate' -s 60 -c 5 -o "$OUT/dav" \
+    python tools/profile_davidson.py 24 > "$OUT/ncu_dav.log" 2>&1
 echo done > "$OUT/DONE"
