@@ -61,6 +61,16 @@ int sbd_set_integrals(sbd_ctx *ctx, int norb, const double *h_host, const double
  * basis.py:138-160).  Validates popcount == n_elec and bits < norb. */
 int sbd_set_strings(sbd_ctx *ctx, int spin, const uint64_t *strings_host, int64_t n, int n_elec);
 
+/* Explicit (full-bitstring) determinant list, caller order (SelectedBasis.explicit,
+ * basis.py:163-180; HamiltonianApplier explicit branch, apply.py:675-683).  The
+ * unique alpha and beta strings become the two sectors (first-seen order);
+ * sbd_build_tables then also builds the (alpha, beta)-sorted determinant index
+ * (duplicates -> SBD_EINVAL), and sbd_diag / sbd_sigma / sbd_sigma_host act on
+ * the n determinants in caller order (_explicit_kernel, apply.py:429-444).  Row
+ * windows and the split sigma are product-mode only. */
+int sbd_set_dets(sbd_ctx *ctx, const uint64_t *alpha_host, const uint64_t *beta_host, int64_t n,
+                 int n_alpha_elec, int n_beta_elec);
+
 /* Configuration processing + excitation generation on the device:
  * radix sort/unique of each sector's strings, CSR in-set singles/doubles
  * with phases (build_excitation_table, basis.py:362-403; build_spin_tables,

@@ -230,6 +230,98 @@ void orc_diag(i64 balo, i64 bahi, i64 nbeta, double *out, const u64 *alpha, cons
     par_for((bahi - balo) * nbeta, 4096, nthreads, diag_range, &j);
 }
 
+/* ---- explicit (full-bitstring) bases: apply.py:320-458 ---- */
+
+/* apply.py:323-335: lower bound on (alpha, beta) over the lexicographically sorted dets */
+static i64 find_det(const u64 *sa, const u64 *sb, i64 n, u64 ta, u64 tb) {
+    i64 lo = 0, hi = n;
+    while (lo < hi) {
+        i64 mid = (lo + hi) >> 1;
+        u64 a = sa[mid];
+        if (a < ta || (a == ta && sb[mid] < tb)) lo = mid + 1;
+        else hi = mid;
+    }
+    if (lo < n && sa[lo] == ta && sb[lo] == tb) return lo;
+    return -1;
+}
+
+/* apply.py:338-426: one explicit row, the reference's loop nesting and accumulation order */
+static double explicit_row(i64 i, const double *x, const double *diag, const u64 *det_a, const u64 *det_b,
+                           const u64 *sa, const u64 *sb, const i64 *perm, i64 n, u64 mask, const double *h,
+                           int norb, const double *eri, double e_core) {
+    const u64 da = det_a[i], db = det_b[i];
+    double acc = diag[i] * x[i];
+    const u64 va = ~da & mask, vb = ~db & mask;
+    for (u64 tp = da; tp; tp &= tp - 1) {  /* alpha singles + their beta-single crosses */
+        int p = ctz(tp);
+        for (u64 tr = va; tr; tr &= tr - 1) {
+            int r = ctz(tr);
+            u64 ta = (da & ~bit(p)) | bit(r);
+            i64 pos = find_det(sa, sb, n, ta, db);
+            if (pos >= 0) acc += orc_hij(da, db, ta, db, h, norb, eri, e_core) * x[perm[pos]];
+            for (u64 uq = db; uq; uq &= uq - 1) {
+                int q = ctz(uq);
+                for (u64 us = vb; us; us &= us - 1) {
+                    int s2 = ctz(us);
+                    u64 tb = (db & ~bit(q)) | bit(s2);
+                    i64 pos2 = find_det(sa, sb, n, ta, tb);
+                    if (pos2 >= 0) acc += orc_hij(da, db, ta, tb, h, norb, eri, e_core) * x[perm[pos2]];
+                }
+            }
+        }
+    }
+    for (u64 tp = db; tp; tp &= tp - 1) {  /* beta singles */
+        int q = ctz(tp);
+        for (u64 tr = vb; tr; tr &= tr - 1) {
+            int s2 = ctz(tr);
+            u64 tb = (db & ~bit(q)) | bit(s2);
+            i64 pos = find_det(sa, sb, n, da, tb);
+            if (pos >= 0) acc += orc_hij(da, db, da, tb, h, norb, eri, e_core) * x[perm[pos]];
+        }
+    }
+    for (int spin = 0; spin < 2; ++spin) {  /* alpha doubles, then beta doubles */
+        const u64 w = spin ? db : da, v = spin ? vb : va;
+        for (u64 t1 = w; t1; t1 &= t1 - 1) {
+            int p = ctz(t1);
+            for (u64 t2 = t1 & (t1 - 1); t2; t2 &= t2 - 1) {
+                int q = ctz(t2);
+                for (u64 u1 = v; u1; u1 &= u1 - 1) {
+                    int r = ctz(u1);
+                    for (u64 u2 = u1 & (u1 - 1); u2; u2 &= u2 - 1) {
+                        int s2 = ctz(u2);
+                        u64 t = (w & ~bit(p) & ~bit(q)) | bit(r) | bit(s2);
+                        u64 ka = spin ? da : t, kb = spin ? t : db;
+                        i64 pos = find_det(sa, sb, n, ka, kb);
+                        if (pos >= 0) acc += orc_hij(da, db, ka, kb, h, norb, eri, e_core) * x[perm[pos]];
+                    }
+                }
+            }
+        }
+    }
+    return acc;
+}
+
+typedef struct {
+    i64 n; double *y; const double *x, *diag; const u64 *det_a, *det_b, *sa, *sb; const i64 *perm;
+    u64 mask; const double *h, *eri; int norb; double e_core;
+} explicit_job;
+
+static void explicit_range(i64 lo, i64 hi, void *vp) {
+    explicit_job *j = (explicit_job *)vp;
+    for (i64 i = lo; i < hi; ++i)
+        j->y[i] += explicit_row(i, j->x, j->diag, j->det_a, j->det_b, j->sa, j->sb, j->perm, j->n, j->mask, j->h,
+                                j->norb, j->eri, j->e_core);
+}
+
+/* apply.py:429-444 + 698-703: y = H x over an explicit determinant list (sa/sb/perm from np.lexsort) */
+void orc_sigma_explicit(i64 n, double *y, const double *x, const double *diag, const u64 *det_a, const u64 *det_b,
+                        const u64 *sa, const u64 *sb, const i64 *perm, const double *h, int norb, const double *eri,
+                        double e_core, int nthreads) {
+    explicit_job j = {n, y, x, diag, det_a, det_b, sa, sb, perm,
+                      norb >= 64 ? ~(u64)0 : (bit(norb) - 1), h, eri, norb, e_core};
+    par_for(n, 64, nthreads, explicit_range, &j);
+}
+
 /* ---- excitation tables: basis.py:72-103 (enumeration order) + 362-403 ---- */
 
 typedef struct { u64 key; i64 idx; } keyidx;

@@ -131,22 +131,25 @@ def build_spin_tables(basis: SelectedBasis, device=None) -> SpinTables:
 
 
 class HamiltonianApplier:
-    """Reusable y = H x over a product basis, resident on one GPU.
+    """Reusable y = H x over a product or explicit basis, resident on one GPU.
 
     ``tables`` (reference-built SpinTables) is accepted for signature
     compatibility; the device always builds its own, bit-identical tables.
     ``row_window=(lo, hi)`` restricts the owned (output) alpha rows, the
     contract of the reference's windowed apply (``apply.py:501-546``) and of
-    one rank of the distributed applier.
+    one rank of the distributed applier (product mode only).  Explicit bases
+    follow the reference's explicit branch (``apply.py:675-683,696-703``):
+    ``tables`` and ``cache`` are None, y is indexed by determinant order.
     """
 
     def __init__(self, basis: SelectedBasis, table: IntegralTable, tables: Optional[SpinTables] = None,
                  exec_policy: str = "parallel", device=None, row_window=None):
         check_policy(exec_policy)
-        if basis.mode != "product":
-            raise NotImplementedError(
-                "explicit (full-bitstring) bases are not on the B200 path yet; use a product basis")
         import torch
+
+        if basis.mode == "explicit":
+            self._init_explicit(basis, table, exec_policy, device, row_window)
+            return
 
         self.basis = basis
         self.table = table
@@ -173,9 +176,44 @@ class HamiltonianApplier:
         torch.cuda.synchronize(self.device)
         self.diag = self.diag_device.cpu().numpy()
 
+    def _init_explicit(self, basis, table, exec_policy, device, row_window):
+        import torch
+
+        if row_window is not None:
+            raise ValueError("row windows apply to product-mode bases only")
+        self.basis = basis
+        self.table = table
+        self.exec_policy = exec_policy
+        self.n = basis.dimension
+        self.apply_count = 0
+        self.cache = None
+        self.device = _device_index(device)
+        self._torch_device = torch.device("cuda", self.device)
+        self._ctx = _lib.Context(self.device)
+        da = np.ascontiguousarray([d.alpha for d in basis.dets], dtype=np.uint64)
+        db = np.ascontiguousarray([d.beta for d in basis.dets], dtype=np.uint64)
+        with torch.cuda.device(self.device):
+            h = np.ascontiguousarray(table.h, dtype=np.float64)
+            eri = np.ascontiguousarray(table.eri, dtype=np.float64)
+            self._ctx("sbd_set_integrals", int(table.norb), _lib.ptr(h), _lib.ptr(eri), int(eri.size),
+                      float(table.e_core))
+            self._ctx("sbd_set_dets", _lib.ptr(da), _lib.ptr(db), int(self.n), int(basis.n_alpha_elec),
+                      int(basis.n_beta_elec))
+            self._ctx("sbd_build_tables")
+        self.row_window = None
+        self.n_own = self.n
+        self._tables = None
+        self.diag_device = torch.empty(self.n, dtype=torch.float64, device=self._torch_device)
+        self._ctx.bind_stream()
+        self._ctx("sbd_diag", _lib.ptr(self.diag_device) if self.n else None)
+        torch.cuda.synchronize(self.device)
+        self.diag = self.diag_device.cpu().numpy()
+
     # -- reference attributes -------------------------------------------------
     @property
-    def tables(self) -> SpinTables:
+    def tables(self):
+        if self.basis.mode != "product":
+            return None  # reference: explicit appliers carry no spin tables (apply.py:680)
         if self._tables is None:
             self._tables = SpinTables(alpha=_export_table(self._ctx, 0, self.basis.norb),
                                       beta=_export_table(self._ctx, 1, self.basis.norb))
@@ -229,9 +267,7 @@ class HamiltonianApplier:
 
 
 def compute_diagonal(basis: SelectedBasis, table: IntegralTable, cache=None, device=None) -> np.ndarray:
-    """d_i = <det_i|H|det_i> (reference ``apply.py:573-586``; bitwise equal)."""
-    if basis.mode != "product":
-        raise NotImplementedError("explicit bases are not on the B200 path yet")
+    """d_i = <det_i|H|det_i> (reference ``apply.py:573-586``; bitwise equal), either basis mode."""
     return HamiltonianApplier(basis, table, device=device).diag
 
 
@@ -247,7 +283,8 @@ def apply_H(x, basis: SelectedBasis, table: IntegralTable, tables: Optional[Spin
     return HamiltonianApplier(basis, table, tables, exec_policy, device=device)(xa)
 
 
-def apply_H_full(x, basis: SelectedBasis, table: IntegralTable, exec_policy: str = "parallel"):
+def apply_H_full(x, basis: SelectedBasis, table: IntegralTable, exec_policy: str = "parallel", device=None):
+    """y = H x over an explicit determinant list (reference ``apply.py:626-648``)."""
     if basis.mode != "explicit":
         raise ValueError("apply_H_full serves explicit-mode bases; see apply_H")
-    raise NotImplementedError("explicit-basis sigma is SURVEY section 8(f) item 2 (next round)")
+    return HamiltonianApplier(basis, table, exec_policy=exec_policy, device=device)(x)

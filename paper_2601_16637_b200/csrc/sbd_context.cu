@@ -168,6 +168,7 @@ int sbd_set_strings(sbd_ctx *ctx, int spin, const uint64_t *strings, int64_t n, 
     SBD_CUDA(ctx, s.str.ensure(sizeof(u64) * (n ? n : 1)));
     if (n) SBD_CUDA(ctx, cudaMemcpy(s.str.p, strings, sizeof(u64) * n, cudaMemcpyHostToDevice));
     ctx->diag_valid = false;
+    ctx->explicit_mode = false;  // sbd_set_dets re-enables it after setting both sectors
     if (spin == 0) ctx->row_lo = 0, ctx->row_hi = -1;
     return SBD_OK;
 }
@@ -191,6 +192,10 @@ int sbd_build_tables(sbd_ctx *ctx) {
         int rc = sbd_build_coefficients(ctx, s, o);
         if (rc) return rc;
         s.built = true;
+    }
+    if (ctx->explicit_mode) {
+        int rc = sbd_build_explicit_index(ctx);
+        if (rc) return rc;
     }
     ctx->diag_valid = false;
     SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -246,6 +251,7 @@ int sbd_export_sorted(sbd_ctx *ctx, int spin, uint64_t *sorted_host, int64_t *pe
 int sbd_set_row_window(sbd_ctx *ctx, int64_t lo, int64_t hi) {
     SBD_CHECK_CTX(ctx);
     if (!ctx->sec[0].present) return sbd_fail(ctx, SBD_EINVAL, "alpha strings not set");
+    if (ctx->explicit_mode) return sbd_fail(ctx, SBD_EINVAL, "row windows apply to product-mode bases only");
     if (!(0 <= lo && lo <= hi && hi <= ctx->sec[0].n))
         return sbd_fail(ctx, SBD_EINVAL, "alpha window (" + std::to_string(lo) + ", " + std::to_string(hi) +
                                              ") exceeds basis");

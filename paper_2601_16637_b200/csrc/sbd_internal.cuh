@@ -90,6 +90,15 @@ struct sbd_ctx {
     cudaStream_t copy_stream = nullptr;  // sbd_sigma_host: H2D/D2H overlapped with the kernels
     std::vector<cudaEvent_t> events;
     int num_sms = 148;
+    // explicit (full-bitstring) basis: dets are (A, B) pairs of unique-string
+    // indices; sec[0]/sec[1] hold the unique alpha/beta strings (first-seen order)
+    bool explicit_mode = false;
+    i64 n_det = 0;
+    std::vector<int32_t> det_a_host, det_b_host;
+    DevBuf det_a, det_b;         // int32[n_det], caller order
+    DevBuf grp_off;              // int32[n_alpha + 1]: dets sorted by (A, B), group of alpha A
+    DevBuf grp_b, grp_perm;      // int32[n_det]: sorted B and caller index
+    bool explicit_built = false;
 
     i64 own_lo() const { return row_lo; }
     i64 own_hi() const { return row_hi < 0 ? sec[0].n : row_hi; }
@@ -123,6 +132,11 @@ int sbd_cuda_fail(sbd_ctx *ctx, cudaError_t e, const char *where);
 int sbd_sort_strings(sbd_ctx *ctx, Sector &s);              // sbd_strings.cu
 int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s);       // sbd_excite.cu
 int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other);  // sbd_excite.cu
+// LSD radix sort of n u64 keys (low key_bits significant) with the sort permutation (sbd_strings.cu)
+int sbd_radix_sort(sbd_ctx *ctx, const u64 *keys, i64 n, int key_bits, DevBuf &sorted, DevBuf &perm);
+int sbd_build_explicit_index(sbd_ctx *ctx);                 // sbd_explicit.cu
+int sbd_explicit_diag(sbd_ctx *ctx, double *out);           // sbd_explicit.cu
+int sbd_explicit_sigma(sbd_ctx *ctx, const double *x, double *y);  // sbd_explicit.cu
 
 // x rows of up to kSellWhole strings are staged whole (H = 1, cluster kernel);
 // longer rows in chunks of at most kSellChunk strings (28 KB)

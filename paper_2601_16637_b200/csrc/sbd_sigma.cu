@@ -749,13 +749,25 @@ bool use_side_tma() {  // SBD_SIDE_LDG=1 selects the register-staged stream (A/B
 }
 
 int require_ready(sbd_ctx *ctx) {
-    if (!ctx->sec[0].built || !ctx->sec[1].built)
+    if (!ctx->sec[0].built || !ctx->sec[1].built || (ctx->explicit_mode && !ctx->explicit_built))
         return sbd_fail(ctx, SBD_EINVAL, "tables not built (call sbd_build_tables)");
+    return SBD_OK;
+}
+
+int require_product(sbd_ctx *ctx) {
+    if (ctx->explicit_mode) return sbd_fail(ctx, SBD_EINVAL, "this entry point serves product-mode bases only");
     return SBD_OK;
 }
 
 int ensure_diag(sbd_ctx *ctx) {
     if (ctx->diag_valid) return SBD_OK;
+    if (ctx->explicit_mode) {
+        SBD_CUDA(ctx, ctx->diag.ensure(sizeof(double) * (ctx->n_det + 2)));
+        int rc = sbd_explicit_diag(ctx, ctx->diag.as<double>());
+        if (rc) return rc;
+        ctx->diag_valid = true;
+        return SBD_OK;
+    }
     const i64 rows = ctx->own_rows(), nb = ctx->sec[1].n;
     SBD_CUDA(ctx, ctx->diag.ensure(sizeof(double) * (rows * nb + 2)));
     if (rows * nb > 0) {
@@ -977,7 +989,7 @@ int sbd_diag(sbd_ctx *ctx, double *out_dev) {
     if (rc) return rc;
     rc = ensure_diag(ctx);
     if (rc) return rc;
-    const i64 n = ctx->own_rows() * ctx->sec[1].n;
+    const i64 n = ctx->explicit_mode ? ctx->n_det : ctx->own_rows() * ctx->sec[1].n;
     if (out_dev && n)
         SBD_CUDA(ctx, cudaMemcpyAsync(out_dev, ctx->diag.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
     return SBD_OK;
@@ -987,6 +999,8 @@ int sbd_sigma_local(sbd_ctx *ctx, const double *x_own) {
     SBD_CHECK_CTX(ctx);
     int rc = require_ready(ctx);
     if (rc) return rc;
+    rc = require_product(ctx);
+    if (rc) return rc;
     rc = ensure_scratch(ctx);
     if (rc) return rc;
     return launch_beta_side(ctx, x_own, 0, ctx->own_rows());
@@ -995,6 +1009,8 @@ int sbd_sigma_local(sbd_ctx *ctx, const double *x_own) {
 int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full, double *y) {
     SBD_CHECK_CTX(ctx);
     int rc = require_ready(ctx);
+    if (rc) return rc;
+    rc = require_product(ctx);
     if (rc) return rc;
     rc = ensure_diag(ctx);
     if (rc) return rc;
@@ -1012,6 +1028,11 @@ int sbd_sigma(sbd_ctx *ctx, const double *x_full, double *y) {
     int rc = require_ready(ctx);
     if (rc) return rc;
     if (!x_full || !y) return sbd_fail(ctx, SBD_EINVAL, "null vector");
+    if (ctx->explicit_mode) {
+        rc = ensure_diag(ctx);
+        if (rc) return rc;
+        return sbd_explicit_sigma(ctx, x_full, y);
+    }
     rc = sbd_sigma_local(ctx, x_full + ctx->own_lo() * ctx->sec[1].n);
     if (rc) return rc;
     return sbd_sigma_remote(ctx, x_full, y);
@@ -1029,11 +1050,14 @@ int sbd_sigma_host(sbd_ctx *ctx, const double *x_host, double *y_host) {
     int rc = require_ready(ctx);
     if (rc) return rc;
     const Sector &A = ctx->sec[0], &B = ctx->sec[1];
-    const i64 nb = B.n, nfull = A.n * nb, rows = ctx->own_rows(), nown = rows * nb;
+    const i64 nb = B.n;
+    const i64 nfull = ctx->explicit_mode ? ctx->n_det : A.n * nb;
+    const i64 rows = ctx->explicit_mode ? 0 : ctx->own_rows();
+    const i64 nown = ctx->explicit_mode ? ctx->n_det : rows * nb;
     SBD_CUDA(ctx, ctx->hx.ensure(sizeof(double) * (nfull + 2)));
     SBD_CUDA(ctx, ctx->hy.ensure(sizeof(double) * (nown + 2)));
     double *dx = ctx->hx.as<double>(), *dy = ctx->hy.as<double>();
-    const bool pipelined = rows == A.n && nb % 2 == 0 && use_side_tma() && rows > 2 * kTW;
+    const bool pipelined = !ctx->explicit_mode && rows == A.n && nb % 2 == 0 && use_side_tma() && rows > 2 * kTW;
     if (!pipelined) {
         if (nfull) SBD_CUDA(ctx, cudaMemcpyAsync(dx, x_host, sizeof(double) * nfull, cudaMemcpyHostToDevice, ctx->stream));
         rc = sbd_sigma(ctx, dx, dy);
@@ -1090,6 +1114,11 @@ int sbd_sigma_model(sbd_ctx *ctx, double *cbar, double *bytes) {
     int rc = require_ready(ctx);
     if (rc) return rc;
     const Sector &A = ctx->sec[0];
+    if (ctx->explicit_mode) {  // no streaming model: report in-set alpha moves per string
+        if (cbar) *cbar = A.n ? (double)(A.ns + A.nd) / (double)A.n : 0.0;
+        if (bytes) *bytes = 0.0;
+        return SBD_OK;
+    }
     double cb = A.n ? (double)(A.ns + A.nd) / (double)A.n : 0.0;
     if (cbar) *cbar = cb;
     if (bytes) *bytes = 8.0 * (double)ctx->own_rows() * (double)ctx->sec[1].n * (3.0 + cb);

@@ -11,6 +11,8 @@
 // Sort: 8-bit LSD digits, only ceil(norb/8) passes (bits >= norb are zero).
 // Per pass: tile histogram -> digit-major exclusive scan -> stable scatter
 // (warp match_any ranking + per-warp digit prefix), tiles of 1024 keys.
+#include <algorithm>
+
 #include "sbd_internal.cuh"
 
 namespace {
@@ -99,41 +101,42 @@ __global__ void count_adjacent_dups(const u64 *__restrict__ sorted, i64 n, int *
 
 }  // namespace
 
-int sbd_sort_strings(sbd_ctx *ctx, Sector &s) {
-    i64 n = s.n;
+int sbd_radix_sort(sbd_ctx *ctx, const u64 *keys, i64 n, int key_bits, DevBuf &sorted, DevBuf &perm) {
     cudaStream_t st = ctx->stream;
-    SBD_CUDA(ctx, s.sorted.ensure(sizeof(u64) * (n ? n : 1)));
-    SBD_CUDA(ctx, s.perm.ensure(sizeof(int32_t) * (n ? n : 1)));
+    SBD_CUDA(ctx, sorted.ensure(sizeof(u64) * (n ? n : 1)));
+    SBD_CUDA(ctx, perm.ensure(sizeof(int32_t) * (n ? n : 1)));
     if (n == 0) return SBD_OK;
-    int nblocks = (int)((n + kTile - 1) / kTile);
-    DevBuf k2, v2, hist, flag;
+    const int nblocks = (int)((n + kTile - 1) / kTile);
+    DevBuf k2, v2, hist;
     SBD_CUDA(ctx, k2.ensure(sizeof(u64) * n));
     SBD_CUDA(ctx, v2.ensure(sizeof(int32_t) * n));
     SBD_CUDA(ctx, hist.ensure(sizeof(int) * 256 * nblocks + 64));
-    SBD_CUDA(ctx, flag.ensure(sizeof(int)));
-
-    int passes = (ctx->norb + 7) / 8;
-    // ping-pong: start from caller order with identity values
-    const u64 *kin = s.str.as<u64>();
+    const int passes = std::max(1, (key_bits + 7) / 8);
+    // ping-pong from caller order with identity values; the LAST pass lands in sorted/perm
+    const u64 *kin = keys;
     const int32_t *vin = nullptr;
-    u64 *bufk[2] = {s.sorted.as<u64>(), k2.as<u64>()};
-    int32_t *bufv[2] = {s.perm.as<int32_t>(), v2.as<int32_t>()};
-    // make the LAST pass land in s.sorted / s.perm
+    u64 *bufk[2] = {sorted.as<u64>(), k2.as<u64>()};
+    int32_t *bufv[2] = {perm.as<int32_t>(), v2.as<int32_t>()};
     int cur = (passes % 2 == 1) ? 0 : 1;
     for (int p = 0; p < passes; ++p) {
-        int shift = 8 * p;
-        radix_hist<<<nblocks, kTile, 0, st>>>(kin, n, shift, hist.as<int>(), nblocks);
+        radix_hist<<<nblocks, kTile, 0, st>>>(kin, n, 8 * p, hist.as<int>(), nblocks);
         exclusive_scan_small<<<1, 1024, 0, st>>>(hist.as<int>(), 256 * nblocks);
-        radix_scatter<<<nblocks, kTile, 0, st>>>(kin, vin, bufk[cur], bufv[cur], n, shift, hist.as<int>(), nblocks);
+        radix_scatter<<<nblocks, kTile, 0, st>>>(kin, vin, bufk[cur], bufv[cur], n, 8 * p, hist.as<int>(), nblocks);
         SBD_LAUNCHED(ctx, "radix sort");
         kin = bufk[cur];
         vin = bufv[cur];
         cur ^= 1;
     }
-    if (passes == 0) {  // norb == 0 cannot happen (norb >= 1), kept for safety
-        SBD_CUDA(ctx, cudaMemcpyAsync(s.sorted.p, s.str.p, sizeof(u64) * n, cudaMemcpyDeviceToDevice, st));
-        iota_i32<<<grid_for(n, 256), 256, 0, st>>>(s.perm.as<int32_t>(), n);
-    }
+    return SBD_OK;
+}
+
+int sbd_sort_strings(sbd_ctx *ctx, Sector &s) {
+    const i64 n = s.n;
+    cudaStream_t st = ctx->stream;
+    int rc = sbd_radix_sort(ctx, s.str.as<u64>(), n, ctx->norb, s.sorted, s.perm);
+    if (rc || n == 0) return rc;
+    DevBuf flag;
+    SBD_CUDA(ctx, flag.ensure(sizeof(int)));
     SBD_CUDA(ctx, cudaMemsetAsync(flag.p, 0, sizeof(int), st));
     count_adjacent_dups<<<grid_for(n, 256), 256, 0, st>>>(s.sorted.as<u64>(), n, flag.as<int>());
     SBD_LAUNCHED(ctx, "dup check");

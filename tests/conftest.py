@@ -26,6 +26,17 @@ def small_golden():
 
 
 @pytest.fixture(scope="session")
+def explicit_golden():
+    return dict(np.load(os.path.join(GOLDEN, "explicit.npz")))
+
+
+@pytest.fixture(scope="session")
+def explicit_meta():
+    with open(os.path.join(GOLDEN, "explicit_meta.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="session")
 def small_meta():
     with open(os.path.join(GOLDEN, "small_meta.json")) as f:
         return json.load(f)
