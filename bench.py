@@ -219,6 +219,76 @@ def run_reference(args):
     return 0
 
 
+# -- explicit-basis section ---------------------------------------------------------------
+
+EXPLICIT_STRINGS = 1000  # per spin: the first 1000 cfg2 strings, all pairs, shuffled = 1e6 dets
+
+
+def explicit_bench(table, a, b, dev, stream, args, with_cpu=True):
+    """Explicit-mode sigma (explicit_sigma_kernel) on 1e6 determinants: device-timed dets/s,
+    parity against the product kernel on the same determinants, and the oracle port of the
+    reference's _explicit_kernel on a bounded row sample."""
+    import torch
+
+    from paper_2601_16637_b200 import Determinant, HamiltonianApplier, SelectedBasis
+
+    w = WORKLOAD
+    sa, sb = a[:EXPLICIT_STRINGS], b[:EXPLICIT_STRINGS]
+    pairs = np.random.default_rng(7).permutation(sa.size * sb.size)
+    da, db = sa[pairs // sb.size], sb[pairs % sb.size]
+    basis = SelectedBasis.explicit([Determinant(int(x), int(y)) for x, y in zip(da, db)], w["norb"], w["n_alpha"],
+                                   w["n_beta"])
+    app = HamiltonianApplier(basis, table, device=dev.index)
+    n = basis.dimension
+    x = torch.empty(n, dtype=torch.float64, device=dev).normal_(generator=torch.Generator(device=dev).manual_seed(3))
+    y = torch.empty_like(x)
+    for _ in range(3):
+        app.sigma_device(x, out=y)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(10, args.steps)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(reps):
+        app.sigma_device(x, out=y)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t = e0.elapsed_time(e1) / 1e3 / reps
+    # same determinants through the product kernel
+    prod = HamiltonianApplier(SelectedBasis.product(sa.tolist(), sb.tolist(), w["norb"], w["n_alpha"], w["n_beta"]),
+                              table, device=dev.index)
+    xp = torch.empty_like(x)
+    xp[torch.from_numpy(pairs).to(dev)] = x
+    yp = prod.sigma_device(xp)[torch.from_numpy(pairs).to(dev)]
+    parity = float((yp - y).abs().max() / y.abs().max())
+    out = {"workload": f"explicit list: all {sa.size} x {sb.size} pairs of the first cfg2 strings, shuffled",
+           "n_dets": int(n), "value": n / t, "unit": "dets/s", "ms_per_step": t * 1e3,
+           "parity_vs_product_kernel": parity, "kernel": "explicit_sigma_kernel"}
+    if with_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+
+        inst = O.ExplicitInstance.make(w["norb"], table.h, table.eri, table.e_core, da, db)
+        xh = x.cpu().numpy()
+        d = np.zeros(n)
+
+        def run(rows):
+            d[:rows] = [O.lib().orc_hdiag(int(p), int(q), inst.h, inst.norb, inst.eri, inst.e_core)
+                        for p, q in zip(da[:rows], db[:rows])]
+            t0 = time.perf_counter()
+            yc = O.sigma_explicit(inst, xh, d, rows=(0, rows))
+            return yc, time.perf_counter() - t0
+
+        _, dt = run(64)  # probe, then a ~8 s sample
+        rows = int(min(n, max(64, 64 * 8.0 / max(dt, 1e-4))))
+        yc, dt = run(rows)
+        err = float(np.abs(yc - y[:rows].cpu().numpy()).max() / max(np.abs(yc).max(), 1e-300))
+        out["cpu_baseline"] = {"value": rows / dt, "unit": "dets/s", "cores": O.max_threads(), "kind": "port",
+                               "sample": f"oracle C port of _explicit_kernel on determinants [0,{rows}) "
+                                         f"({dt:.2f} s), all host threads; max rel diff vs GPU {err:.1e}"}
+    del app, prod
+    return out
+
+
 # -- GPU arm -----------------------------------------------------------------------------
 
 
@@ -388,6 +458,11 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(table, a, b)
 
+    # ---- explicit (full-bitstring) basis: SURVEY section 8(f)2 ---------------------------
+    expl = None
+    if rank == 0 and world == 1 and not args.no_explicit:
+        expl = explicit_bench(table, a, b, dev, stream, args, with_cpu=not args.no_cpu)
+
     launches_per_step = 4  # transpose, beta side, task-0 cross, alpha side
     line = {
         "metric": METRIC, "value": value, "unit": "dets/s", "n_gpus": world, "steps": args.steps,
@@ -407,6 +482,7 @@ def run_ours(args):
         "clocks": clocks,
         "davidson": dav,
         "cpu_baseline": cpu,
+        "explicit": expl,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -427,6 +503,7 @@ def main():
     ap.add_argument("--davidson-iters", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-explicit", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

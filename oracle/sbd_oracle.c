@@ -302,24 +302,25 @@ static double explicit_row(i64 i, const double *x, const double *diag, const u64
 }
 
 typedef struct {
-    i64 n; double *y; const double *x, *diag; const u64 *det_a, *det_b, *sa, *sb; const i64 *perm;
+    i64 n, i0; double *y; const double *x, *diag; const u64 *det_a, *det_b, *sa, *sb; const i64 *perm;
     u64 mask; const double *h, *eri; int norb; double e_core;
 } explicit_job;
 
 static void explicit_range(i64 lo, i64 hi, void *vp) {
     explicit_job *j = (explicit_job *)vp;
     for (i64 i = lo; i < hi; ++i)
-        j->y[i] += explicit_row(i, j->x, j->diag, j->det_a, j->det_b, j->sa, j->sb, j->perm, j->n, j->mask, j->h,
-                                j->norb, j->eri, j->e_core);
+        j->y[i] += explicit_row(j->i0 + i, j->x, j->diag, j->det_a, j->det_b, j->sa, j->sb, j->perm, j->n, j->mask,
+                                j->h, j->norb, j->eri, j->e_core);
 }
 
-/* apply.py:429-444 + 698-703: y = H x over an explicit determinant list (sa/sb/perm from np.lexsort) */
-void orc_sigma_explicit(i64 n, double *y, const double *x, const double *diag, const u64 *det_a, const u64 *det_b,
-                        const u64 *sa, const u64 *sb, const i64 *perm, const double *h, int norb, const double *eri,
-                        double e_core, int nthreads) {
-    explicit_job j = {n, y, x, diag, det_a, det_b, sa, sb, perm,
+/* apply.py:429-444 + 698-703: y = H x over an explicit determinant list (sa/sb/perm from
+ * np.lexsort); rows [i0, i1) only (y has i1 - i0 entries, diag is indexed globally) */
+void orc_sigma_explicit(i64 n, i64 i0, i64 i1, double *y, const double *x, const double *diag, const u64 *det_a,
+                        const u64 *det_b, const u64 *sa, const u64 *sb, const i64 *perm, const double *h, int norb,
+                        const double *eri, double e_core, int nthreads) {
+    explicit_job j = {n, i0, y, x, diag, det_a, det_b, sa, sb, perm,
                       norb >= 64 ? ~(u64)0 : (bit(norb) - 1), h, eri, norb, e_core};
-    par_for(n, 64, nthreads, explicit_range, &j);
+    par_for(i1 - i0, 64, nthreads, explicit_range, &j);
 }
 
 /* ---- excitation tables: basis.py:72-103 (enumeration order) + 362-403 ---- */
