@@ -71,6 +71,18 @@ int sbd_set_strings(sbd_ctx *ctx, int spin, const uint64_t *strings_host, int64_
 int sbd_set_dets(sbd_ctx *ctx, const uint64_t *alpha_host, const uint64_t *beta_host, int64_t n,
                  int n_alpha_elec, int n_beta_elec);
 
+/* Device ingestion of sampled determinants (ingest_samples, basis.py:251-313):
+ * samples whose per-spin popcount differs from the electron counts are
+ * filtered, duplicates dropped keeping FIRST-SEEN order, multiplicities
+ * counted (det_counts), and the unique alpha / beta halves collected in
+ * first-seen order.  Bits at or above norb -> SBD_EINVAL.  Results stay in the
+ * context until sbd_ingest_export copies them out (any pointer may be NULL). */
+int sbd_ingest_samples(sbd_ctx *ctx, const uint64_t *alpha_host, const uint64_t *beta_host, int64_t n, int norb,
+                       int n_alpha_elec, int n_beta_elec, int64_t *n_filtered, int64_t *n_unique_dets,
+                       int64_t *n_unique_alpha, int64_t *n_unique_beta);
+int sbd_ingest_export(sbd_ctx *ctx, uint64_t *det_alpha_host, uint64_t *det_beta_host, int64_t *det_count_host,
+                      uint64_t *alpha_strings_host, uint64_t *beta_strings_host);
+
 /* Configuration processing + excitation generation on the device:
  * radix sort/unique of each sector's strings, CSR in-set singles/doubles
  * with phases (build_excitation_table, basis.py:362-403; build_spin_tables,

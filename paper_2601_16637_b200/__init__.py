@@ -31,6 +31,7 @@ from .basis import (
     single_phase,
 )
 from .davidson import DavidsonOptions, DavidsonResult, DavidsonStats, davidson_solve
+from .ingest import ingest_sample_arrays, start_vector
 from .integrals import FcidumpError, IntegralTable, parse_fcidump, write_fcidump
 
 __all__ = [
@@ -51,6 +52,9 @@ __all__ = [
     "build_excitation_table",
     "compute_diagonal",
     "apply_H_full",
+    # B200 extensions: device ingestion
+    "ingest_sample_arrays",
+    "start_vector",
     "ExcitationTable",
     "DavidsonStats",
     "FcidumpError",

@@ -30,6 +30,8 @@ _SIGS = {
     "sbd_set_integrals": [_vp, _c_int, _vp, _vp, _c_i64, _c_dbl],
     "sbd_set_strings": [_vp, _c_int, _vp, _c_i64, _c_int],
     "sbd_set_dets": [_vp, _vp, _vp, _c_i64, _c_int, _c_int],
+    "sbd_ingest_samples": [_vp, _vp, _vp, _c_i64, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp],
+    "sbd_ingest_export": [_vp, _vp, _vp, _vp, _vp, _vp],
     "sbd_build_tables": [_vp],
     "sbd_table_counts": [_vp, _c_int, _vp, _vp, _vp],
     "sbd_export_table": [_vp, _c_int] + [_vp] * 12,

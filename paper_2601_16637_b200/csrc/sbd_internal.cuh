@@ -66,6 +66,13 @@ struct Sector {
     bool built = false;
 };
 
+// device ingestion results (sbd_ingest.cu), first-seen order
+struct IngestState {
+    DevBuf det_a, det_b, det_count, alpha, beta;
+    i64 n_det = 0, n_alpha = 0, n_beta = 0, n_samples = 0, n_kept = 0;
+    bool ready = false;
+};
+
 struct sbd_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -99,6 +106,7 @@ struct sbd_ctx {
     DevBuf grp_off;              // int32[n_alpha + 1]: dets sorted by (A, B), group of alpha A
     DevBuf grp_b, grp_perm;      // int32[n_det]: sorted B and caller index
     bool explicit_built = false;
+    IngestState ingest;
 
     i64 own_lo() const { return row_lo; }
     i64 own_hi() const { return row_hi < 0 ? sec[0].n : row_hi; }
