@@ -91,6 +91,7 @@ class DavidsonStats:
     restart_iters: list = field(default_factory=list)
     iter_seconds: list = field(default_factory=list)  # B200 extension: wall time per iteration
     phase_ms: dict = field(default_factory=dict)  # B200 extension: summed device time per phase
+    host_ms: dict = field(default_factory=dict)  # B200 extension: host time per section (enqueue / wait)
 
 
 @dataclass
@@ -352,11 +353,10 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
     host_ms = {}
     _tick = [time.perf_counter()]
 
-    def hp(name):  # host-side time per section (profile mode only)
-        if opts.profile:
-            t = time.perf_counter()
-            host_ms[name] = host_ms.get(name, 0.0) + (t - _tick[0]) * 1e3
-            _tick[0] = t
+    def hp(name):  # host-side time per section (perf_counter only: always on, reported in stats.host_ms)
+        t = time.perf_counter()
+        host_ms[name] = host_ms.get(name, 0.0) + (t - _tick[0]) * 1e3
+        _tick[0] = t
 
     def readback(t_dev, cnt):
         host[:cnt].copy_(t_dev[:cnt], non_blocking=True)
@@ -495,6 +495,7 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
     eng("sbd_combine", _p(V), kk, ld, n_loc, _p(Y_dev), mk, _p(U), n_loc)
     del V, W, Tv
     torch.cuda.current_stream(dev).synchronize()
+    stats.host_ms = host_ms
     if opts.profile:
         stats.phase_ms = eng.summary()
         stats.phase_ms.update({"host:" + k_: v for k_, v in host_ms.items()})
