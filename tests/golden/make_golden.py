@@ -225,8 +225,36 @@ def make_explicit():
         json.dump(meta, f, indent=1, sort_keys=True)
 
 
+CLI_CASES = [
+    ["solve", "--gen-random", "8,4,4,3", "--strings", "30", "--json"],
+    ["solve", "--gen-random", "10,5,4,7", "--strings", "60", "--nroots", "2", "--json"],
+    ["solve", "--gen-random", "8,3,3,5", "--strings", "200", "--mode", "explicit", "--json"],
+    ["verify", "--gen-random", "6,3,3,2", "--strings", "20", "--json"],
+]
+
+
+def make_cli():
+    """Reports of the reference CLI (cli.py) on --gen-random instances."""
+    import contextlib
+    import io
+
+    from sbdiag.cli import main
+
+    out = []
+    for argv in CLI_CASES:
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = main(list(argv))
+        rep = json.loads(buf.getvalue())
+        for k in ("solve_seconds", "apply_seconds"):
+            rep.pop(k, None)
+        out.append(dict(argv=argv, rc=rc, report=rep))
+    with open(os.path.join(HERE, "cli.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
-    jobs = dict(small=make_small, cfg1=make_cfg1, cfg2=make_cfg2, cfg4=make_cfg4, explicit=make_explicit,
+    jobs = dict(small=make_small, cli=make_cli, cfg1=make_cfg1, cfg2=make_cfg2, cfg4=make_cfg4, explicit=make_explicit,
                 **{"cfg1-davidson": make_cfg1_davidson})
     for arg in sys.argv[1:]:
         jobs[arg]()

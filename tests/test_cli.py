@@ -1,0 +1,99 @@
+"""CLI parity (reference cli.py): commands, flags, exit codes and report schema.
+
+CPU tests cover argument handling and exit codes (usage/input errors exit 1
+before any device work); GPU tests compare reports against the reference
+CLI's own reports (tests/golden/cli.json, made by make_golden.py cli).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2601_16637_b200.cli import EXIT_INPUT_ERROR, build_parser, main
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "cli.json")
+
+
+@pytest.mark.parametrize("argv", [[], ["bogus"], ["solve"], ["solve", "--gen-random", "3,2"],
+                                  ["solve", "--gen-random", "99,2,2,1"], ["bench", "--gen-random", "x"],
+                                  ["solve", "--fcidump", "/nonexistent", "--samples", "/nonexistent"]])
+def test_usage_and_input_errors_exit_1(argv, capsys):
+    assert main(argv) == EXIT_INPUT_ERROR
+    assert "error:" in capsys.readouterr().err
+
+
+def test_parser_matches_reference_flags():
+    p = build_parser()
+    a = p.parse_args(["solve", "--gen-random", "8,4,4,3", "--strings", "30", "--nroots", "2", "--tol", "1e-9",
+                      "--max-iter", "50", "--max-subspace", "16", "--restart-keep", "3", "--delta", "1e-5",
+                      "--json", "--mode", "explicit", "--workers", "1", "--overlap", "off", "--deterministic"])
+    assert (a.nroots, a.tol, a.max_iter, a.max_subspace, a.restart_keep, a.delta) == (2, 1e-9, 50, 16, 3, 1e-5)
+    v = p.parse_args(["verify", "--gen-random", "6,3,3,2", "--tol-match", "1e-7", "--oracle-cap", "100"])
+    assert (v.tol_match, v.oracle_cap) == (1e-7, 100)
+    b = p.parse_args(["bench", "--gen-random", "6,3,3,2", "--workers", "1", "--repeats", "2"])
+    assert (b.workers_list, b.repeats) == ("1", 2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", range(4))
+def test_reports_match_reference_cli(case, capsys):
+    with open(GOLDEN) as f:
+        ref = json.load(f)[case]
+    rc = main(list(ref["argv"]))
+    rep = json.loads(capsys.readouterr().out)
+    assert rc == ref["rc"]
+    r = ref["report"]
+    assert rep["schema_version"] == r["schema_version"] and rep["command"] == r["command"]
+    assert rep["basis"] == r["basis"]
+    if r["command"] == "solve":
+        np.testing.assert_allclose(rep["energies"], r["energies"], atol=1e-8)
+        assert rep["converged"] == r["converged"]
+        assert abs(rep["iterations"] - r["iterations"]) <= 1
+        assert set(r) - {"solve_seconds", "apply_seconds"} <= set(rep)
+    else:
+        assert abs(rep["davidson_energy"] - r["davidson_energy"]) <= 1e-8
+        assert abs(rep["oracle_energy"] - r["oracle_energy"]) <= 1e-8
+        assert rep["passed"] == r["passed"]
+
+
+@pytest.mark.gpu
+def test_bench_and_text_report(capsys, tmp_path):
+    out = tmp_path / "rep.txt"
+    assert main(["bench", "--gen-random", "8,4,4,3", "--strings", "30", "--repeats", "2", "--out", str(out)]) == 0
+    text = out.read_text()
+    assert "mult timing over 2 repeats" in text and "speedup" in text
+    assert main(["solve", "--gen-random", "8,4,4,3", "--strings", "30"]) == 0
+    assert "energies = [" in capsys.readouterr().out
+
+
+@pytest.mark.gpu
+def test_solve_from_fcidump_and_samples(tmp_path, capsys):
+    """The file path: FCIDUMP + sample lines -> ingest -> multiplicity start vector -> Davidson."""
+    from paper_2601_16637_b200 import (DavidsonOptions, Determinant, HamiltonianApplier, davidson_solve,
+                                       det_to_line, ingest_samples, start_vector, write_fcidump)
+    from paper_2601_16637_b200.synth import random_integrals, random_product_strings
+
+    norb, na, nb = 8, 3, 2
+    table = random_integrals(norb, seed=4)
+    table.nelec, table.ms2 = na + nb, na - nb
+    fcid = tmp_path / "FCIDUMP"
+    fcid.write_text(write_fcidump(table))
+    a, b = random_product_strings(norb, na, nb, 12, 9, seed=6)
+    rng = np.random.default_rng(2)
+    lines = [det_to_line(Determinant(int(a[i]), int(b[j])), norb)
+             for i, j in zip(rng.integers(0, a.size, 400), rng.integers(0, b.size, 400))]
+    lines += ["# comment", "", det_to_line(Determinant(0b1111, 0b11), norb)]  # filtered (4 alpha electrons)
+    samples = tmp_path / "samples.txt"
+    samples.write_text("\n".join(lines) + "\n")
+    assert main(["solve", "--fcidump", str(fcid), "--samples", str(samples), "--json"]) == 0
+    rep = json.loads(capsys.readouterr().out)
+    basis, report = ingest_samples(lines, norb, na, nb)
+    assert rep["ingest"] == {"n_lines": report.n_lines, "n_filtered": report.n_filtered,
+                             "n_duplicates": report.n_duplicates}
+    app = HamiltonianApplier(basis, table)
+    res = davidson_solve(app, app.diag, x0=start_vector(basis, report), opts=DavidsonOptions())
+    np.testing.assert_allclose(rep["energies"], res.energies, atol=1e-10)
