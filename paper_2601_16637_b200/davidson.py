@@ -317,8 +317,8 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
     jac_v = torch.zeros((k_max * k_max,), **f64)
     jac_info = torch.zeros(1, dtype=torch.int32, device=dev)
     c_dev = torch.zeros(64, **f64)
-    pack = torch.zeros(64 + 8, **f64)
-    host = torch.zeros(64 + 8, dtype=torch.float64, pin_memory=True)
+    pack = torch.zeros(2 * 64 + 32, **f64)
+    host = torch.zeros(2 * 64 + 32, dtype=torch.float64, pin_memory=True)
 
     # start vector (davidson.py:219-227)
     if x0 is None:
@@ -406,7 +406,16 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
         pack[2 * mk + 1] = jac_info[0].to(torch.float64)
         if opts.track_orthogonality:
             pack[2 * mk + 2] = torch.linalg.norm(G[:k, :k] - eye[:k, :k])
-        hv = readback(pack, 2 * mk + 3)
+        # speculative CGS pass 1 on the projected root (the usual next step: not
+        # converged, same target root, no restart), read back with the pack, so an
+        # iteration costs one host round trip instead of two
+        spec = opts.reorthogonalize and k < k_max and iteration < opts.max_iters
+        npk = 2 * mk + 3
+        if spec:
+            eng("sbd_gs_update", _p(V), k, ld, n_loc, _p(c_dev), _p(Tv[jp]), _p(small2))
+            reduce(small2[: k + 1])
+            pack[npk:npk + k + 1].copy_(small2[: k + 1])
+        hv = readback(pack, npk + (k + 1 if spec else 0))
         stats.apply_seconds.append(ev0.elapsed_time(ev1) / 1e3)
         if hv[2 * mk + 1] >= 64:
             raise RuntimeError("Jacobi sweep limit 64 reached without convergence")
@@ -431,6 +440,7 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
 
         target = int(np.argmax(res_norms > opts.tol_residual))
         t_vec = Tv[target]
+        pre = (hv[npk:npk + k].copy(), float(hv[npk + k])) if spec and target == jp else None
         if target != jp:
             # the fused projection used another root: one extra pass
             eng("sbd_vdots2", _p(V), k, ld, n_loc, _p(t_vec), _p(t_vec), _p(small))
@@ -462,7 +472,7 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
             ritz_rotated = True
 
         v_ok = _orthogonalize_device(eng, V, k, ld, n_loc, t_vec, c_dev, t_norm2, opts, small2, scale, reduce,
-                                     readback)
+                                     readback, pre)
         attempts = 0
         while not v_ok and attempts < 3:
             stats.breakdowns += 1
@@ -505,8 +515,11 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
     return DavidsonResult(energies=theta.copy(), vectors=vectors, residual_norms=res_norms.copy(), stats=stats)
 
 
-def _orthogonalize_device(eng, V, k, ld, n_loc, t, c, t_norm2, opts, small, scale, reduce, readback) -> bool:
+def _orthogonalize_device(eng, V, k, ld, n_loc, t, c, t_norm2, opts, small, scale, reduce, readback,
+                          pre=None) -> bool:
     """CGS2 of t against V[:k] given c = V^T t (device); writes the normalised V[k] on success.
+
+    ``pre = (c2, |t'|^2)``: CGS pass 1 already ran (speculatively, output in ``small``).
 
     Rejection rule of the reference orthogonalize (davidson.py:166-185): the
     remainder norm must stay >= 1e-12 of the input norm.
@@ -516,10 +529,13 @@ def _orthogonalize_device(eng, V, k, ld, n_loc, t, c, t_norm2, opts, small, scal
         return False
     if opts.reorthogonalize:
         # CGS pass 1: t' = t - V c ; c2 = V^T t' ; |t'|^2
-        eng("sbd_gs_update", _p(V), k, ld, n_loc, _p(c), _p(t), _p(small))
-        reduce(small[: k + 1])
-        hv = readback(small, k + 1)
-        c2, n2p = hv[:k], float(hv[k])
+        if pre is None:
+            eng("sbd_gs_update", _p(V), k, ld, n_loc, _p(c), _p(t), _p(small))
+            reduce(small[: k + 1])
+            hv = readback(small, k + 1)
+            c2, n2p = hv[:k], float(hv[k])
+        else:
+            c2, n2p = pre
         n2 = n2p - float(c2 @ c2)  # |t' - V c2|^2 for orthonormal V
         c2d = small[:k].clone()
         if n2p > 0.0 and n2 > 0.5 * n2p:

@@ -14,6 +14,12 @@ GPU (``torch.distributed``, NCCL over NVLink/NVSwitch):
   alpha-beta parts (``sbd_sigma_remote``) start once the gather lands;
 * Davidson: vectors stay row-partitioned; the O(k) dot products of every
   fused pass are all-reduced (a few hundred bytes per iteration).
+* sparse exchange (the successor of the reference ring): a rank
+  only reads the x rows its own rows connect to.  When those are a minority
+  of the remote rows (cfg4: ~40%), the all-gather is replaced by grouped
+  point-to-point transfers of exactly the referenced rows (request lists are
+  exchanged once at construction; each sigma packs, sends, receives and
+  scatters rows), cutting the per-sigma NVLink volume in proportion.
 
 ``DistributedApplier(...).apply(x)`` keeps the reference signature (full
 numpy x on every rank in, full y out).  The device-resident path is
@@ -102,6 +108,34 @@ class Comm:
         if self.world > 1:
             self.dist.barrier(group=self.group)
 
+    def allgather_object(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def exchange_rows(self, sends: dict, recvs: dict):
+        """Point-to-point transfers {peer: tensor}; returns a list of waitables (empty when staged)."""
+        if self.backend == "gloo":  # gloo: host-staged, blocking
+            import torch
+
+            ops, host_recv = [], {}
+            for p, t in sends.items():
+                ops.append(self.dist.isend(t.cpu(), self._global(p), group=self.group))
+            for p, t in recvs.items():
+                host_recv[p] = torch.empty(t.shape, dtype=t.dtype)
+                ops.append(self.dist.irecv(host_recv[p], self._global(p), group=self.group))
+            for op in ops:
+                op.wait()
+            for p, t in recvs.items():
+                t.copy_(host_recv[p])
+            return []
+        ops = [self.dist.P2POp(self.dist.isend, t, self._global(p), group=self.group) for p, t in sends.items()]
+        ops += [self.dist.P2POp(self.dist.irecv, t, self._global(p), group=self.group) for p, t in recvs.items()]
+        return self.dist.batch_isend_irecv(ops) if ops else []
+
+    def _global(self, rank: int) -> int:
+        return rank if self.group is None else self.dist.get_global_rank(self.group, rank)
+
 
 class _CudaRank:
     """This rank's slice of the operator on its GPU (a row-windowed HamiltonianApplier)."""
@@ -129,6 +163,12 @@ class _CudaRank:
     def context(self):
         return self.app.context
 
+    def alpha_targets(self, lo, hi):
+        """Alpha rows that rows [lo, hi) connect to (singles and doubles, in-set)."""
+        t = self.app.tables.alpha
+        parts = [t.s_tgt[t.s_off[lo]:t.s_off[hi]], t.d_tgt[t.d_off[lo]:t.d_off[hi]]]
+        return np.unique(np.concatenate(parts).astype(np.int64))
+
 
 class DistributedApplier:
     """One rank of the alpha-block partitioned y = H x (reference ``distsim.py:130-316``).
@@ -139,7 +179,8 @@ class DistributedApplier:
     """
 
     def __init__(self, basis, table, tables=None, partition: Optional[Partition] = None, n_workers: Optional[int] = None,
-                 overlap: bool = True, transfer_delay: float = 0.0, group=None, device=None, _rank_engine=None):
+                 overlap: bool = True, transfer_delay: float = 0.0, group=None, device=None, _rank_engine=None,
+                 exchange: str = "auto", sparse_threshold: float = 0.6):
         import torch
 
         if basis.mode != "product":
@@ -173,6 +214,58 @@ class DistributedApplier:
         nb = self.n_beta
         self._views = [self._x_full[a * nb:b * nb] for a, b in self.partition.alpha_blocks]
         self.apply_count = 0
+        if exchange not in ("auto", "allgather", "sparse"):
+            raise ValueError(f"exchange must be 'auto', 'allgather' or 'sparse', got {exchange!r}")
+        self.exchange = "allgather"
+        self.remote_rows_needed = 0
+        if world > 1 and exchange != "allgather":
+            self._plan_sparse(exchange, sparse_threshold)
+
+    # -- sparse row exchange ------------------------------------------
+    def _plan_sparse(self, exchange, threshold):
+        import torch
+
+        blocks = self.partition.alpha_blocks
+        need = self.engine.alpha_targets(self.lo, self.hi)
+        need = need[(need < self.lo) | (need >= self.hi)]
+        owner = np.searchsorted(np.array([b for _, b in blocks]), need, side="right")
+        req = {int(p): need[owner == p] for p in np.unique(owner)}
+        everyone = self.comm.allgather_object(req)  # setup only: who needs which of my rows
+        n_alpha = blocks[-1][1]
+        # the decision must be the same on every rank: the largest needed fraction decides
+        frac = max(sum(v.size for v in r.values()) / max(n_alpha - (b - a), 1) for r, (a, b) in zip(everyone, blocks))
+        self.remote_rows_needed = int(need.size)
+        self.remote_rows_total = int(n_alpha - (self.hi - self.lo))
+        self.sparse_fraction = float(frac)
+        if exchange == "auto" and frac > threshold:
+            return  # dense enough: the all-gather moves about as much and is one collective
+        dev = self.device
+        nb = self.n_beta
+        self._recv_rows = {p: torch.from_numpy(rows).to(dev) for p, rows in req.items() if rows.size}
+        self._recv_buf = {p: torch.empty((rows.numel(), nb), dtype=torch.float64, device=dev)
+                          for p, rows in self._recv_rows.items()}
+        self._send_rows = {}
+        for q, r in enumerate(everyone):
+            if q != self.rank and self.rank in r and r[self.rank].size:
+                self._send_rows[q] = torch.from_numpy(r[self.rank] - self.lo).to(dev)
+        self._send_buf = {q: torch.empty((rows.numel(), nb), dtype=torch.float64, device=dev)
+                          for q, rows in self._send_rows.items()}
+        self.exchange = "sparse"
+
+    def _sparse_start(self, x_own):
+        nb = self.n_beta
+        xo = x_own.view(-1, nb)
+        for q, rows in self._send_rows.items():
+            self._send_buf[q].copy_(xo.index_select(0, rows))
+        return self.comm.exchange_rows(self._send_buf, self._recv_buf)
+
+    def _sparse_finish(self, x_own, works):
+        for w in works:
+            w.wait()
+        xf = self._x_full.view(-1, self.n_beta)
+        for p, rows in self._recv_rows.items():
+            xf.index_copy_(0, rows, self._recv_buf[p])
+        self._views[self.rank].copy_(x_own)
 
     # -- device-resident path -----------------------------------------------------
     def apply_device(self, x_own, y_own=None):
@@ -183,6 +276,16 @@ class DistributedApplier:
             raise ValueError(f"expected {self.n_own} local amplitudes, got {x_own.numel()}")
         y = torch.empty(self.n_own, dtype=torch.float64, device=self.device) if y_own is None else y_own
         self.apply_count += 1
+        if self.exchange == "sparse":
+            works = self._sparse_start(x_own)                      # NCCL p2p, referenced rows only
+            if self.overlap:
+                self.engine.sigma_local(x_own)                     # compute stream, concurrently
+                self._sparse_finish(x_own, works)
+            else:
+                self._sparse_finish(x_own, works)
+                self.engine.sigma_local(x_own)
+            self.engine.sigma_remote(self._x_full, y)
+            return y
         if self.overlap:
             work = self.comm.allgather_start(self._views, x_own)  # NCCL stream
             self.engine.sigma_local(x_own)                         # compute stream, concurrently

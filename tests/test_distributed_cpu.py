@@ -44,11 +44,16 @@ class OracleRank:
     def sigma_local(self, x_own):
         self.local_calls += 1
 
+    def alpha_targets(self, lo, hi):
+        t = self.inst.ta
+        return np.unique(np.concatenate([t["s_tgt"][t["s_off"][lo]:t["s_off"][hi]],
+                                         t["d_tgt"][t["d_off"][lo]:t["d_off"][hi]]]).astype(np.int64))
+
     def sigma_remote(self, x_full, y_own):
         y_own.copy_(torch.from_numpy(self.O.sigma(self.inst, x_full.numpy(), bra=(self.lo, self.hi))))
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, q, exchange="allgather"):
     try:
         import sys
 
@@ -63,9 +68,12 @@ def _worker(rank, world, port, case, q):
         norb, na, nb, nsa, nsb, seed = case
         table = random_integrals(norb, seed)
         basis = random_product_basis(norb, na, nb, nsa, nsb, seed + 1)
-        dapp = DistributedApplier(basis, table, _rank_engine=OracleRank)
+        dapp = DistributedApplier(basis, table, _rank_engine=OracleRank, exchange=exchange)
+        if exchange == "sparse":  # rows a rank does not receive must never be read
+            dapp._x_full.fill_(float("nan"))
         x = np.random.default_rng(seed).standard_normal(basis.dimension)
         y = dapp(x)
+        assert dapp.exchange == ("sparse" if exchange == "sparse" else "allgather")
         x0 = dapp.global_argmin_start()
         dist.barrier()
         q.put((rank, dapp.lo, dapp.hi, y, x0.numpy(), dapp.engine.local_calls))
@@ -76,12 +84,14 @@ def _worker(rank, world, port, case, q):
         q.put((rank, "error", traceback.format_exc()))
 
 
+@pytest.mark.parametrize("exchange", ["allgather", "sparse"])
 @pytest.mark.parametrize("world,case", [
     (2, (8, 4, 3, 30, 25, 3)),   # even-ish split
     (3, (8, 4, 4, 31, 20, 5)),   # uneven alpha blocks (11, 10, 10)
     (2, (6, 3, 3, 3, 20, 7)),    # tiny alpha sector
+    (4, (12, 4, 4, 60, 20, 9)),  # sparse connectivity: ranks need a fraction of the remote rows
 ])
-def test_partitioned_apply_matches_serial(world, case):
+def test_partitioned_apply_matches_serial(world, case, exchange):
     import oracle as O
 
     from paper_2601_16637_b200.distributed import make_partition
@@ -90,7 +100,7 @@ def test_partitioned_apply_matches_serial(world, case):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in range(world)]

@@ -28,7 +28,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, q, exchange="auto"):
     try:
         import sys
 
@@ -46,7 +46,10 @@ def _worker(rank, world, port, case, q):
         norb, na, nb, nsa, nsb, seed, nroots = case
         table = random_integrals(norb, seed)
         basis = random_product_basis(norb, na, nb, nsa, nsb, seed + 1)
-        dapp = DistributedApplier(basis, table, device=0)
+        dapp = DistributedApplier(basis, table, device=0, exchange=exchange)
+        if exchange == "sparse":  # rows a rank does not receive must never be read
+            assert dapp.exchange == "sparse"
+            dapp._x_full.fill_(float("nan"))
         x = np.random.default_rng(seed).standard_normal(basis.dimension)
         y = dapp(x)
         res = dapp.davidson(opts=DavidsonOptions(n_roots=nroots, max_subspace=16, restart_keep=4))
@@ -59,15 +62,18 @@ def _worker(rank, world, port, case, q):
         q.put((rank, "error", traceback.format_exc()))
 
 
-@pytest.mark.parametrize("world,case", [(2, (10, 5, 5, 60, 50, 3, 1)), (3, (12, 4, 5, 100, 91, 4, 2))])
-def test_partitioned_sigma_and_davidson_match_single_gpu(world, case):
+@pytest.mark.parametrize("world,case,exchange", [(2, (10, 5, 5, 60, 50, 3, 1), "allgather"),
+                                                 (3, (12, 4, 5, 100, 91, 4, 2), "allgather"),
+                                                 (3, (12, 4, 5, 100, 91, 4, 2), "sparse"),
+                                                 (2, (16, 4, 4, 300, 40, 5, 1), "sparse")])
+def test_partitioned_sigma_and_davidson_match_single_gpu(world, case, exchange):
     from paper_2601_16637_b200 import DavidsonOptions, HamiltonianApplier, davidson_solve
     from paper_2601_16637_b200.synth import random_integrals, random_product_basis
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=600) for _ in range(world)]
