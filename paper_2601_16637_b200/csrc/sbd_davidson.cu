@@ -54,14 +54,20 @@ __device__ __forceinline__ void block_partials(const double (&acc)[K], double *_
 // Ordered sum of per-block partials (deterministic).  Output slot i < k reads
 // partial slot i; slot i >= k reads partial slot kfix + (i - k), so kernels
 // can keep a compile-time accumulator layout for a runtime subspace size.
+// One warp per output: lane l sums blocks l, l+32, ... in order, then a fixed
+// shuffle tree -- the same order every call.
+constexpr int kFinishBlocks = 24;  // x 4 warps >= the largest output count (2*64 + 9)
 __global__ void finish_partials(const double *__restrict__ partial, int nblocks, int stride, int k, int kfix,
                                 int cnt, double *__restrict__ out) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= cnt) return;
-    const int src = i < k ? i : kfix + (i - k);
-    double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += partial[(i64)b * stride + src];
-    out[i] = s;
+    const int lane = threadIdx.x & 31;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < cnt; i += (gridDim.x * blockDim.x) >> 5) {
+        const int src = i < k ? i : kfix + (i - k);
+        double s = 0.0;
+        for (int b = lane; b < nblocks; b += 32) s += partial[(i64)b * stride + src];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) out[i] = s;
+    }
 }
 
 // Streaming over element "slots": with V2 a slot is a 16-byte pair of doubles
@@ -1441,7 +1447,7 @@ struct VdotsL {
         if (int rc = ensure_red(ctx, nb, K)) return rc;
         if (vec_ok(V, ldv, w)) vdots_kernel<K, true><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, w, ctx->red.as<double>());
         else vdots_kernel<K, false><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, w, ctx->red.as<double>());
-        finish_partials<<<1, 64, 0, ctx->stream>>>(ctx->red.as<double>(), nb, K, k, K, k, out);
+        finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nb, K, k, K, k, out);
         SBD_LAUNCHED(ctx, "vdots");
         return SBD_OK;
     }
@@ -1456,14 +1462,14 @@ struct Vdots2L {
         if (vec_ok(V, ldv, w, u)) {
             const int nt = tile_blocks(ctx, n, 1024);
             vdots2_tile<K><<<nt, kBlock, 0, ctx->stream>>>(V, k, ldv, n, w, u, ctx->red.as<double>());
-            finish_partials<<<1, 64, 0, ctx->stream>>>(ctx->red.as<double>(), nt, 2 * K, k, K, k, out);
-            finish_partials<<<1, 64, 0, ctx->stream>>>(ctx->red.as<double>() + K, nt, 2 * K, k, K, k, out + k);
+            finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, 2 * K, k, K, k, out);
+            finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>() + K, nt, 2 * K, k, K, k, out + k);
             SBD_LAUNCHED(ctx, "vdots2");
             return SBD_OK;
         }
         vdots2_kernel<K, false><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, w, u, ctx->red.as<double>());
-        finish_partials<<<1, 64, 0, ctx->stream>>>(ctx->red.as<double>(), nb, 2 * K, k, K, k, out);
-        finish_partials<<<1, 64, 0, ctx->stream>>>(ctx->red.as<double>() + K, nb, 2 * K, k, K, k, out + k);
+        finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nb, 2 * K, k, K, k, out);
+        finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>() + K, nb, 2 * K, k, K, k, out + k);
         SBD_LAUNCHED(ctx, "vdots2");
         return SBD_OK;
     }
@@ -1524,7 +1530,7 @@ struct ResidL {
         else if (m == 2) bs = launch<2>(ctx, nb, V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T, ldt);
         else if (m <= 4) bs = launch<4>(ctx, nb, V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T, ldt);
         else bs = launch<8>(ctx, nb, V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T, ldt);
-        finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), bs.first, bs.second, k, K, k + 1 + m, out);
+        finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>(), bs.first, bs.second, k, K, k + 1 + m, out);
         SBD_LAUNCHED(ctx, "residual_precond");
         return SBD_OK;
     }
@@ -1545,7 +1551,7 @@ struct GsL {
             else
                 gs_reg<(K <= 32 ? K : 32), false><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst,
                                                                                    scale, ctx->red.as<double>());
-            finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
+            finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
             SBD_LAUNCHED(ctx, "gs_update");
             return SBD_OK;
         }
@@ -1559,7 +1565,7 @@ struct GsL {
                 attr = true;
             }
             gs_tma<K><<<nt, kBlock, smem, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale, ctx->red.as<double>());
-            finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
+            finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
             SBD_LAUNCHED(ctx, "gs_update");
             return SBD_OK;
         }
@@ -1567,10 +1573,10 @@ struct GsL {
         if (vec_ok(V, ldv, t)) {
             const int nt = tile_blocks(ctx, n, 512);
             gs_tile<K><<<nt, kBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, ctx->red.as<double>());
-            finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
+            finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
         } else {
             gs_kernel<K, false><<<nb, kBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, ctx->red.as<double>());
-            finish_partials<<<1, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nb, K + 1, kdot, K, kdot + 1, out);
+            finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nb, K + 1, kdot, K, kdot + 1, out);
         }
         if (out_vec) scale_copy_kernel<<<nb * 2, kBlock, 0, ctx->stream>>>(t, out_vec, n, scale);
         SBD_LAUNCHED(ctx, "gs_update");

@@ -602,23 +602,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrossThreads, 1) cr
         if (lane == 0 && nitems > 0) {
             const uint32_t bv = (uint32_t)(2 * a.ld * sizeof(double));
             const uint32_t bx = (uint32_t)(a.nb * sizeof(double));
-            const uint32_t peer0 = cluster_map(&peer[0], 0);
+            const uint32_t peer_other = cluster_map(&peer[0], (uint32_t)(rank ^ 1));
+            // each rank multicasts half of the row (rank 0 also the ERI row), so both
+            // CTAs' TMA units work on every item
+            const i64 half = (a.nb / 2 + 1) & ~(i64)1;
+            const i64 x0 = rank == 0 ? 0 : half, xn = rank == 0 ? half : a.nb - half;
             for (i64 item = 0; item < nitems; ++item) {
                 const int s = (int)(item & 1);
                 const uint32_t use = (uint32_t)(item >> 1);
-                if (item >= kMcStages) mbar_wait(&empty[s], (use - 1) & 1);
-                mbar_arrive_expect_tx(&full[s], bx + bv);
-                if (rank == 1) {
-                    mbar_arrive_remote(peer0 + (uint32_t)(s * sizeof(uint64_t)));
-                } else {
-                    mbar_wait_cluster(&peer[s], use & 1);
-                    const SConn sa = a.a_sconn[e0 + item];
-                    if (item + kMcPrefetch < nitems)  // next-but-one rows: L2 hits for the TMA
-                        prefetch_l2(a.X + (i64)a.a_sconn[e0 + item + kMcPrefetch].tgt * a.nb, bx);
-                    double *dst = st0 + s * sdbl;
-                    tma_load_1d_multicast(dst, a.X + (i64)sa.tgt * a.nb, bx, &full[s], 0x3);
-                    tma_load_1d_multicast(dst + a.chunk + 2, vrow(a, sa), bv, &full[s], 0x3);
-                }
+                if (item >= kMcStages) mbar_wait(&empty[s], (use - 1) & 1);  // my consumers released s
+                mbar_arrive_expect_tx(&full[s], bx + bv);                       // armed for the whole item
+                mbar_arrive_remote(peer_other + (uint32_t)(s * sizeof(uint64_t)));  // my side free + armed
+                mbar_wait_cluster(&peer[s], use & 1);                           // the peer's side too
+                const SConn sa = a.a_sconn[e0 + item];
+                const double *row = a.X + (i64)sa.tgt * a.nb;
+                if (item + kMcPrefetch < nitems && xn > 0)  // next-but-one rows: L2 hits for the TMA
+                    prefetch_l2(a.X + (i64)a.a_sconn[e0 + item + kMcPrefetch].tgt * a.nb + x0,
+                                (uint32_t)(xn * sizeof(double)));
+                double *dst = st0 + s * sdbl;
+                if (xn > 0) tma_load_1d_multicast(dst + x0, row + x0, (uint32_t)(xn * sizeof(double)), &full[s], 0x3);
+                if (rank == 0) tma_load_1d_multicast(dst + a.chunk + 2, vrow(a, sa), bv, &full[s], 0x3);
             }
         }
     } else {
