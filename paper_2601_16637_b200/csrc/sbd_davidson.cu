@@ -1136,6 +1136,8 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(const double *__res
 // the k V pairs the same thread just loaded (L2 hits: only the first touch
 // costs HBM).  Per-thread accumulators are reduced once at the end.
 constexpr int kRegBlock = 256;
+// roots handled by the register residual pass (more roots keep the TMA-staged pass)
+constexpr int kRegMaxRoots = 4;
 
 template <int K, int NA>
 __device__ __forceinline__ void block_store_partials(double (&acc)[NA], double *__restrict__ partial, int stride) {
@@ -1482,7 +1484,7 @@ struct ResidL {
     static std::pair<int, int> launch(sbd_ctx *ctx, int nb, const double *V, const double *W, int k, i64 ldv, i64 n,
                                       const double *Y, const double *theta, int m, int jp, const double *diag,
                                       double delta, double *T, i64 ldt) {
-        if (K <= 32 && M <= 2 && vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_reg()) {
+        if (K <= 32 && M <= kRegMaxRoots && vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_reg()) {
             const int nt = ctx->num_sms * 2;
             residual_reg<(K <= 32 ? K : 32), M><<<nt, kRegBlock, 0, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp,
                                                                                  diag, delta, T, ldt, ctx->red.as<double>());

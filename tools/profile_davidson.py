@@ -10,7 +10,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def main(iters: int = 40):
+def main(iters: int = 40, roots: int = 1):
     import torch
 
     import bench
@@ -18,7 +18,7 @@ def main(iters: int = 40):
 
     table, a, b = bench._instance()
     app = HamiltonianApplier(SelectedBasis.product(a.tolist(), b.tolist(), 26, 7, 7), table)
-    opts = DavidsonOptions(max_iters=iters, profile=True)
+    opts = DavidsonOptions(max_iters=iters, profile=True, n_roots=roots, restart_keep=max(4, roots))
     t0 = time.perf_counter()
     res = davidson_solve(app, app.diag_device, opts=opts, return_device=True)
     torch.cuda.synchronize()
@@ -31,4 +31,4 @@ def main(iters: int = 40):
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 40)
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 40, int(sys.argv[2]) if len(sys.argv) > 2 else 1)
