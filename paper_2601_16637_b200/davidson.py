@@ -92,6 +92,7 @@ class DavidsonStats:
     iter_seconds: list = field(default_factory=list)  # B200 extension: wall time per iteration
     phase_ms: dict = field(default_factory=dict)  # B200 extension: summed device time per phase
     host_ms: dict = field(default_factory=dict)  # B200 extension: host time per section (enqueue / wait)
+    timeline: list = field(default_factory=list)  # B200 extension (profile): one iteration on the device clock
 
 
 @dataclass
@@ -151,6 +152,14 @@ class _Engine:
         for name, s, e in self._events:
             out[name] = out.get(name, 0.0) + s.elapsed_time(e)
         return out
+
+    def timeline(self, first: int, count: int) -> list:
+        """(name, start, duration) in ms, relative to event `first` (profile mode; gaps = idle device)."""
+        ev = self._events[first:first + count]
+        if not ev:
+            return []
+        t0 = ev[0][1]
+        return [(n, t0.elapsed_time(s), s.elapsed_time(e)) for n, s, e in ev]
 
 
 def _p(t):
@@ -359,7 +368,8 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
         _tick[0] = t
 
     def readback(t_dev, cnt):
-        host[:cnt].copy_(t_dev[:cnt], non_blocking=True)
+        with eng.phase("readback"):
+            host[:cnt].copy_(t_dev[:cnt], non_blocking=True)
         hp("enqueue")
         stream.synchronize()
         hp("sync_wait")
@@ -378,18 +388,20 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
         # T[:, k-1] = V^T w and the Gram row of v_{k-1}: one pass over V
         eng("sbd_vdots2", _p(V), k, ld, n_loc, _p(W[k - 1]), _p(V[k - 1]), _p(small))
         reduce(small[: 2 * k])
-        T[:k, k - 1] = small[:k]
-        T[k - 1, :k] = small[:k]
-        G[:k, k - 1] = small[k:2 * k]
-        G[k - 1, :k] = small[k:2 * k]
+        with eng.phase("torch:T"):
+            T[:k, k - 1] = small[:k]
+            T[k - 1, :k] = small[:k]
+            G[:k, k - 1] = small[k:2 * k]
+            G[k - 1, :k] = small[k:2 * k]
 
         # Rayleigh-Ritz on the device, in place on T (davidson.py:251)
         eng("sbd_jacobi", _p(T), k, k_max, _p(jac_w), _p(jac_v), 64, _p(jac_info))
         # numpy slicing in the reference keeps min(m, k) roots while k < m
         mk = min(m, k)
         evecs = jac_v[: k * k].view(k, k)
-        Y_dev[: k * mk].copy_(evecs[:, :mk].reshape(-1))
-        th_dev[:mk].copy_(jac_w[:mk])
+        with eng.phase("torch:ritz"):
+            Y_dev[: k * mk].copy_(evecs[:, :mk].reshape(-1))
+            th_dev[:mk].copy_(jac_w[:mk])
         ritz_rotated = False
 
         # residuals, preconditioned corrections and V^T t in one pass
@@ -400,12 +412,13 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
         c_dev[:k].copy_(small[:k])
 
         # one packed read-back: theta | residual^2 | |t|^2 | sweeps | ortho
-        pack[:mk].copy_(jac_w[:mk])
-        pack[mk:2 * mk].copy_(small[k + 1:k + 1 + mk])
-        pack[2 * mk] = small[k]
-        pack[2 * mk + 1] = jac_info[0].to(torch.float64)
-        if opts.track_orthogonality:
-            pack[2 * mk + 2] = torch.linalg.norm(G[:k, :k] - eye[:k, :k])
+        with eng.phase("torch:pack"):
+            pack[:mk].copy_(jac_w[:mk])
+            pack[mk:2 * mk].copy_(small[k + 1:k + 1 + mk])
+            pack[2 * mk] = small[k]
+            pack[2 * mk + 1] = jac_info[0].to(torch.float64)
+            if opts.track_orthogonality:
+                pack[2 * mk + 2] = torch.linalg.norm(G[:k, :k] - eye[:k, :k])
         # speculative CGS pass 1 on the projected root (the usual next step: not
         # converged, same target root, no restart), read back with the pack, so an
         # iteration costs one host round trip instead of two
@@ -508,6 +521,10 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
     stats.host_ms = host_ms
     if opts.profile:
         stats.phase_ms = eng.summary()
+        sig = [i for i, ev in enumerate(eng._events) if ev[0] == "sigma"]
+        if len(sig) >= 3:
+            a, b = sig[len(sig) // 2], sig[len(sig) // 2 + 1]
+            stats.timeline = eng.timeline(a, b - a + 1)
         stats.phase_ms.update({"host:" + k_: v for k_, v in host_ms.items()})
     vectors = U if return_device else U.cpu().numpy()
     if eng.own_ctx:

@@ -27,6 +27,8 @@ def main(iters: int = 40, roots: int = 1):
     ph = {k: v / it for k, v in sorted(res.stats.phase_ms.items(), key=lambda kv: -kv[1])}
     out = {"iterations": it, "wall_ms_per_iter": wall * 1e3 / it, "device_ms_per_iter_by_phase": ph,
            "device_ms_per_iter_total": sum(ph.values())}
+    # one steady-state iteration on the device clock: (phase, start ms, duration ms); gaps are idle time
+    out["timeline_one_iteration"] = [(n, round(t0, 4), round(d, 4)) for n, t0, d in res.stats.timeline]
     print(json.dumps(out, indent=1))
 
 
