@@ -1139,33 +1139,53 @@ constexpr int kRegBlock = 256;
 // roots handled by the register residual pass (more roots keep the TMA-staged pass)
 constexpr int kRegMaxRoots = 4;
 
-template <int K, int NA>
-__device__ __forceinline__ void block_store_partials(double (&acc)[NA], double *__restrict__ partial, int stride) {
-    __shared__ double red[kRegBlock / 32][NA];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Per-block partials: vector slots [0, KV) (thread-owned subsets, see below)
+// followed by NX scalar accumulators.  With S threads per element pair, thread
+// h = lane % S owns vectors i = h + S j (j < K/S); a lane-strided shuffle tree
+// reduces each subset among its own lanes only.
+template <int K, int S, int NX>
+__device__ __forceinline__ void block_store_partials(const double (&acc)[K / S], const double (&xs)[NX],
+                                                     double *__restrict__ partial, int stride) {
+    __shared__ double red[kRegBlock / 32][K + NX];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, h = lane % S;
 #pragma unroll
-    for (int i = 0; i < NA; ++i) {
-        const double v = warp_sum(acc[i]);
-        if (lane == 0) red[warp][i] = v;
+    for (int j = 0; j < K / S; ++j) {
+        double v = acc[j];
+#pragma unroll
+        for (int o = 16; o >= S; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane < S) red[warp][h + S * j] = v;
+    }
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+        const double v = warp_sum(xs[j]);
+        if (lane == 0) red[warp][K + j] = v;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < NA; i += blockDim.x) {
+    for (int i = threadIdx.x; i < K + NX; i += blockDim.x) {
         double sum = 0.0;
         for (int w = 0; w < kRegBlock / 32; ++w) sum += red[w][i];
         partial[(i64)blockIdx.x * stride + i] = sum;
     }
 }
 
-// Lane 0 of each warp bulk-prefetches, into L2, the 32 element pairs (512 B)
-// the warp touches kPfDist grid-stride iterations ahead in vector v.  With
-// kPfDist = 0 the whole iteration's slices of all k vectors are requested at
-// once, so the thread's register-staged loads (8 vectors at a time) find them
-// in L2 instead of paying one HBM latency per group of 8.
-constexpr int kPfDist = 0;
-__device__ __forceinline__ void warp_prefetch(const double *v, i64 p_warp_next, i64 np) {
-    if (p_warp_next < np) {
-        const i64 cnt = min((i64)32, np - p_warp_next);
-        prefetch_l2(v + 2 * p_warp_next, (uint32_t)(cnt * 16));
+template <int S>
+__device__ __forceinline__ double2 pair_sum(double2 v) {  // sum over the S lanes sharing an element pair
+    if (S == 2) {  // only the two lanes of the pair take part: other pairs may have left the loop
+        const unsigned pm = 3u << ((threadIdx.x & 31) & ~1u);
+        v.x += __shfl_xor_sync(pm, v.x, 1);
+        v.y += __shfl_xor_sync(pm, v.y, 1);
+    }
+    return v;
+}
+
+// Lane 0 of each warp bulk-prefetches, into L2, the element pairs the warp
+// touches in vector v this iteration, so the thread's register-staged loads
+// (8 vectors at a time) find them in L2 instead of paying one HBM latency per
+// group of 8.
+__device__ __forceinline__ void warp_prefetch(const double *v, i64 p_warp, i64 np, int npairs) {
+    if (p_warp < np) {
+        const i64 cnt = min((i64)npairs, np - p_warp);
+        prefetch_l2(v + 2 * p_warp, (uint32_t)(cnt * 16));
     }
 }
 
@@ -1176,12 +1196,14 @@ __device__ __forceinline__ double precond_div(double r, double d, double th, dou
 
 // Residuals, preconditioned corrections and V^T t_jp (davidson.py:252-258,159-163).
 // partial per block (stride K+1+M): [0,K) dots | K: |t_jp|^2 | K+1+j: |r_j|^2
-template <int K, int M>
+// S threads per element pair (S = 2 halves the per-thread accumulators at K = 32).
+template <int K, int M, int S>
 __global__ void __launch_bounds__(kRegBlock, 2)
 residual_reg(const double *__restrict__ V, const double *__restrict__ W, int k, i64 ldv, i64 n,
              const double *__restrict__ Y, const double *__restrict__ theta, int m, int jp,
              const double *__restrict__ diag, double delta, double *__restrict__ T, i64 ldt,
              double *__restrict__ partial) {
+    constexpr int KS = K / S;
     __shared__ double ys[K * M];
     __shared__ double th[M];
     for (int idx = threadIdx.x; idx < K * M; idx += blockDim.x) {
@@ -1190,36 +1212,46 @@ residual_reg(const double *__restrict__ V, const double *__restrict__ W, int k, 
     }
     if (threadIdx.x < M) th[threadIdx.x] = threadIdx.x < m ? theta[threadIdx.x] : 0.0;
     __syncthreads();
-    constexpr int NA = K + 1 + M;
-    double acc[NA];
+    const int h = (threadIdx.x & 31) % S;
+    double acc[KS], xs[1 + M];
 #pragma unroll
-    for (int i = 0; i < NA; ++i) acc[i] = 0.0;
-    const i64 np = n / 2;
-    const i64 stride = (i64)gridDim.x * blockDim.x;
-    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += stride) {
+    for (int i = 0; i < KS; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j <= M; ++j) xs[j] = 0.0;
+    const i64 np = n / 2, stride = (i64)gridDim.x * blockDim.x / S;
+    for (i64 p = ((i64)blockIdx.x * blockDim.x + threadIdx.x) / S; p < np; p += stride) {
         if ((threadIdx.x & 31) == 0) {
-            const i64 pn = p + kPfDist * stride;
             for (int i = 0; i < k; ++i) {
-                warp_prefetch(V + i * ldv, pn, np);
-                warp_prefetch(W + i * ldv, pn, np);
+                warp_prefetch(V + i * ldv, p, np, 32 / S);
+                warp_prefetch(W + i * ldv, p, np, 32 / S);
             }
-            warp_prefetch(diag, pn, np);
+            warp_prefetch(diag, p, np, 32 / S);
         }
         double2 u[M], wy[M];
 #pragma unroll
         for (int j = 0; j < M; ++j) u[j] = wy[j] = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-            if (i < k) {
-                const double2 v = reinterpret_cast<const double2 *>(V + i * ldv)[p];
-                const double2 w = __ldcs(reinterpret_cast<const double2 *>(W + i * ldv) + p);
+        for (int q0 = 0; q0 < KS; q0 += 4) {  // 4 vectors x (V, W): 8 independent loads, then the FMAs
+            double2 v[4], w[4];
 #pragma unroll
-                for (int j = 0; j < M; ++j) {
-                    const double y = ys[i * M + j];
-                    u[j].x = fma(y, v.x, u[j].x);
-                    u[j].y = fma(y, v.y, u[j].y);
-                    wy[j].x = fma(y, w.x, wy[j].x);
-                    wy[j].y = fma(y, w.y, wy[j].y);
+            for (int e = 0; e < 4; ++e) {
+                const int i = h + S * (q0 + e);
+                const bool on = q0 + e < KS && i < k;
+                v[e] = on ? reinterpret_cast<const double2 *>(V + i * ldv)[p] : make_double2(0.0, 0.0);
+                w[e] = on ? __ldcs(reinterpret_cast<const double2 *>(W + i * ldv) + p) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = h + S * (q0 + e);
+                if (q0 + e < KS && i < k) {
+#pragma unroll
+                    for (int j = 0; j < M; ++j) {
+                        const double y = ys[i * M + j];
+                        u[j].x = fma(y, v[e].x, u[j].x);
+                        u[j].y = fma(y, v[e].y, u[j].y);
+                        wy[j].x = fma(y, w[e].x, wy[j].x);
+                        wy[j].y = fma(y, w[e].y, wy[j].y);
+                    }
                 }
             }
         }
@@ -1228,23 +1260,28 @@ residual_reg(const double *__restrict__ V, const double *__restrict__ W, int k, 
 #pragma unroll
         for (int j = 0; j < M; ++j) {
             if (j < m) {
+                u[j] = pair_sum<S>(u[j]);
+                wy[j] = pair_sum<S>(wy[j]);
                 const double rx = wy[j].x - th[j] * u[j].x, ry = wy[j].y - th[j] * u[j].y;
                 const double2 t = make_double2(precond_div(rx, d.x, th[j], delta), precond_div(ry, d.y, th[j], delta));
-                __stcs(reinterpret_cast<double2 *>(T + j * ldt) + p, t);
-                acc[K + 1 + j] = fma(rx, rx, fma(ry, ry, acc[K + 1 + j]));
+                if (h == 0) {
+                    __stcs(reinterpret_cast<double2 *>(T + j * ldt) + p, t);
+                    xs[1 + j] = fma(rx, rx, fma(ry, ry, xs[1 + j]));
+                }
                 if (j == jp) tj = t;
             }
         }
-        acc[K] = fma(tj.x, tj.x, fma(tj.y, tj.y, acc[K]));
+        if (h == 0) xs[0] = fma(tj.x, tj.x, fma(tj.y, tj.y, xs[0]));
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
+        for (int q = 0; q < KS; ++q) {
+            const int i = h + S * q;
             if (i < k) {
                 const double2 v = __ldcs(reinterpret_cast<const double2 *>(V + i * ldv) + p);
-                acc[i] = fma(v.x, tj.x, fma(v.y, tj.y, acc[i]));
+                acc[q] = fma(v.x, tj.x, fma(v.y, tj.y, acc[q]));
             }
         }
     }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail element
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x < S) {  // odd tail element: the S lanes of pair 0
         const i64 e = n - 1;
         double u[M], wy[M];
 #pragma unroll
@@ -1261,98 +1298,113 @@ residual_reg(const double *__restrict__ V, const double *__restrict__ W, int k, 
             if (j < m) {
                 const double r = wy[j] - th[j] * u[j];
                 const double t = precond_div(r, diag[e], th[j], delta);
-                T[j * ldt + e] = t;
-                acc[K + 1 + j] = fma(r, r, acc[K + 1 + j]);
+                if (h == 0) {
+                    T[j * ldt + e] = t;
+                    xs[1 + j] = fma(r, r, xs[1 + j]);
+                }
                 if (j == jp) tj = t;
             }
-        acc[K] = fma(tj, tj, acc[K]);
+        if (h == 0) xs[0] = fma(tj, tj, xs[0]);
 #pragma unroll
-        for (int i = 0; i < K; ++i)
-            if (i < k) acc[i] = fma(V[i * ldv + e], tj, acc[i]);
+        for (int q = 0; q < KS; ++q)
+            if (h + S * q < k) acc[q] = fma(V[(h + S * q) * ldv + e], tj, acc[q]);
     }
-    block_store_partials<K, NA>(acc, partial, NA);
+    block_store_partials<K, S, 1 + M>(acc, xs, partial, K + 1 + M);
 }
 
 // t_new = t - V c ; out = scale * t_new (out may alias t) ; dots V_i . t_new (i < kdot) ; |t_new|^2
-// partial per block (stride K+1): [0,K) dots | K: |t_new|^2
-template <int K, bool DOTS>
+// partial per block (stride K+1): [0,K) dots | K: |t_new|^2 ; S threads per element pair.
+template <int K, bool DOTS, int S>
 __global__ void __launch_bounds__(kRegBlock, 2)
 gs_reg(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__restrict__ c, int kdot, const double *t,
        double *out, const double *__restrict__ scale, double *__restrict__ partial) {
+    constexpr int KS = K / S;
     __shared__ double cs[K];
     for (int i = threadIdx.x; i < K; i += blockDim.x) cs[i] = i < k ? c[i] : 0.0;
     __syncthreads();
     const double sc = scale ? *scale : 1.0;
-    constexpr int NA = K + 1;
-    double acc[NA];
+    const int h = (threadIdx.x & 31) % S;
+    double acc[KS], xs[1] = {0.0};
 #pragma unroll
-    for (int i = 0; i < NA; ++i) acc[i] = 0.0;
-    const i64 np = n / 2;
-    const i64 stride = (i64)gridDim.x * blockDim.x;
-    for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += stride) {
+    for (int i = 0; i < KS; ++i) acc[i] = 0.0;
+    const i64 np = n / 2, stride = (i64)gridDim.x * blockDim.x / S;
+    for (i64 p = ((i64)blockIdx.x * blockDim.x + threadIdx.x) / S; p < np; p += stride) {
         if ((threadIdx.x & 31) == 0) {
-            const i64 pn = p + kPfDist * stride;
-            for (int i = 0; i < k; ++i) warp_prefetch(V + i * ldv, pn, np);
-            warp_prefetch(t, pn, np);
+            for (int i = 0; i < k; ++i) warp_prefetch(V + i * ldv, p, np, 32 / S);
+            warp_prefetch(t, p, np, 32 / S);
         }
-        double2 tv = reinterpret_cast<const double2 *>(t)[p];
+        double2 sv = make_double2(0.0, 0.0);
 #pragma unroll
-        for (int i0 = 0; i0 < K; i0 += 8) {  // 8 independent loads ahead of each FMA chain
+        for (int q0 = 0; q0 < KS; q0 += 8) {  // 8 independent loads ahead of each FMA chain
             double2 v[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (i0 + u < k)
-                    v[u] = DOTS ? reinterpret_cast<const double2 *>(V + (i0 + u) * ldv)[p]
-                                : __ldcs(reinterpret_cast<const double2 *>(V + (i0 + u) * ldv) + p);
+            for (int u = 0; u < 8; ++u) {
+                const int i = h + S * (q0 + u);
+                if (q0 + u < KS && i < k)
+                    v[u] = DOTS ? reinterpret_cast<const double2 *>(V + i * ldv)[p]
+                                : __ldcs(reinterpret_cast<const double2 *>(V + i * ldv) + p);
+            }
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (i0 + u < k) {
-                    tv.x = fma(-cs[i0 + u], v[u].x, tv.x);
-                    tv.y = fma(-cs[i0 + u], v[u].y, tv.y);
+            for (int u = 0; u < 8; ++u) {
+                const int i = h + S * (q0 + u);
+                if (q0 + u < KS && i < k) {
+                    sv.x = fma(cs[i], v[u].x, sv.x);
+                    sv.y = fma(cs[i], v[u].y, sv.y);
                 }
+            }
         }
-        reinterpret_cast<double2 *>(out)[p] = make_double2(tv.x * sc, tv.y * sc);
-        acc[K] = fma(tv.x, tv.x, fma(tv.y, tv.y, acc[K]));
+        sv = pair_sum<S>(sv);
+        const double2 t0 = reinterpret_cast<const double2 *>(t)[p];
+        const double2 tv = make_double2(t0.x - sv.x, t0.y - sv.y);
+        if (h == 0) {
+            reinterpret_cast<double2 *>(out)[p] = make_double2(tv.x * sc, tv.y * sc);
+            xs[0] = fma(tv.x, tv.x, fma(tv.y, tv.y, xs[0]));
+        }
         if (DOTS) {
 #pragma unroll
-            for (int i = 0; i < K; ++i) {
+            for (int q = 0; q < KS; ++q) {
+                const int i = h + S * q;
                 if (i < kdot) {
                     const double2 v = __ldcs(reinterpret_cast<const double2 *>(V + i * ldv) + p);  // L2 hit
-                    acc[i] = fma(v.x, tv.x, fma(v.y, tv.y, acc[i]));
+                    acc[q] = fma(v.x, tv.x, fma(v.y, tv.y, acc[q]));
                 }
             }
         }
     }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x < S) {
         const i64 e = n - 1;
-        double x = t[e];
-        for (int i = 0; i < k; ++i) x = fma(-cs[i], V[i * ldv + e], x);
-        out[e] = x * sc;
-        acc[K] = fma(x, x, acc[K]);
+        double sx = 0.0;
+        for (int i = 0; i < k; ++i) sx = fma(cs[i], V[i * ldv + e], sx);
+        const double x = t[e] - sx;
+        if (h == 0) {
+            out[e] = x * sc;
+            xs[0] = fma(x, x, xs[0]);
+        }
 #pragma unroll
-        for (int i = 0; i < K; ++i)
-            if (i < kdot) acc[i] = fma(V[i * ldv + e], x, acc[i]);
+        for (int q = 0; q < KS; ++q)
+            if (h + S * q < kdot) acc[q] = fma(V[(h + S * q) * ldv + e], x, acc[q]);
     }
-    block_store_partials<K, NA>(acc, partial, NA);
+    block_store_partials<K, S, 1>(acc, xs, partial, K + 1);
 }
 
-// Thick restart in place: V[j] <- sum_i Y[i, j] V[i] for j < keep <= 8
-// (davidson.py:280-289).  Thread per element pair; the whole pair column of
-// V is read (L2-prefetched in bulk, then 8 vectors at a time) before any of
-// the keep outputs is written, so the in-place update is safe.
+// out[j] <- sum_i Y[i, j] V[i] for j < nout <= 8: the thick restart in place
+// (out = V, davidson.py:280-289) and the final Ritz vectors (out = U,
+// davidson.py:256).  Thread per element pair; the whole pair column of V is
+// read (L2-prefetched in bulk, then 8 vectors at a time) before any output is
+// written, so the in-place form is safe.
 template <int K>
 __global__ void __launch_bounds__(kRegBlock, 2)
-rotate_reg(double *__restrict__ V, int k, i64 ldv, i64 n, const double *__restrict__ Y, int keep) {
+mix_reg(const double *V, int k, i64 ldv, i64 n, const double *__restrict__ Y, int nout, double *out, i64 ldo) {
     __shared__ double ys[K * 8];
     for (int idx = threadIdx.x; idx < K * 8; idx += blockDim.x) {
         const int i = idx / 8, j = idx % 8;
-        ys[idx] = (i < k && j < keep) ? Y[i * keep + j] : 0.0;
+        ys[idx] = (i < k && j < nout) ? Y[i * nout + j] : 0.0;
     }
     __syncthreads();
     const i64 np = n / 2, stride = (i64)gridDim.x * blockDim.x;
     for (i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x; p < np; p += stride) {
         if ((threadIdx.x & 31) == 0)
-            for (int i = 0; i < k; ++i) warp_prefetch(V + i * ldv, p, np);
+            for (int i = 0; i < k; ++i) warp_prefetch(V + i * ldv, p, np, 32);
         double2 u[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) u[j] = make_double2(0.0, 0.0);
@@ -1374,7 +1426,7 @@ rotate_reg(double *__restrict__ V, int k, i64 ldv, i64 n, const double *__restri
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-            if (j < keep) reinterpret_cast<double2 *>(V + j * ldv)[p] = u[j];
+            if (j < nout) reinterpret_cast<double2 *>(out + j * ldo)[p] = u[j];
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const i64 e = n - 1;
@@ -1384,7 +1436,9 @@ rotate_reg(double *__restrict__ V, int k, i64 ldv, i64 n, const double *__restri
 #pragma unroll
             for (int j = 0; j < 8; ++j) u[j] = fma(ys[i * 8 + j], v, u[j]);
         }
-        for (int j = 0; j < keep; ++j) V[j * ldv + e] = u[j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (j < nout) out[j * ldo + e] = u[j];
     }
 }
 
@@ -1413,6 +1467,17 @@ inline bool use_reg() {  // SBD_DAV_TMA=1 selects the TMA-staged passes (A/B mea
     return v == 1;
 }
 
+// lane-pair vector split at K = 32 for pass `which` (0 residual, 1 CGS); SBD_PAIR_SPLIT is a
+// two-bit mask override for A/B measurements
+inline bool pair_split(int which) {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("SBD_PAIR_SPLIT");
+        v = e && *e ? atoi(e) : 1;
+    }
+    return (v >> which) & 1;
+}
+
 int tile_blocks(sbd_ctx *ctx, i64 n, int tt) {
     i64 b = (n + tt - 1) / tt;
     return (int)std::max<i64>(1, std::min<i64>(b, (i64)ctx->num_sms * 8));
@@ -1438,6 +1503,7 @@ template <template <int> class Launch, class... Args>
 int dispatch_k(int k, Args... args) {
     if (k <= 8) return Launch<8>::run(args...);
     if (k <= 16) return Launch<16>::run(args...);
+    if (k <= 24) return Launch<24>::run(args...);
     if (k <= 32) return Launch<32>::run(args...);
     return Launch<64>::run(args...);
 }
@@ -1486,8 +1552,13 @@ struct ResidL {
                                       double delta, double *T, i64 ldt) {
         if (K <= 32 && M <= kRegMaxRoots && vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_reg()) {
             const int nt = ctx->num_sms * 2;
-            residual_reg<(K <= 32 ? K : 32), M><<<nt, kRegBlock, 0, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp,
-                                                                                 diag, delta, T, ldt, ctx->red.as<double>());
+            constexpr int KR = K <= 32 ? K : 32;
+            if (KR >= 24 && pair_split(0))  // two lanes per element pair: half the accumulators per thread
+                residual_reg<KR, M, 2><<<nt, kRegBlock, 0, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag,
+                                                                         delta, T, ldt, ctx->red.as<double>());
+            else
+                residual_reg<KR, M, 1><<<nt, kRegBlock, 0, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag,
+                                                                         delta, T, ldt, ctx->red.as<double>());
             return {nt, K + 1 + M};
         }
         const int TTA = tma_tile(2 * k + 1);
@@ -1547,12 +1618,20 @@ struct GsL {
         double *dst = out_vec ? out_vec : t;
         if (K <= 32 && vec_ok(V, ldv, t) && al16(dst) && use_reg()) {
             const int nt = ctx->num_sms * 2;
-            if (kdot > 0)
-                gs_reg<(K <= 32 ? K : 32), true><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale,
-                                                                                  ctx->red.as<double>());
+            constexpr int KR = K <= 32 ? K : 32;
+            const bool split = KR == 32 && pair_split(1);
+            if (kdot > 0 && split)
+                gs_reg<KR, true, 2><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale,
+                                                                      ctx->red.as<double>());
+            else if (kdot > 0)
+                gs_reg<KR, true, 1><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale,
+                                                                      ctx->red.as<double>());
+            else if (split)
+                gs_reg<KR, false, 2><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale,
+                                                                       ctx->red.as<double>());
             else
-                gs_reg<(K <= 32 ? K : 32), false><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst,
-                                                                                   scale, ctx->red.as<double>());
+                gs_reg<KR, false, 1><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale,
+                                                                       ctx->red.as<double>());
             finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
             SBD_LAUNCHED(ctx, "gs_update");
             return SBD_OK;
@@ -1590,7 +1669,7 @@ template <int K>
 struct RotL {
     static int run(sbd_ctx *ctx, double *V, int k, i64 ldv, i64 n, const double *Y, int keep) {
         if (K <= 32 && keep <= 8 && vec_ok(V, ldv) && use_reg()) {
-            rotate_reg<(K <= 32 ? K : 32)><<<ctx->num_sms * 2, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, Y, keep);
+            mix_reg<(K <= 32 ? K : 32)><<<ctx->num_sms * 2, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, Y, keep, V, ldv);
             SBD_LAUNCHED(ctx, "rotate");
             return SBD_OK;
         }
@@ -1603,6 +1682,11 @@ struct RotL {
 template <int K>
 struct CombL {
     static int run(sbd_ctx *ctx, const double *V, int k, i64 ldv, i64 n, const double *Y, int m, double *U, i64 ldu) {
+        if (K <= 32 && m <= 8 && vec_ok(V, ldv) && al16(U) && ldu % 2 == 0 && use_reg()) {
+            mix_reg<(K <= 32 ? K : 32)><<<ctx->num_sms * 2, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, Y, m, U, ldu);
+            SBD_LAUNCHED(ctx, "combine");
+            return SBD_OK;
+        }
         combine_kernel<K><<<red_blocks(ctx, n) * 2, kBlock, 0, ctx->stream>>>(V, k, ldv, n, Y, m, U, ldu);
         SBD_LAUNCHED(ctx, "combine");
         return SBD_OK;

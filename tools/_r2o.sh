@@ -1,0 +1,5 @@
+mkdir -p gpurun_out/r2o
+timeout 300 python tools/profile_davidson.py 40 > gpurun_out/r2o/dav.json 2>&1
+timeout 300 python tools/profile_davidson.py 40 3 > gpurun_out/r2o/dav3.json 2>&1
+timeout 1200 python -m pytest tests/test_gpu_davidson.py tests/test_gpu_distributed.py tests/test_gpu_explicit.py -m gpu -x -q --timeout 300 > gpurun_out/r2o/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/r2o/pytest_gpu.log
+timeout 600 python bench.py --no-cpu --no-explicit --no-e2e > gpurun_out/r2o/bench.json 2> gpurun_out/r2o/bench.err
