@@ -1170,10 +1170,13 @@ __device__ __forceinline__ void block_store_partials(const double (&acc)[K / S],
 
 template <int S>
 __device__ __forceinline__ double2 pair_sum(double2 v) {  // sum over the S lanes sharing an element pair
-    if (S == 2) {  // only the two lanes of the pair take part: other pairs may have left the loop
-        const unsigned pm = 3u << ((threadIdx.x & 31) & ~1u);
-        v.x += __shfl_xor_sync(pm, v.x, 1);
-        v.y += __shfl_xor_sync(pm, v.y, 1);
+    if (S > 1) {  // only the S lanes of the group take part: other groups may have left the loop
+        const unsigned gm = ((1u << S) - 1u) << ((threadIdx.x & 31) & ~(unsigned)(S - 1));
+#pragma unroll
+        for (int o = 1; o < S; o <<= 1) {
+            v.x += __shfl_xor_sync(gm, v.x, o);
+            v.y += __shfl_xor_sync(gm, v.y, o);
+        }
     }
     return v;
 }
@@ -1202,7 +1205,7 @@ __global__ void __launch_bounds__(kRegBlock, 2)
 residual_reg(const double *__restrict__ V, const double *__restrict__ W, int k, i64 ldv, i64 n,
              const double *__restrict__ Y, const double *__restrict__ theta, int m, int jp,
              const double *__restrict__ diag, double delta, double *__restrict__ T, i64 ldt,
-             double *__restrict__ partial) {
+             double *__restrict__ partial, int pf) {
     constexpr int KS = K / S;
     __shared__ double ys[K * M];
     __shared__ double th[M];
@@ -1220,7 +1223,7 @@ residual_reg(const double *__restrict__ V, const double *__restrict__ W, int k, 
     for (int j = 0; j <= M; ++j) xs[j] = 0.0;
     const i64 np = n / 2, stride = (i64)gridDim.x * blockDim.x / S;
     for (i64 p = ((i64)blockIdx.x * blockDim.x + threadIdx.x) / S; p < np; p += stride) {
-        if ((threadIdx.x & 31) == 0) {
+        if (pf && (threadIdx.x & 31) == 0) {
             for (int i = 0; i < k; ++i) {
                 warp_prefetch(V + i * ldv, p, np, 32 / S);
                 warp_prefetch(W + i * ldv, p, np, 32 / S);
@@ -1467,15 +1470,12 @@ inline bool use_reg() {  // SBD_DAV_TMA=1 selects the TMA-staged passes (A/B mea
     return v == 1;
 }
 
-// lane-pair vector split at K = 32 for pass `which` (0 residual, 1 CGS); SBD_PAIR_SPLIT is a
-// two-bit mask override for A/B measurements
-inline bool pair_split(int which) {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SBD_PAIR_SPLIT");
-        v = e && *e ? atoi(e) : 1;
-    }
-    return (v >> which) & 1;
+// lanes per element pair for pass `which` (0 residual, 1 CGS); SBD_RES_SPLIT / SBD_GS_SPLIT
+// override the default for A/B measurements
+inline int split_lanes(int which, int dflt) {
+    const char *e = getenv(which == 0 ? "SBD_RES_SPLIT" : "SBD_GS_SPLIT");
+    const int v = e && *e ? atoi(e) : dflt;
+    return (v == 1 || v == 2 || v == 4) ? v : dflt;
 }
 
 int tile_blocks(sbd_ctx *ctx, i64 n, int tt) {
@@ -1553,12 +1553,22 @@ struct ResidL {
         if (K <= 32 && M <= kRegMaxRoots && vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_reg()) {
             const int nt = ctx->num_sms * 2;
             constexpr int KR = K <= 32 ? K : 32;
-            if (KR >= 24 && pair_split(0))  // two lanes per element pair: half the accumulators per thread
+            // S lanes per element pair split the k vectors: fewer accumulators per thread, so the
+            // compiler keeps the loads of a thread in flight together (k > 16)
+            const int sp = split_lanes(0, KR >= 24 ? 2 : 1);
+            // L2 bulk prefetch of the residual's 2k+1 slices: measured slower once the loads are
+            // batched (the bulk-prefetch issue rate becomes the limit); SBD_RES_PF=1 re-enables it
+            const char *pfe = getenv("SBD_RES_PF");
+            const int pf = pfe && *pfe == '1' ? 1 : 0;
+            if (sp == 4)
+                residual_reg<KR, M, 4><<<nt, kRegBlock, 0, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag,
+                                                                         delta, T, ldt, ctx->red.as<double>(), pf);
+            else if (sp == 2)
                 residual_reg<KR, M, 2><<<nt, kRegBlock, 0, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag,
-                                                                         delta, T, ldt, ctx->red.as<double>());
+                                                                         delta, T, ldt, ctx->red.as<double>(), pf);
             else
                 residual_reg<KR, M, 1><<<nt, kRegBlock, 0, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag,
-                                                                         delta, T, ldt, ctx->red.as<double>());
+                                                                         delta, T, ldt, ctx->red.as<double>(), pf);
             return {nt, K + 1 + M};
         }
         const int TTA = tma_tile(2 * k + 1);
@@ -1619,7 +1629,7 @@ struct GsL {
         if (K <= 32 && vec_ok(V, ldv, t) && al16(dst) && use_reg()) {
             const int nt = ctx->num_sms * 2;
             constexpr int KR = K <= 32 ? K : 32;
-            const bool split = KR == 32 && pair_split(1);
+            const bool split = KR == 32 && split_lanes(1, 1) == 2;
             if (kdot > 0 && split)
                 gs_reg<KR, true, 2><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale,
                                                                       ctx->red.as<double>());
