@@ -1320,7 +1320,7 @@ residual_reg(const double *__restrict__ V, const double *__restrict__ W, int k, 
 template <int K, bool DOTS, int S>
 __global__ void __launch_bounds__(kRegBlock, 2)
 gs_reg(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__restrict__ c, int kdot, const double *t,
-       double *out, const double *__restrict__ scale, double *__restrict__ partial) {
+       double *out, const double *__restrict__ scale, double *__restrict__ partial, int pf) {
     constexpr int KS = K / S;
     __shared__ double cs[K];
     for (int i = threadIdx.x; i < K; i += blockDim.x) cs[i] = i < k ? c[i] : 0.0;
@@ -1332,7 +1332,7 @@ gs_reg(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__rest
     for (int i = 0; i < KS; ++i) acc[i] = 0.0;
     const i64 np = n / 2, stride = (i64)gridDim.x * blockDim.x / S;
     for (i64 p = ((i64)blockIdx.x * blockDim.x + threadIdx.x) / S; p < np; p += stride) {
-        if ((threadIdx.x & 31) == 0) {
+        if (pf && (threadIdx.x & 31) == 0) {
             for (int i = 0; i < k; ++i) warp_prefetch(V + i * ldv, p, np, 32 / S);
             warp_prefetch(t, p, np, 32 / S);
         }
@@ -1360,7 +1360,7 @@ gs_reg(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__rest
         const double2 t0 = reinterpret_cast<const double2 *>(t)[p];
         const double2 tv = make_double2(t0.x - sv.x, t0.y - sv.y);
         if (h == 0) {
-            reinterpret_cast<double2 *>(out)[p] = make_double2(tv.x * sc, tv.y * sc);
+            __stcs(reinterpret_cast<double2 *>(out) + p, make_double2(tv.x * sc, tv.y * sc));  // no dirty-L2 backlog
             xs[0] = fma(tv.x, tv.x, fma(tv.y, tv.y, xs[0]));
         }
         if (DOTS) {
@@ -1630,18 +1630,22 @@ struct GsL {
             const int nt = ctx->num_sms * 2;
             constexpr int KR = K <= 32 ? K : 32;
             const bool split = KR == 32 && split_lanes(1, 1) == 2;
+            // L2 bulk prefetch helps the pass with the dot phase (it re-reads V), not the plain update;
+            // SBD_GS_PF=0/1 forces it off/on
+            const char *pfe = getenv("SBD_GS_PF");
+            const int pf = pfe && *pfe ? (*pfe == '1') : (kdot > 0 ? 1 : 0);
             if (kdot > 0 && split)
                 gs_reg<KR, true, 2><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale,
-                                                                      ctx->red.as<double>());
+                                                                      ctx->red.as<double>(), pf);
             else if (kdot > 0)
                 gs_reg<KR, true, 1><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale,
-                                                                      ctx->red.as<double>());
+                                                                      ctx->red.as<double>(), pf);
             else if (split)
                 gs_reg<KR, false, 2><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale,
-                                                                       ctx->red.as<double>());
+                                                                       ctx->red.as<double>(), pf);
             else
                 gs_reg<KR, false, 1><<<nt, kRegBlock, 0, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale,
-                                                                       ctx->red.as<double>());
+                                                                       ctx->red.as<double>(), pf);
             finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
             SBD_LAUNCHED(ctx, "gs_update");
             return SBD_OK;
