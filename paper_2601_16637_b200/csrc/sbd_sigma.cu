@@ -206,9 +206,11 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
 // is the only synchronisation (no barriers in the stream).
 constexpr int kTW = 256;
 
+constexpr int kSideCtas = 4;  // resident CTAs per SM: registers <= 64, 4 x 48 KB rings (5 CTAs spill and need a 2-slot ring: slower)
+
 template <bool ALPHA>
 struct SideAsync {
-    static constexpr int kRing = 4;  // the alpha side's epilogue tile reuses the ring after the stream
+    static constexpr int kRing = 3;  // the alpha side epilogue tile reuses the ring after the stream
     static constexpr size_t smem() { return sizeof(double) * (size_t)kRowsPerCta * kRing * kTW; }
     static_assert(sizeof(double) * kTW * (kRowsPerCta + 1) <= smem(), "epilogue tile must fit the ring");
 };
@@ -221,7 +223,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <bool ALPHA>
-__global__ void __launch_bounds__(kRowsPerCta * 32, 3) side_kernel_async(SideArgs a) {
+__global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async(SideArgs a) {
     constexpr int R = SideAsync<ALPHA>::kRing;
     extern __shared__ __align__(128) unsigned char ssm[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
