@@ -21,6 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 POINTS = [  # norb, electrons per spin, strings per spin
+    (12, 6, 924),    # cfg1: the full 12-orbital string set (dense: task 0 dominates)
     (16, 8, 1000),
     (20, 10, 3162),
     (26, 7, 10000),
