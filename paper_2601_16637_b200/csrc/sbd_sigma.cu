@@ -210,9 +210,8 @@ constexpr int kSideCtas = 4;  // resident CTAs per SM: registers <= 64, 4 x 48 K
 
 template <bool ALPHA>
 struct SideAsync {
-    static constexpr int kRing = 3;  // the alpha side epilogue tile reuses the ring after the stream
+    static constexpr int kRing = 3;
     static constexpr size_t smem() { return sizeof(double) * (size_t)kRowsPerCta * kRing * kTW; }
-    static_assert(sizeof(double) * kTW * (kRowsPerCta + 1) <= smem(), "epilogue tile must fit the ring");
 };
 
 __device__ __forceinline__ void cp_async16(void *dst_smem, const void *src) {
@@ -289,47 +288,32 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
         cp_async_wait<0>();
     }
 
-    if (ALPHA) {
-        // + (B X^T)^T : tile YT[c0:c0+256, r0:r0+8] through shared memory (the
-        // rings are drained: every warp waited for its last copy group)
-        __syncthreads();
-        double(*tile)[kRowsPerCta + 1] = reinterpret_cast<double(*)[kRowsPerCta + 1]>(ssm);
-        const i64 r0 = (i64)blockIdx.x * kRowsPerCta;
-        {
-            const int i = threadIdx.x;  // one column of the tile per thread
-            if (i < ncol) {
-                const double2 *srcp = reinterpret_cast<const double2 *>(a.YT + (c0 + i) * a.ldyt + r0);
+    if (ALPHA && row_ok) {
+        // + (B X^T)^T: Y^T[c, r] read directly.  The CTA's 8 rows r0..r0+7 are 64
+        // contiguous bytes of each Y^T column, so the 8 warps share one L1 line per
+        // column and no block barrier (warps finish unevenly) is needed.
+        const i64 g = a.row_base + r;
+        const double *drow = a.diag + r * a.ldy + c0, *xrow = a.X + g * a.ldx + c0;
+        const bool t0 = a.a_s_off != nullptr && a.a_s_off[g + 1] != a.a_s_off[g];
+        const double *yrow = a.Y + r * a.ldy + c0;
+        const double *ytc = a.YT + c0 * a.ldyt + r;
 #pragma unroll
-                for (int q = 0; q < kRowsPerCta / 2; ++q) {
-                    const double2 u = srcp[q];
-                    tile[i][2 * q] = u.x;
-                    tile[i][2 * q + 1] = u.y;
+        for (int h = 0; h < 4; ++h) {
+            const int cc = 2 * lane + 64 * h;
+            if (ok[2 * h + 1]) {
+                const double2 d = __ldcs(reinterpret_cast<const double2 *>(drow + cc));
+                const double2 x = __ldg(reinterpret_cast<const double2 *>(xrow + cc));
+                const double t0v = __ldg(ytc + cc * a.ldyt), t1v = __ldg(ytc + (cc + 1) * a.ldyt);
+                acc[2 * h] = fma(d.x, x.x, acc[2 * h] + t0v);
+                acc[2 * h + 1] = fma(d.y, x.y, acc[2 * h + 1] + t1v);
+                if (t0) {
+                    const double2 p = *reinterpret_cast<const double2 *>(yrow + cc);
+                    acc[2 * h] += p.x;
+                    acc[2 * h + 1] += p.y;
                 }
-            }
-        }
-        __syncthreads();
-        if (row_ok) {
-            const i64 g = a.row_base + r;
-            const double *drow = a.diag + r * a.ldy + c0, *xrow = a.X + g * a.ldx + c0;
-            const bool t0 = a.a_s_off != nullptr && a.a_s_off[g + 1] != a.a_s_off[g];
-            const double *yrow = a.Y + r * a.ldy + c0;
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int cc = 2 * lane + 64 * h;
-                if (ok[2 * h + 1]) {
-                    const double2 d = __ldcs(reinterpret_cast<const double2 *>(drow + cc));
-                    const double2 x = __ldg(reinterpret_cast<const double2 *>(xrow + cc));
-                    acc[2 * h] = fma(d.x, x.x, acc[2 * h] + tile[cc][w]);
-                    acc[2 * h + 1] = fma(d.y, x.y, acc[2 * h + 1] + tile[cc + 1][w]);
-                    if (t0) {
-                        const double2 p = *reinterpret_cast<const double2 *>(yrow + cc);
-                        acc[2 * h] += p.x;
-                        acc[2 * h + 1] += p.y;
-                    }
-                } else if (ok[2 * h]) {
-                    acc[2 * h] = fma(drow[cc], xrow[cc], acc[2 * h] + tile[cc][w]);
-                    if (t0) acc[2 * h] += yrow[cc];
-                }
+            } else if (ok[2 * h]) {
+                acc[2 * h] = fma(drow[cc], xrow[cc], acc[2 * h] + __ldg(ytc + cc * a.ldyt));
+                if (t0) acc[2 * h] += yrow[cc];
             }
         }
     }
