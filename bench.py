@@ -474,9 +474,11 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (x = 800 MB); no flush", "setup_s": setup_s},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "sigma build (transpose + beta-side + alpha-side row-stream kernels)",
+                     "kernel": "sigma build (transpose + beta-side + task-0 + alpha-side kernels)",
                      "algorithmic_bytes": "8*N_own*(3 + cbar_alpha) per sigma (BASELINE.md section 4)",
-                     "bytes_per_launch": bytes_rank},
+                     "bytes_per_launch": bytes_rank,
+                     "per_kernel_ncu": (traffic_rec or {}).get("per_kernel"),
+                     "ncu_source": (traffic_rec or {}).get("source")},
         "kernels": kernels,
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
