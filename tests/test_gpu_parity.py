@@ -175,7 +175,8 @@ def test_random_instances_vs_oracle(unstaged, monkeypatch):
         monkeypatch.setenv("SBD_CROSS_UNSTAGED", "1")
     cases = [(10, 5, 4, 77, 131, 1), (14, 3, 4, 301, 257, 2), (16, 8, 8, 500, 1, 3), (16, 8, 8, 1, 499, 4),
              (12, 6, 6, 924, 129, 5), (20, 2, 9, 190, 600, 6), (14, 2, 7, 40, 3432, 7),
-             (12, 6, 6, 924, 130, 8)]  # 924 rows, even n_beta: pipelined host-buffer path
+             (12, 6, 6, 924, 130, 8),   # 924 rows, even n_beta: pipelined host-buffer path
+             (64, 2, 3, 300, 220, 9)]   # 64 orbitals: bit 63 in play, 2016 orbital pairs
     for norb, na, nb, nsa, nsb, seed in cases:
         a, _ = random_product_strings(norb, na, na, nsa, 1, seed)
         _, b = random_product_strings(norb, nb, nb, 1, nsb, seed + 100)
