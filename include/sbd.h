@@ -191,6 +191,57 @@ int sbd_combine(sbd_ctx *ctx, const double *V_dev, int k, int64_t ldv, int64_t n
 int sbd_jacobi(sbd_ctx *ctx, const double *A_dev, int k, int lda, double *evals_dev,
                double *evecs_dev, int max_sweeps, int *info_dev);
 
+/* ---- Native Davidson driver (davidson_solve, davidson.py:191-306) ---- */
+
+/* DavidsonOptions (davidson.py:32-53) with the reference defaults
+ * (sbd_davidson_default_opts), plus the B200 orthogonality tracking flag. */
+typedef struct sbd_davidson_opts {
+    int n_roots;             /* 1 */
+    double tol_residual;     /* 1e-8 */
+    int max_iters;           /* 200 */
+    int max_subspace;        /* 32 (<= 64) */
+    int restart_keep;        /* 4 */
+    double precond_delta;    /* 1e-6 */
+    int reorthogonalize;     /* 1 */
+    int track_orthogonality; /* 1: ortho_hist[i] = ||G - I||_F from the fused Gram row */
+} sbd_davidson_opts;
+
+/* DavidsonStats (davidson.py:56-68).  The history pointers are optional
+ * caller-owned HOST arrays (NULL = not recorded): theta_hist and res_hist hold
+ * max_iters x n_roots doubles (row = iteration, NaN past the roots found),
+ * ortho_hist, apply_ms_hist (sigma device time) and iter_ms_hist (host wall
+ * time per iteration) max_iters doubles, restart_iters max_iters ints. */
+typedef struct sbd_davidson_stats {
+    int iterations;
+    int converged;
+    int n_applies;
+    int restarts;
+    int breakdowns;
+    int n_found;          /* roots returned: min(n_roots, final subspace size) */
+    double sigma_ms;      /* summed device time of the sigma builds (CUDA events) */
+    double *theta_hist;
+    double *res_hist;
+    double *ortho_hist;
+    double *apply_ms_hist;
+    double *iter_ms_hist;
+    int *restart_iters;
+} sbd_davidson_stats;
+
+int sbd_davidson_default_opts(sbd_davidson_opts *opts);
+
+/* Lowest n_roots eigenpairs of the context's Hamiltonian (product or explicit
+ * basis; all rows must be owned -- multi-GPU solves go through the Python
+ * DistributedApplier).  diag_dev: the preconditioner's diagonal (N doubles) or
+ * NULL for the context's own H_ii (sbd_diag).  x0_dev: start vector (N doubles, normalised inside) or
+ * NULL for e_argmin(diag) (davidson.py:219-227).  evals_host / res_norms_host:
+ * n_roots doubles; evecs_dev: n_roots rows of ldu doubles (may be NULL).
+ * Non-convergence is not an error: stats->converged = 0 (davidson.py:271-275).
+ * Jacobi non-convergence returns SBD_ECUDA (RuntimeError, davidson.py:144-145).
+ * Breakdown recovery draws its random direction on the device, not from
+ * numpy's generator (davidson.py:295). */
+int sbd_davidson(sbd_ctx *ctx, const sbd_davidson_opts *opts, const double *diag_dev, const double *x0_dev,
+                 double *evals_host, double *res_norms_host, double *evecs_dev, int64_t ldu, sbd_davidson_stats *stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -56,7 +56,25 @@ _SIGS = {
     "sbd_rotate": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _c_int],
     "sbd_combine": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _c_int, _vp, _c_i64],
     "sbd_jacobi": [_vp, _vp, _c_int, _c_int, _vp, _vp, _c_int, _vp],
+    "sbd_davidson_default_opts": [_vp],
+    "sbd_davidson": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _vp],
 }
+
+
+class DavidsonOptsC(ctypes.Structure):
+    """``sbd_davidson_opts`` (include/sbd.h)."""
+    _fields_ = [("n_roots", _c_int), ("tol_residual", _c_dbl), ("max_iters", _c_int), ("max_subspace", _c_int),
+                ("restart_keep", _c_int), ("precond_delta", _c_dbl), ("reorthogonalize", _c_int),
+                ("track_orthogonality", _c_int)]
+
+
+class DavidsonStatsC(ctypes.Structure):
+    """``sbd_davidson_stats`` (include/sbd.h); history pointers are caller-owned host arrays."""
+    _fields_ = [("iterations", _c_int), ("converged", _c_int), ("n_applies", _c_int), ("restarts", _c_int),
+                ("breakdowns", _c_int), ("n_found", _c_int), ("sigma_ms", _c_dbl), ("theta_hist", _vp),
+                ("res_hist", _vp), ("ortho_hist", _vp), ("apply_ms_hist", _vp), ("iter_ms_hist", _vp), ("restart_iters", _vp)]
+
+
 _RESTYPE = {"sbd_last_error": ctypes.c_char_p}
 
 EXPORTED = tuple(_SIGS)

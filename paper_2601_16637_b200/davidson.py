@@ -243,13 +243,18 @@ def _operator(apply_h, n: int, device):
 
 def davidson_solve(apply_h: Callable, diag, x0=None, opts: Optional[DavidsonOptions] = None,
                    device=None, return_device: bool = False, allreduce=None,
-                   rank_offset: int = 0, ctx=None) -> DavidsonResult:
+                   rank_offset: int = 0, ctx=None, native: Optional[bool] = None) -> DavidsonResult:
     """Lowest ``opts.n_roots`` eigenpairs (reference ``davidson.py:191-306``).
 
     ``allreduce(tensor)`` (optional) sums a small CUDA tensor over ranks in
     place; the row-partitioned multi-GPU driver passes an NCCL all-reduce,
     its ``apply_h(x_dev, y_dev)`` on the rank's rows, and ``rank_offset`` =
     global index of the rank's first amplitude.
+
+    ``native``: run the control loop in C++ (``sbd_davidson``, same algorithm
+    and kernels, no Python between the passes).  Default: on for a
+    single-GPU ``HamiltonianApplier`` unless ``opts.profile`` is set or
+    ``SBD_DAV_PYTHON=1``; ``True`` raises ValueError where it cannot apply.
     """
     import torch
 
@@ -277,9 +282,83 @@ def davidson_solve(apply_h: Callable, diag, x0=None, opts: Optional[DavidsonOpti
         if device is None:
             device = torch.cuda.current_device()
     dev = torch.device("cuda", int(device))
+    if _use_native(apply_h, allreduce, opts, native):
+        with torch.cuda.device(dev):
+            dd = diag if isinstance(diag, torch.Tensor) else torch.from_numpy(diag_np)
+            return _solve_native(apply_h, dd.to(dev, torch.float64).contiguous(), x0, opts, n, dev, return_device)
     with torch.cuda.device(dev):
         return _solve(apply_h, diag_dev if diag_dev is not None else torch.from_numpy(diag_np).to(dev),
                       x0, opts, n, n_loc, dev, return_device, allreduce, rank_offset, ctx)
+
+
+def _use_native(apply_h, allreduce, opts, native) -> bool:
+    import os
+
+    from .apply import HamiltonianApplier
+
+    ok = (allreduce is None and isinstance(apply_h, HamiltonianApplier) and apply_h.n_own == apply_h.n
+          and not opts.profile)
+    if native is None:
+        return ok and os.environ.get("SBD_DAV_PYTHON", "0") != "1"
+    if native and not ok:
+        raise ValueError("native=True needs a single-GPU HamiltonianApplier owning all rows and profile=False")
+    return bool(native)
+
+
+def _solve_native(app, diag_dev, x0, opts, n, dev, return_device):
+    """C++ control loop (``sbd_davidson``, csrc/sbd_solver.cu) over the applier's context."""
+    import ctypes
+
+    import torch
+
+    f64 = dict(dtype=torch.float64, device=dev)
+    if diag_dev.numel() != n:
+        raise ValueError(f"diag has {diag_dev.numel()} entries, expected {n}")
+    v0 = None
+    if x0 is not None:
+        v0 = (x0.to(**f64) if isinstance(x0, torch.Tensor)
+              else torch.from_numpy(np.asarray(x0, dtype=np.float64).copy()).to(dev)).reshape(-1).contiguous()
+        if v0.numel() != n:
+            raise ValueError(f"x0 has {v0.numel()} entries, expected {n}")
+    m, mi = opts.n_roots, opts.max_iters
+    hist = {name: np.full(mi * (m if name in ("theta", "res") else 1), np.nan)
+            for name in ("theta", "res", "ortho", "apply", "iter")}
+    restart_iters = np.zeros(mi, dtype=np.int32)
+    o = _lib.DavidsonOptsC(n_roots=m, tol_residual=float(opts.tol_residual), max_iters=mi,
+                           max_subspace=opts.max_subspace, restart_keep=opts.restart_keep,
+                           precond_delta=float(opts.precond_delta), reorthogonalize=int(opts.reorthogonalize),
+                           track_orthogonality=int(opts.track_orthogonality))
+    st = _lib.DavidsonStatsC(theta_hist=hist["theta"].ctypes.data, res_hist=hist["res"].ctypes.data,
+                             ortho_hist=hist["ortho"].ctypes.data, apply_ms_hist=hist["apply"].ctypes.data,
+                             iter_ms_hist=hist["iter"].ctypes.data, restart_iters=restart_iters.ctypes.data)
+    evals = np.full(m, np.nan)
+    res = np.full(m, np.nan)
+    U = torch.empty((m, n), **f64)
+    ctx = app.context
+    ctx.bind_stream()
+    ctx("sbd_davidson", ctypes.byref(o), _p(diag_dev), _p(v0), evals.ctypes.data, res.ctypes.data, _p(U), n,
+        ctypes.byref(st))
+    app.apply_count += st.n_applies
+    it, nf = st.iterations, st.n_found
+    stats = DavidsonStats(iterations=it, converged=bool(st.converged), n_applies=st.n_applies,
+                          restarts=st.restarts, breakdowns=st.breakdowns)
+    th = hist["theta"].reshape(mi, m)[:it]
+    rs = hist["res"].reshape(mi, m)[:it]
+    prev = None
+    for i in range(it):
+        row = th[i][~np.isnan(th[i])]
+        stats.theta_history.append(row.copy())
+        stats.residual_history.append(rs[i][~np.isnan(rs[i])].copy())
+        stats.theta_deltas.append(abs(row[0] - prev) if prev is not None else np.inf)
+        prev = row[0]
+    stats.ortho_history = [float(v) for v in hist["ortho"][:it]]
+    stats.apply_seconds = [float(v) / 1e3 for v in hist["apply"][:it]]
+    stats.iter_seconds = [float(v) / 1e3 for v in hist["iter"][:it]]
+    stats.restart_iters = [int(v) for v in restart_iters[:st.restarts]]
+    stats.host_ms = {"native": float(np.nansum(hist["iter"][:it]))}
+    U = U[:nf]
+    vectors = U if return_device else U.cpu().numpy()
+    return DavidsonResult(energies=evals[:nf].copy(), vectors=vectors, residual_norms=res[:nf].copy(), stats=stats)
 
 
 def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce, rank_offset, ctx):

@@ -148,3 +148,85 @@ def test_cfg1_ground_state_vs_reference():
     assert res.converged
     assert res.energies[0] == pytest.approx(ref["energy"], abs=1e-8)
     assert abs(res.stats.iterations - ref["iterations"]) <= 2
+
+
+@pytest.mark.parametrize("case", [
+    dict(),                                                   # reference defaults
+    dict(n_roots=3, restart_keep=4, max_iters=120),           # multi-root, stops unconverged
+    dict(max_subspace=6, restart_keep=2, max_iters=400),      # many thick restarts
+    dict(reorthogonalize=False),                              # single Gram-Schmidt pass
+    dict(track_orthogonality=False, tol_residual=1e-10),
+])
+def test_native_driver_matches_python_driver(case):
+    """sbd_davidson (C++ control loop) runs the same kernels in the same order as the Python driver."""
+    from paper_2601_16637_b200 import DavidsonOptions, HamiltonianApplier, SelectedBasis, davidson_solve
+    from paper_2601_16637_b200.synth import random_integrals, random_product_strings
+
+    a, b = random_product_strings(12, 5, 4, 400, 300, seed=31)
+    app = HamiltonianApplier(SelectedBasis.product(a.tolist(), b.tolist(), 12, 5, 4), random_integrals(12, seed=3))
+    opts = DavidsonOptions(**case)
+    nat = davidson_solve(app, app.diag, opts=opts, native=True)
+    py = davidson_solve(app, app.diag, opts=opts, native=False)
+    assert nat.converged == py.converged and (nat.converged or opts.max_iters == 120)
+    assert nat.stats.iterations == py.stats.iterations
+    assert nat.stats.restarts == py.stats.restarts and nat.stats.restart_iters == py.stats.restart_iters
+    np.testing.assert_allclose(nat.energies, py.energies, atol=1e-10, rtol=0)
+    np.testing.assert_allclose(nat.residual_norms, py.residual_norms, atol=1e-9, rtol=1e-4)
+    for j in range(opts.n_roots):
+        assert abs(abs(nat.vectors[j] @ py.vectors[j]) - 1.0) <= 1e-9
+    assert len(nat.stats.theta_history) == nat.stats.iterations
+    np.testing.assert_allclose(nat.stats.theta_history[-1], py.stats.theta_history[-1], atol=1e-10, rtol=0)
+    if opts.track_orthogonality:
+        assert max(nat.stats.ortho_history) <= 1e-10
+    assert len(nat.stats.apply_seconds) == nat.stats.iterations and min(nat.stats.apply_seconds) > 0
+
+
+def test_native_driver_edge_cases():
+    from paper_2601_16637_b200 import (DavidsonOptions, HamiltonianApplier, IntegralTable, SelectedBasis,
+                                       davidson_solve)
+    from paper_2601_16637_b200.synth import random_integrals, random_product_strings
+
+    # Hubbard dimer: k_max = n = 4, the subspace fills and breaks down
+    t = IntegralTable(2)
+    t.set_h(0, 1, -1.0)
+    t.set_eri(0, 0, 0, 0, 4.0)
+    t.set_eri(1, 1, 1, 1, 4.0)
+    app = HamiltonianApplier(SelectedBasis.product([1, 2], [1, 2], 2, 1, 1), t)
+    res = davidson_solve(app, app.diag, native=True)
+    assert res.converged and res.energies[0] == pytest.approx(2.0 - np.sqrt(8.0), abs=1e-8)
+    # x0 from the sample weights, and the zero-x0 error
+    a, b = random_product_strings(10, 5, 5, 60, 50, seed=2)
+    app = HamiltonianApplier(SelectedBasis.product(a.tolist(), b.tolist(), 10, 5, 5), random_integrals(10, seed=1))
+    inst = O.Instance.make(10, app.table.h, app.table.eri, app.table.e_core, a, b)
+    ref = O.davidson(lambda v: O.sigma(inst, v), O.diag(inst)).energies[0]
+    x0 = np.random.default_rng(5).random(app.n)
+    r1 = davidson_solve(app, app.diag, x0=x0, native=True)
+    r2 = davidson_solve(app, app.diag, x0=x0, native=False)
+    # x0 is normalised by a different reduction order (ulp-level start difference)
+    assert r1.converged and abs(r1.energies[0] - ref) <= 1e-8 and abs(r1.stats.iterations - r2.stats.iterations) <= 4
+    with pytest.raises(ValueError):
+        davidson_solve(app, app.diag, x0=np.zeros(app.n), native=True)
+    with pytest.raises(ValueError):
+        davidson_solve(lambda v: v, np.ones(3), native=True)
+    # max_iters honoured, not converged is not an error
+    r = davidson_solve(app, app.diag, opts=DavidsonOptions(max_iters=3), native=True)
+    assert r.stats.iterations == 3 and not r.converged and np.isfinite(r.energies).all()
+    assert app.apply_count >= 3
+
+
+def test_native_driver_explicit_basis(explicit_golden, explicit_meta):
+    from paper_2601_16637_b200 import DavidsonOptions, HamiltonianApplier, davidson_solve
+
+    from test_gpu_explicit import _basis
+
+    for name in ("expl_10_5_5", "expl_single"):
+        m = explicit_meta[name]
+        basis, table = _basis(explicit_golden, explicit_meta, name)
+        app = HamiltonianApplier(basis, table)
+        n = basis.dimension
+        opts = DavidsonOptions(n_roots=m["n_roots"], restart_keep=min(4, n), max_subspace=min(32, n))
+        nat = davidson_solve(app, app.diag, opts=opts, native=True)
+        py = davidson_solve(app, app.diag, opts=opts, native=False)
+        assert nat.converged and nat.stats.iterations == py.stats.iterations
+        np.testing.assert_allclose(nat.energies, explicit_golden[f"{name}/energies"], atol=1e-8)
+        np.testing.assert_allclose(nat.energies, py.energies, atol=1e-10, rtol=0)

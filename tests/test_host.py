@@ -138,3 +138,18 @@ def test_no_cpu_fallback_without_gpu():
 
     with pytest.raises(RuntimeError):
         HamiltonianApplier(full_product_basis(4, 2, 2), random_integrals(4, seed=0))
+
+
+def test_native_davidson_default_options_match_reference_defaults():
+    """sbd_davidson_default_opts (C) == DavidsonOptions() (davidson.py:33-40); struct layout via ctypes."""
+    import ctypes
+
+    from paper_2601_16637_b200 import DavidsonOptions, _lib
+
+    o = _lib.DavidsonOptsC()
+    assert _lib.load().sbd_davidson_default_opts(ctypes.byref(o)) == 0
+    d = DavidsonOptions()
+    for f in ("n_roots", "tol_residual", "max_iters", "max_subspace", "restart_keep", "precond_delta",
+              "reorthogonalize", "track_orthogonality"):
+        assert getattr(o, f) == getattr(d, f), f
+    assert _lib.load().sbd_davidson_default_opts(None) == 1
