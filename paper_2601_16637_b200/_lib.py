@@ -13,7 +13,8 @@ from typing import Optional
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsbd_b200.so")
+# SBD_LIB overrides the in-tree library (A/B measurements of two builds on one box)
+LIB_PATH = os.environ.get("SBD_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsbd_b200.so")
 
 _c_i64 = ctypes.c_int64
 _c_int = ctypes.c_int

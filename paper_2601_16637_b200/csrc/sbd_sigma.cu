@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
 // is the only synchronisation (no barriers in the stream).
 constexpr int kTW = 256;
 
+constexpr double kEpiCbar = 8.0;  // alpha side stages the epilogue operands in the ring below this c-bar
 constexpr int kSideCtas = 4;  // resident CTAs per SM: registers <= 64, 4 x 48 KB rings (5 CTAs spill and need a 2-slot ring: slower)
 
 template <bool ALPHA>
@@ -221,7 +222,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <bool ALPHA>
+template <bool ALPHA, bool EPI = false>
 __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async(SideArgs a) {
     constexpr int R = SideAsync<ALPHA>::kRing;
     extern __shared__ __align__(128) unsigned char ssm[];
@@ -241,11 +242,28 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
     double acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    i64 nstream = 0;
     if (row_ok) {
         const i64 g = a.row_base + r;
         const i64 e0 = a.conn_off[g], n = a.conn_off[g + 1] - e0;
+        // EPI (alpha side, sparse configs): the two ring slots the stream frees last
+        // are refilled with the epilogue's diag and own-x segments (ring positions n
+        // and n + 1), so their HBM latency overlaps the stream's tail instead of
+        // following it.  Same-box A/B: -6% at 1e9 dets (c-bar 0.74), -1.5% at cfg4
+        // (4.1), but +3-4% at 3.2e8 (13) and cfg2 (57): chosen by c-bar below kEpiCbar.
         auto issue = [&](i64 i, int slot) {
-            if (i < n) {
+            if constexpr (EPI) {
+                const double *src = nullptr;
+                if (i < n) src = a.X + (i64)a.conn[e0 + i].tgt * a.ldx + c0;
+                else if (i == n) src = a.diag + r * a.ldy + c0;
+                else if (i == n + 1) src = a.X + g * a.ldx + c0;
+                if (src) {
+                    double *dst = ring + (size_t)slot * kTW;
+#pragma unroll
+                    for (int h = 0; h < 4; ++h)
+                        if (pair[h]) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
+                }
+            } else if (i < n) {
                 const double *src = a.X + (i64)a.conn[e0 + i].tgt * a.ldx + c0;
                 double *dst = ring + (size_t)slot * kTW;
 #pragma unroll
@@ -254,6 +272,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
             }
             cp_async_commit();
         };
+        if (EPI) nstream = n;
 #pragma unroll
         for (int i = 0; i < R - 1; ++i) issue(i, i);
         int slot = 0;
@@ -293,7 +312,9 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
         // contiguous bytes of each Y^T column, so the 8 warps share one L1 line per
         // column and no block barrier (warps finish unevenly) is needed.
         const i64 g = a.row_base + r;
+        constexpr bool epi = EPI;
         const double *drow = a.diag + r * a.ldy + c0, *xrow = a.X + g * a.ldx + c0;
+        const double *dring = ring + (size_t)(nstream % R) * kTW, *xring = ring + (size_t)((nstream + 1) % R) * kTW;
         const bool t0 = a.a_s_off != nullptr && a.a_s_off[g + 1] != a.a_s_off[g];
         const double *yrow = a.Y + r * a.ldy + c0;
         const double *ytc = a.YT + c0 * a.ldyt + r;
@@ -301,8 +322,10 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
         for (int h = 0; h < 4; ++h) {
             const int cc = 2 * lane + 64 * h;
             if (ok[2 * h + 1]) {
-                const double2 d = __ldcs(reinterpret_cast<const double2 *>(drow + cc));
-                const double2 x = __ldg(reinterpret_cast<const double2 *>(xrow + cc));
+                const double2 d = epi ? *reinterpret_cast<const double2 *>(dring + cc)
+                                      : __ldcs(reinterpret_cast<const double2 *>(drow + cc));
+                const double2 x = epi ? *reinterpret_cast<const double2 *>(xring + cc)
+                                      : __ldg(reinterpret_cast<const double2 *>(xrow + cc));
                 const double t0v = __ldg(ytc + cc * a.ldyt), t1v = __ldg(ytc + (cc + 1) * a.ldyt);
                 acc[2 * h] = fma(d.x, x.x, acc[2 * h] + t0v);
                 acc[2 * h + 1] = fma(d.y, x.y, acc[2 * h + 1] + t1v);
@@ -312,7 +335,8 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
                     acc[2 * h + 1] += p.y;
                 }
             } else if (ok[2 * h]) {
-                acc[2 * h] = fma(drow[cc], xrow[cc], acc[2 * h] + __ldg(ytc + cc * a.ldyt));
+                acc[2 * h] = fma(epi ? dring[cc] : drow[cc], epi ? xring[cc] : xrow[cc],
+                                 acc[2 * h] + __ldg(ytc + cc * a.ldyt));
                 if (t0) acc[2 * h] += yrow[cc];
             }
         }
@@ -945,10 +969,16 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
         if (!attr) {
             SBD_CUDA(ctx, cudaFuncSetAttribute(side_kernel_async<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)SideAsync<true>::smem()));
+            SBD_CUDA(ctx, cudaFuncSetAttribute(side_kernel_async<true, true>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SideAsync<true>::smem()));
             attr = true;
         }
         dim3 gt((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kTW - 1) / kTW));
-        side_kernel_async<true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
+        const double cbar = A.n ? (double)(A.ns + A.nd) / (double)A.n : 0.0;
+        if (cbar < kEpiCbar)
+            side_kernel_async<true, true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
+        else
+            side_kernel_async<true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
     } else {
         dim3 g((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kColsPerWarp - 1) / kColsPerWarp));
         if (vec) side_kernel<true, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
