@@ -398,6 +398,8 @@ struct CrossArgs {
     int pbits;
     const double *vsg;       // sign-folded ERI rows, row (P, s) at (2P + s) * 2 ld
     i64 ld;
+    i64 gz;                  // groups processed (a prefix: groups are sorted by single count)
+    bool add;                // y += task 0 on the processed positions (run after the alpha side)
 };
 
 __device__ __forceinline__ const double *vrow(const CrossArgs &a, const SConn &sa) {
@@ -414,7 +416,7 @@ __device__ __forceinline__ void cross_accumulate(double (&acc)[CPT], const Cross
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
         const i64 g = g_lo + warp + (i64)j * nw;
-        if (g < a.groups) {
+        if (g < a.gz) {
             const int o0 = goff_h[g], w = (goff_h[g + 1] - o0) >> 5;
             const uint32_t *ep = ent + o0 + lane;
             int q = 0;
@@ -443,11 +445,14 @@ __device__ __forceinline__ void cross_store(double (&acc)[CPT], const CrossArgs 
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {  // all column loads first: one round trip, not CPT
         const i64 g = g_lo + warp + (i64)j * nw;
-        c[j] = g < a.groups ? __ldg(a.col + g * 32 + lane) : -1;
+        c[j] = g < a.gz ? __ldg(a.col + g * 32 + lane) : -1;
     }
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
-        if (c[j] >= 0) yr[c[j]] = acc[j];
+        if (c[j] >= 0) {
+            if (a.add) yr[c[j]] += acc[j];
+            else yr[c[j]] = acc[j];
+        }
         acc[j] = 0.0;
     }
 }
@@ -840,7 +845,27 @@ int launch_cross_tma_cpt(sbd_ctx *ctx, const CrossArgs &ca, size_t smem, i64 cpt
     return launch_cross_tma<14, SENT>(ctx, ca, smem);
 }
 
-int launch_cross(sbd_ctx *ctx, const double *x_full, double *y) {
+// Beta SELL groups that hold any single (a prefix: sorted by total count).
+i64 sell_nonzero_groups(const Sector &B) {
+    const i64 G = B.sell_groups;
+    i64 nz = 0;
+    for (i64 g = 0; g < G; ++g) {
+        i64 w = 0;
+        for (i64 h = 0; h < B.sell_h; ++h) w += B.sell_goff_host[h * (G + 1) + g + 1] - B.sell_goff_host[h * (G + 1) + g];
+        if (w > 0) nz = g + 1;
+    }
+    return nz;
+}
+
+// Additive task 0: when most beta strings have no in-set single (sparse configs),
+// task 0 is added to the finished rows on the few positions it touches, after
+// the alpha side, instead of writing whole rows that the alpha side reads back.
+bool cross_additive(const sbd_ctx *ctx) {
+    const Sector &B = ctx->sec[1];
+    return B.sell_groups > 0 && 2 * sell_nonzero_groups(B) < B.sell_groups;
+}
+
+int launch_cross(sbd_ctx *ctx, const double *x_full, double *y, bool additive = false) {
     const Sector &A = ctx->sec[0], &B = ctx->sec[1];
     CrossArgs ca{};
     ca.n_rows = ctx->own_rows();
@@ -860,6 +885,8 @@ int launch_cross(sbd_ctx *ctx, const double *x_full, double *y) {
     ca.pbits = B.sell_pbits;
     ca.vsg = ctx->vpp.as<double>();
     ca.ld = ctx->ld_vpp;
+    ca.gz = ca.groups;
+    ca.add = false;
     constexpr size_t kSmemMax = 227 * 1024;
     const i64 ngoff = ca.H * (ca.groups + 1);
     const size_t base = 128 + sizeof(double) * kCrossStages * (size_t)cross_stage_doubles(ca.chunk, ca.ld) +
@@ -868,7 +895,11 @@ int launch_cross(sbd_ctx *ctx, const double *x_full, double *y) {
     const i64 cpt = (ca.groups + kCrossThreads / 32 - 2) / (kCrossThreads / 32 - 1);
     const char *force = getenv("SBD_CROSS_UNSTAGED");  // test knob: exercise the flat variant
     const char *nomc = getenv("SBD_CROSS_NO_CLUSTER");  // test knob: exercise the single-CTA pipeline
-    if (!(force && force[0] == '1') && !(nomc && nomc[0] == '1') && ca.H == 1 && (B.n % 2 == 0) &&
+    if (additive) {
+        ca.gz = sell_nonzero_groups(B);
+        ca.add = true;
+    }
+    if (!additive && !(force && force[0] == '1') && !(nomc && nomc[0] == '1') && ca.H == 1 && (B.n % 2 == 0) &&
         aligned16(x_full) && (ctx->num_sms % 2 == 0)) {
         const i64 ngl = mc_local_groups(ca.groups, 0);
         i64 ent0 = 0, ent1 = 0;  // SELL entries per rank (host copy of the offsets)
@@ -884,12 +915,12 @@ int launch_cross(sbd_ctx *ctx, const double *x_full, double *y) {
             return launch_cross_mc<8>(ctx, ca, smem_mc);
         }
     }
-    const bool staged_ok = !(force && force[0] == '1') && (B.n % 2 == 0) && aligned16(x_full) && cpt <= 14;
+    const bool staged_ok = !additive && !(force && force[0] == '1') && (B.n % 2 == 0) && aligned16(x_full) && cpt <= 14;
     if (staged_ok && with_ent <= kSmemMax) return launch_cross_tma_cpt<true>(ctx, ca, with_ent, cpt);
     if (staged_ok && base <= kSmemMax) return launch_cross_tma_cpt<false>(ctx, ca, base, cpt);
     constexpr int kCpt = 8;
     const i64 gpt = (i64)(kCrossThreadsFlat / 32) * kCpt;
-    const i64 tiles = std::max<i64>(1, (ca.groups + gpt - 1) / gpt);
+    const i64 tiles = std::max<i64>(1, (ca.gz + gpt - 1) / gpt);
     const unsigned gx = (unsigned)std::max<i64>(1, std::min<i64>((i64)ctx->num_sms * 8 / tiles + 1, ctx->own_rows()));
     dim3 grid(gx, (unsigned)tiles);
     cross_kernel_flat<kCpt><<<grid, kCrossThreadsFlat, 0, ctx->stream>>>(ca);
@@ -942,7 +973,7 @@ int launch_beta_side(sbd_ctx *ctx, const double *x_own, i64 r0, i64 r1) {
 }
 
 // Alpha side (+ diagonal, task 0, beta side fold-in) for own rows [r0, r1) (local).
-int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64 r1) {
+int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64 r1, bool with_t0 = true) {
     const Sector &A = ctx->sec[0], &B = ctx->sec[1];
     const i64 nb = B.n, rows = r1 - r0;
     if (rows <= 0 || nb == 0) return SBD_OK;
@@ -962,7 +993,7 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
     a.YT = ctx->yt.as<double>() + r0;
     a.ldyt = ctx->ld_t;
     a.diag = ctx->diag.as<double>() + r0 * nb;
-    a.a_s_off = (A.ns > 0 && B.ns > 0) ? A.s_off.as<int64_t>() : nullptr;
+    a.a_s_off = (with_t0 && A.ns > 0 && B.ns > 0) ? A.s_off.as<int64_t>() : nullptr;
     const bool vec = (nb % 2 == 0) && aligned16(x_full) && aligned16(y) && (r0 % 2 == 0);
     if (vec && use_side_tma()) {
         static bool attr = false;
@@ -1035,6 +1066,11 @@ int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full, double *y) {
     if (rc) return rc;
     const Sector &A = ctx->sec[0], &B = ctx->sec[1];
     if (ctx->own_rows() == 0 || B.n == 0) return SBD_OK;
+    if (A.ns > 0 && B.ns > 0 && cross_additive(ctx)) {  // sparse singles: task 0 added afterwards
+        rc = launch_alpha_side(ctx, x_full, y, 0, ctx->own_rows(), false);
+        if (rc) return rc;
+        return launch_cross(ctx, x_full, y, true);
+    }
     if (A.ns > 0 && B.ns > 0) {  // task 0 exists only when both sectors have in-set singles
         rc = launch_cross(ctx, x_full, y);
         if (rc) return rc;
@@ -1076,7 +1112,8 @@ int sbd_sigma_host(sbd_ctx *ctx, const double *x_host, double *y_host) {
     SBD_CUDA(ctx, ctx->hx.ensure(sizeof(double) * (nfull + 2)));
     SBD_CUDA(ctx, ctx->hy.ensure(sizeof(double) * (nown + 2)));
     double *dx = ctx->hx.as<double>(), *dy = ctx->hy.as<double>();
-    const bool pipelined = !ctx->explicit_mode && rows == A.n && nb % 2 == 0 && use_side_tma() && rows > 2 * kTW;
+    const bool pipelined = !ctx->explicit_mode && rows == A.n && nb % 2 == 0 && use_side_tma() && rows > 2 * kTW &&
+                           !(A.ns > 0 && B.ns > 0 && cross_additive(ctx));
     if (!pipelined) {
         if (nfull) SBD_CUDA(ctx, cudaMemcpyAsync(dx, x_host, sizeof(double) * nfull, cudaMemcpyHostToDevice, ctx->stream));
         rc = sbd_sigma(ctx, dx, dy);
