@@ -25,4 +25,7 @@ timeout 600 python tools/profile_davidson.py > "$OUT/dav_profile.json" 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:'residual|gs_|vdots2|rotate' -s 60 -c 5 -o "$OUT/dav" \
     python tools/profile_davidson.py 24 > "$OUT/ncu_dav.log" 2>&1
+# keep the merged-back output under gpurun's 64 MiB: summarise the Davidson capture on the box
+python tools/ncu_summary.py "$OUT/dav.ncu-rep" > "$OUT/ncu_davidson_full.jsonl" 2>/dev/null && rm -f "$OUT/dav.ncu-rep"
+python tools/ncu_summary.py "$OUT/sigma.ncu-rep" > "$OUT/ncu_sigma_full.jsonl" 2>/dev/null
 echo done > "$OUT/DONE"
