@@ -687,7 +687,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrossThreads, 1) cr
                 }
 #pragma unroll
                 for (int j = 0; j < CPT; ++j) {
-                    if (c[j] >= 0) yr[c[j]] = acc[j];
+                    if (c[j] >= 0) {
+                        if (a.add) yr[c[j]] += acc[j];
+                        else yr[c[j]] = acc[j];
+                    }
                     acc[j] = 0.0;
                 }
             }
@@ -862,6 +865,8 @@ i64 sell_nonzero_groups(const Sector &B) {
 // the alpha side, instead of writing whole rows that the alpha side reads back.
 bool cross_additive(const sbd_ctx *ctx) {
     const Sector &B = ctx->sec[1];
+    const char *e = getenv("SBD_CROSS_ADD");  // 0/1 forces the task-0 order (A/B measurements, tests)
+    if (e && *e) return e[0] == '1';
     return B.sell_groups > 0 && 2 * sell_nonzero_groups(B) < B.sell_groups;
 }
 
@@ -899,7 +904,7 @@ int launch_cross(sbd_ctx *ctx, const double *x_full, double *y, bool additive = 
         ca.gz = sell_nonzero_groups(B);
         ca.add = true;
     }
-    if (!additive && !(force && force[0] == '1') && !(nomc && nomc[0] == '1') && ca.H == 1 && (B.n % 2 == 0) &&
+    if (!(force && force[0] == '1') && !(nomc && nomc[0] == '1') && ca.H == 1 && (B.n % 2 == 0) &&
         aligned16(x_full) && (ctx->num_sms % 2 == 0)) {
         const i64 ngl = mc_local_groups(ca.groups, 0);
         i64 ent0 = 0, ent1 = 0;  // SELL entries per rank (host copy of the offsets)
@@ -915,7 +920,7 @@ int launch_cross(sbd_ctx *ctx, const double *x_full, double *y, bool additive = 
             return launch_cross_mc<8>(ctx, ca, smem_mc);
         }
     }
-    const bool staged_ok = !additive && !(force && force[0] == '1') && (B.n % 2 == 0) && aligned16(x_full) && cpt <= 14;
+    const bool staged_ok = !(force && force[0] == '1') && (B.n % 2 == 0) && aligned16(x_full) && cpt <= 14;
     if (staged_ok && with_ent <= kSmemMax) return launch_cross_tma_cpt<true>(ctx, ca, with_ent, cpt);
     if (staged_ok && base <= kSmemMax) return launch_cross_tma_cpt<false>(ctx, ca, base, cpt);
     constexpr int kCpt = 8;

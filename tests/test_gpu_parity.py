@@ -160,8 +160,8 @@ def test_cfg2_full_size_properties():
     assert np.array_equal(ys, hx.cpu().numpy())
 
 
-@pytest.mark.parametrize("unstaged", [False, True])
-def test_random_instances_vs_oracle(unstaged, monkeypatch):
+@pytest.mark.parametrize("unstaged,order", [(False, "auto"), (True, "auto"), (False, "additive"), (True, "additive")])
+def test_random_instances_vs_oracle(unstaged, order, monkeypatch):
     """Ragged random sets across shapes, incl. odd n_beta (scalar path) and 1-string sectors.
 
     ``unstaged`` forces the task-0 kernel variant that gathers through L1/L2
@@ -173,6 +173,8 @@ def test_random_instances_vs_oracle(unstaged, monkeypatch):
 
     if unstaged:
         monkeypatch.setenv("SBD_CROSS_UNSTAGED", "1")
+    if order == "additive":  # task 0 added after the alpha side, whatever the single density
+        monkeypatch.setenv("SBD_CROSS_ADD", "1")
     cases = [(10, 5, 4, 77, 131, 1), (14, 3, 4, 301, 257, 2), (16, 8, 8, 500, 1, 3), (16, 8, 8, 1, 499, 4),
              (12, 6, 6, 924, 129, 5), (20, 2, 9, 190, 600, 6), (14, 2, 7, 40, 3432, 7),
              (12, 6, 6, 924, 130, 8),   # 924 rows, even n_beta: pipelined host-buffer path
