@@ -74,12 +74,13 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.start = 0
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
         except OSError:
@@ -89,6 +90,14 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def running(self) -> bool:
+        """True once nvidia-smi has produced a sample (or when it is unavailable)."""
+        return self.proc is None or len(self.lines) > 0
+
+    def mark(self):
+        """Start of the timed region: summary() only uses samples taken after this."""
+        self.start = len(self.lines)
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -101,7 +110,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[self.start:]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -359,6 +368,23 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
+        # keep the GPU busy (untimed) until the sampler is live, so every sample it
+        # reports below lies inside the timed region
+        t_wait = time.perf_counter()
+        while True:
+            live = clk.running() or time.perf_counter() - t_wait > 5.0
+            if world > 1:  # every rank runs the same number of (collective) steps
+                import torch.distributed as dist
+
+                flag = torch.tensor([0.0 if live else 1.0], device=dev)
+                dist.all_reduce(flag)
+                live = float(flag.item()) == 0.0
+            if live:
+                break
+            step()
+            torch.cuda.synchronize(dev)
+        barrier()
+        clk.mark()
         e0.record(stream)
         for _ in range(args.steps):
             step()
