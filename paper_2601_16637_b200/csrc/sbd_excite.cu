@@ -325,17 +325,59 @@ static int build_sell(sbd_ctx *ctx, Sector &s) {
     const uint32_t null_ent = (uint32_t)chunk << pbits;
     std::vector<uint32_t> ent((size_t)total + 4, null_ent);
     std::vector<int32_t> col((size_t)groups * 32 + 1, -1), go((size_t)H * (groups + 1));
-    for (i64 p = 0; p < n; ++p) {
-        const i64 g = p / 32, l = p % 32;
-        const int32_t c = order[p];
-        std::vector<i64> fill(H, 0);
-        for (i64 k = off[c]; k < off[c + 1]; ++k) {
-            const i64 h = sc[k].tgt / chunk, jl = sc[k].tgt - h * chunk;
-            const i64 P = std::abs(sc[k].info) - 1, neg = sc[k].info < 0;
-            ent[goff[h * (groups + 1) + g] + 32 * fill[h] + l] = ((uint32_t)jl << pbits) | (uint32_t)(P + neg * ctx->ld_vpp);
-            ++fill[h];
+    // Slot assignment.  A position's singles may sit in its slots in any order (the
+    // sum is the same up to rounding), so each slot's 32 entries are chosen to
+    // spread the two shared-memory gathers of the task-0 inner loop -- x[jl] and
+    // the ERI row at (chunk + 2 + q) -- over the 16 64-bit banks of each half-warp:
+    // greedy, per half-warp and slot, the position's remaining entry whose two
+    // banks are least used so far.  Padding entries all read one address
+    // (broadcast, no conflict).
+    for (i64 p = 0; p < n; ++p) col[p] = order[p];
+    std::vector<std::vector<uint32_t>> rem(32);
+    for (i64 g = 0; g < groups; ++g) {
+        for (i64 h = 0; h < H; ++h) {
+            const i64 base = goff[h * (groups + 1) + g];
+            const i64 w = (goff[h * (groups + 1) + g + 1] - base) / 32;
+            if (w == 0) continue;
+            for (int l = 0; l < 32; ++l) {
+                rem[l].clear();
+                const i64 p = g * 32 + l;
+                if (p >= n) continue;
+                const int32_t c = order[p];
+                for (i64 k = off[c]; k < off[c + 1]; ++k) {
+                    if (sc[k].tgt / chunk != h) continue;
+                    const i64 jl = sc[k].tgt - h * chunk;
+                    const i64 P = std::abs(sc[k].info) - 1, neg = sc[k].info < 0;
+                    rem[l].push_back(((uint32_t)jl << pbits) | (uint32_t)(P + neg * ctx->ld_vpp));
+                }
+            }
+            for (i64 q = 0; q < w; ++q) {
+                for (int half = 0; half < 2; ++half) {
+                    int xb[16] = {0}, vb[16] = {0};
+                    for (int l = 16 * half; l < 16 * half + 16; ++l) {
+                        auto &r = rem[l];
+                        if (r.empty()) continue;
+                        size_t best = 0;
+                        int best_cost = 1 << 30;
+                        for (size_t t = 0; t < r.size(); ++t) {
+                            const uint32_t e = r[t];
+                            const int bx = (int)((e >> pbits) & 15), bv = (int)((chunk + 2 + (e & ((1u << pbits) - 1))) & 15);
+                            const int cost = 4 * std::max(xb[bx], vb[bv]) + xb[bx] + vb[bv];
+                            if (cost < best_cost) {
+                                best_cost = cost;
+                                best = t;
+                            }
+                        }
+                        const uint32_t e = r[best];
+                        r[best] = r.back();
+                        r.pop_back();
+                        ++xb[(e >> pbits) & 15];
+                        ++vb[(chunk + 2 + (e & ((1u << pbits) - 1))) & 15];
+                        ent[base + 32 * q + l] = e;
+                    }
+                }
+            }
         }
-        col[p] = c;
     }
     for (size_t i = 0; i < go.size(); ++i) go[i] = (int32_t)goff[i];
     s.sell_groups = groups;
