@@ -326,21 +326,43 @@ static int build_sell(sbd_ctx *ctx, Sector &s) {
     std::vector<uint32_t> ent((size_t)total + 4, null_ent);
     std::vector<int32_t> col((size_t)groups * 32 + 1, -1), go((size_t)H * (groups + 1));
     // Slot assignment.  A position's singles may sit in its slots in any order (the
-    // sum is the same up to rounding), so each slot's 32 entries are chosen to
+    // sum is the same up to rounding), so each slot's 32 entries can be chosen to
     // spread the two shared-memory gathers of the task-0 inner loop -- x[jl] and
-    // the ERI row at (chunk + 2 + q) -- over the 16 64-bit banks of each half-warp:
-    // greedy, per half-warp and slot, the position's remaining entry whose two
-    // banks are least used so far.  Padding entries all read one address
-    // (broadcast, no conflict).
+    // the ERI row at (chunk + 2 + q) -- over the 16 64-bit banks of each half-warp.
+    // Cost model: per half-warp and slot, a gather takes as many wavefronts as the
+    // most-loaded bank has DISTINCT addresses (equal addresses broadcast).  Per
+    // (group, chunk) the table keeps the better of the enumeration order (often
+    // well spread and broadcast-friendly for structured string sets) and a greedy
+    // assignment (per lane, the remaining entry that adds the fewest wavefronts).
     for (i64 p = 0; p < n; ++p) col[p] = order[p];
-    std::vector<std::vector<uint32_t>> rem(32);
+    const uint32_t qmask = (1u << pbits) - 1u;
+    auto xaddr = [&](uint32_t e) { return (i64)(e >> pbits); };
+    auto vaddr = [&](uint32_t e) { return chunk + 2 + (i64)(e & qmask); };
+    struct BankSet {  // distinct addresses per 64-bit bank
+        std::vector<i64> a[16];
+        int load(i64 addr) const {
+            const auto &v = a[addr & 15];
+            return (int)v.size() + (std::find(v.begin(), v.end(), addr) == v.end() ? 1 : 0);
+        }
+        void add(i64 addr) {
+            auto &v = a[addr & 15];
+            if (std::find(v.begin(), v.end(), addr) == v.end()) v.push_back(addr);
+        }
+        int maxload() const {
+            size_t m = 0;
+            for (const auto &v : a) m = std::max(m, v.size());
+            return (int)m;
+        }
+    };
+    std::vector<std::vector<uint32_t>> rem(32), nat(32);
+    std::vector<uint32_t> slots;
     for (i64 g = 0; g < groups; ++g) {
         for (i64 h = 0; h < H; ++h) {
             const i64 base = goff[h * (groups + 1) + g];
             const i64 w = (goff[h * (groups + 1) + g + 1] - base) / 32;
             if (w == 0) continue;
             for (int l = 0; l < 32; ++l) {
-                rem[l].clear();
+                nat[l].clear();
                 const i64 p = g * 32 + l;
                 if (p >= n) continue;
                 const int32_t c = order[p];
@@ -348,21 +370,36 @@ static int build_sell(sbd_ctx *ctx, Sector &s) {
                     if (sc[k].tgt / chunk != h) continue;
                     const i64 jl = sc[k].tgt - h * chunk;
                     const i64 P = std::abs(sc[k].info) - 1, neg = sc[k].info < 0;
-                    rem[l].push_back(((uint32_t)jl << pbits) | (uint32_t)(P + neg * ctx->ld_vpp));
+                    nat[l].push_back(((uint32_t)jl << pbits) | (uint32_t)(P + neg * ctx->ld_vpp));
                 }
             }
-            for (i64 q = 0; q < w; ++q) {
+            // enumeration order and its cost
+            slots.assign((size_t)32 * w, null_ent);
+            int cost_nat = 0;
+            for (i64 q = 0; q < w; ++q)
                 for (int half = 0; half < 2; ++half) {
-                    int xb[16] = {0}, vb[16] = {0};
+                    BankSet bx, bv;
+                    for (int l = 16 * half; l < 16 * half + 16; ++l)
+                        if (q < (i64)nat[l].size()) {
+                            bx.add(xaddr(nat[l][q]));
+                            bv.add(vaddr(nat[l][q]));
+                        }
+                    cost_nat += bx.maxload() + bv.maxload();
+                }
+            // greedy
+            for (int l = 0; l < 32; ++l) rem[l] = nat[l];
+            int cost_gr = 0;
+            for (i64 q = 0; q < w; ++q)
+                for (int half = 0; half < 2; ++half) {
+                    BankSet bx, bv;
                     for (int l = 16 * half; l < 16 * half + 16; ++l) {
                         auto &r = rem[l];
                         if (r.empty()) continue;
                         size_t best = 0;
                         int best_cost = 1 << 30;
                         for (size_t t = 0; t < r.size(); ++t) {
-                            const uint32_t e = r[t];
-                            const int bx = (int)((e >> pbits) & 15), bv = (int)((chunk + 2 + (e & ((1u << pbits) - 1))) & 15);
-                            const int cost = 4 * std::max(xb[bx], vb[bv]) + xb[bx] + vb[bv];
+                            const int lx = bx.load(xaddr(r[t])), lv = bv.load(vaddr(r[t]));
+                            const int cost = 4 * std::max(lx, lv) + lx + lv;
                             if (cost < best_cost) {
                                 best_cost = cost;
                                 best = t;
@@ -371,12 +408,17 @@ static int build_sell(sbd_ctx *ctx, Sector &s) {
                         const uint32_t e = r[best];
                         r[best] = r.back();
                         r.pop_back();
-                        ++xb[(e >> pbits) & 15];
-                        ++vb[(chunk + 2 + (e & ((1u << pbits) - 1))) & 15];
-                        ent[base + 32 * q + l] = e;
+                        bx.add(xaddr(e));
+                        bv.add(vaddr(e));
+                        slots[(size_t)32 * q + l] = e;
                     }
+                    cost_gr += bx.maxload() + bv.maxload();
                 }
-            }
+            const bool use_greedy = cost_gr < cost_nat;
+            for (i64 q = 0; q < w; ++q)
+                for (int l = 0; l < 32; ++l)
+                    ent[base + 32 * q + l] = use_greedy ? slots[(size_t)32 * q + l]
+                                                        : (q < (i64)nat[l].size() ? nat[l][q] : null_ent);
         }
     }
     for (size_t i = 0; i < go.size(); ++i) go[i] = (int32_t)goff[i];
