@@ -62,14 +62,17 @@ def _worker(rank, world, port, case, q, exchange="auto"):
         q.put((rank, "error", traceback.format_exc()))
 
 
-@pytest.mark.parametrize("world,case,exchange", [(2, (10, 5, 5, 60, 50, 3, 1), "allgather"),
-                                                 (3, (12, 4, 5, 100, 91, 4, 2), "allgather"),
-                                                 (3, (12, 4, 5, 100, 91, 4, 2), "sparse"),
-                                                 (2, (16, 4, 4, 300, 40, 5, 1), "sparse")])
-def test_partitioned_sigma_and_davidson_match_single_gpu(world, case, exchange):
+@pytest.mark.parametrize("world,case,exchange,order", [(2, (10, 5, 5, 60, 50, 3, 1), "allgather", "auto"),
+                                                       (3, (12, 4, 5, 100, 91, 4, 2), "allgather", "auto"),
+                                                       (3, (12, 4, 5, 100, 91, 4, 2), "sparse", "auto"),
+                                                       (2, (16, 4, 4, 300, 40, 5, 1), "sparse", "auto"),
+                                                       (3, (12, 4, 5, 100, 91, 4, 2), "allgather", "additive")])
+def test_partitioned_sigma_and_davidson_match_single_gpu(world, case, exchange, order, monkeypatch):
     from paper_2601_16637_b200 import DavidsonOptions, HamiltonianApplier, davidson_solve
     from paper_2601_16637_b200.synth import random_integrals, random_product_basis
 
+    if order == "additive":  # task 0 added after the alpha side on every rank's row window
+        monkeypatch.setenv("SBD_CROSS_ADD", "1")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
