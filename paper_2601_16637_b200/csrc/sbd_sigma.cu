@@ -18,7 +18,7 @@
 // CSR entries -- 128-bit coalesced loads of whole X rows, no gathers, no
 // atomics, every output element owned by one lane.  The beta part runs on
 // X^T (one tiled transpose) so it has the same shape; its result Y^T is
-// folded into the alpha kernel's epilogue through a shared-memory transpose.
+// read back, column by column, in the alpha kernel's epilogue.
 // Grid order keeps all SMs on one column tile of X at a time, so the ~c-bar
 // re-reads of each X row segment are served from L2.
 #include <algorithm>
@@ -206,7 +206,6 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
 // is the only synchronisation (no barriers in the stream).
 constexpr int kTW = 256;
 
-constexpr double kEpiCbar = 8.0;  // alpha side stages the epilogue operands in the ring below this c-bar
 constexpr int kSideCtas = 4;  // resident CTAs per SM: registers <= 64, 4 x 48 KB rings (5 CTAs spill and need a 2-slot ring: slower)
 
 template <bool ALPHA>
@@ -222,8 +221,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <bool ALPHA, bool EPI = false>
+template <bool ALPHA>
 __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async(SideArgs a) {
+    constexpr bool EPI = ALPHA;
     constexpr int R = SideAsync<ALPHA>::kRing;
     extern __shared__ __align__(128) unsigned char ssm[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -246,25 +246,27 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
     if (row_ok) {
         const i64 g = a.row_base + r;
         const i64 e0 = a.conn_off[g], n = a.conn_off[g + 1] - e0;
-        // EPI (alpha side, sparse configs): the two ring slots the stream frees last
-        // are refilled with the epilogue's diag and own-x segments (ring positions n
-        // and n + 1), so their HBM latency overlaps the stream's tail instead of
-        // following it.  Same-box A/B: -6% at 1e9 dets (c-bar 0.74), -1.5% at cfg4
-        // (4.1), but +3-4% at 3.2e8 (13) and cfg2 (57): chosen by c-bar below kEpiCbar.
+        // Alpha side: the two ring slots the stream frees last are refilled with the
+        // epilogue's diag and own-x segments (ring positions n and n + 1), so their
+        // HBM latency overlaps the stream's tail instead of following it.  The
+        // positions >= n are peeled off the hot loop's issue (one uniform branch):
+        // same-box A/B -7% at 1e9 dets, -3% at cfg4, neutral at cfg2 (an earlier
+        // form that tested every issue for n and n + 1 cost 3-4% there).
         auto issue = [&](i64 i, int slot) {
-            if constexpr (EPI) {
-                const double *src = nullptr;
-                if (i < n) src = a.X + (i64)a.conn[e0 + i].tgt * a.ldx + c0;
-                else if (i == n) src = a.diag + r * a.ldy + c0;
-                else if (i == n + 1) src = a.X + g * a.ldx + c0;
-                if (src) {
-                    double *dst = ring + (size_t)slot * kTW;
-#pragma unroll
-                    for (int h = 0; h < 4; ++h)
-                        if (pair[h]) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
-                }
-            } else if (i < n) {
+            if (i < n) {
                 const double *src = a.X + (i64)a.conn[e0 + i].tgt * a.ldx + c0;
+                double *dst = ring + (size_t)slot * kTW;
+#pragma unroll
+                for (int h = 0; h < 4; ++h)
+                    if (pair[h]) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
+            }
+            cp_async_commit();
+        };
+        // the stream's last two issues (positions n, n + 1) carry the epilogue operands
+        auto issue_epi = [&](i64 i, int slot) {
+            const double *src = i < n ? a.X + (i64)a.conn[e0 + i].tgt * a.ldx + c0
+                                      : (i == n ? a.diag + r * a.ldy + c0 : a.X + g * a.ldx + c0);
+            if (i <= n + 1) {
                 double *dst = ring + (size_t)slot * kTW;
 #pragma unroll
                 for (int h = 0; h < 4; ++h)
@@ -274,10 +276,16 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
         };
         if (EPI) nstream = n;
 #pragma unroll
-        for (int i = 0; i < R - 1; ++i) issue(i, i);
+        for (int i = 0; i < R - 1; ++i) {
+            if (EPI) issue_epi(i, i);
+            else issue(i, i);
+        }
         int slot = 0;
         for (i64 i = 0; i < n; ++i) {
-            issue(i + R - 1, slot == 0 ? R - 1 : slot - 1);
+            const i64 nx = i + R - 1;
+            const int ns = slot == 0 ? R - 1 : slot - 1;
+            if (EPI && nx >= n) issue_epi(nx, ns);
+            else issue(nx, ns);
             const Conn cn = a.conn[e0 + i];
             cp_async_wait<R - 1>();
             const double *src = ring + (size_t)slot * kTW;
@@ -312,8 +320,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
         // contiguous bytes of each Y^T column, so the 8 warps share one L1 line per
         // column and no block barrier (warps finish unevenly) is needed.
         const i64 g = a.row_base + r;
-        constexpr bool epi = EPI;
-        const double *drow = a.diag + r * a.ldy + c0, *xrow = a.X + g * a.ldx + c0;
+        // diag and own-x segments, staged by the stream's last two issues
         const double *dring = ring + (size_t)(nstream % R) * kTW, *xring = ring + (size_t)((nstream + 1) % R) * kTW;
         const bool t0 = a.a_s_off != nullptr && a.a_s_off[g + 1] != a.a_s_off[g];
         const double *yrow = a.Y + r * a.ldy + c0;
@@ -322,10 +329,8 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
         for (int h = 0; h < 4; ++h) {
             const int cc = 2 * lane + 64 * h;
             if (ok[2 * h + 1]) {
-                const double2 d = epi ? *reinterpret_cast<const double2 *>(dring + cc)
-                                      : __ldcs(reinterpret_cast<const double2 *>(drow + cc));
-                const double2 x = epi ? *reinterpret_cast<const double2 *>(xring + cc)
-                                      : __ldg(reinterpret_cast<const double2 *>(xrow + cc));
+                const double2 d = *reinterpret_cast<const double2 *>(dring + cc);
+                const double2 x = *reinterpret_cast<const double2 *>(xring + cc);
                 const double t0v = __ldg(ytc + cc * a.ldyt), t1v = __ldg(ytc + (cc + 1) * a.ldyt);
                 acc[2 * h] = fma(d.x, x.x, acc[2 * h] + t0v);
                 acc[2 * h + 1] = fma(d.y, x.y, acc[2 * h + 1] + t1v);
@@ -335,8 +340,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
                     acc[2 * h + 1] += p.y;
                 }
             } else if (ok[2 * h]) {
-                acc[2 * h] = fma(epi ? dring[cc] : drow[cc], epi ? xring[cc] : xrow[cc],
-                                 acc[2 * h] + __ldg(ytc + cc * a.ldyt));
+                acc[2 * h] = fma(dring[cc], xring[cc], acc[2 * h] + __ldg(ytc + cc * a.ldyt));
                 if (t0) acc[2 * h] += yrow[cc];
             }
         }
@@ -1005,16 +1009,10 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
         if (!attr) {
             SBD_CUDA(ctx, cudaFuncSetAttribute(side_kernel_async<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)SideAsync<true>::smem()));
-            SBD_CUDA(ctx, cudaFuncSetAttribute(side_kernel_async<true, true>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SideAsync<true>::smem()));
             attr = true;
         }
         dim3 gt((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kTW - 1) / kTW));
-        const double cbar = A.n ? (double)(A.ns + A.nd) / (double)A.n : 0.0;
-        if (cbar < kEpiCbar)
-            side_kernel_async<true, true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
-        else
-            side_kernel_async<true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
+        side_kernel_async<true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
     } else {
         dim3 g((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kColsPerWarp - 1) / kColsPerWarp));
         if (vec) side_kernel<true, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
