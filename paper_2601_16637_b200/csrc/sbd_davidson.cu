@@ -1577,11 +1577,7 @@ struct ResidL {
             TTA <= 32 * resid_epl(K)) {
             const size_t smem = smem_tma;
             const int nt = std::max(1, std::min<int>((int)((n + TTA - 1) / TTA), ctx->num_sms));
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(residual_tma<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-                attr = true;
-            }
+            (void)sbd_smem_attr((const void *)residual_tma<K, M>, ctx->device, 220 * 1024);  // launch errors surface below
             residual_tma<K, M><<<nt, kBlock, smem, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T,
                                                                  ldt, ctx->red.as<double>());
             return {nt, K + 1 + M};
@@ -1590,11 +1586,7 @@ struct ResidL {
             constexpr int TT = 512 / M;
             const int nt = tile_blocks(ctx, n, TT);
             const size_t smem = sizeof(double2) * (2 * kWarpsT * M * (TT / 2) + TT / 2);
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(residual_tile<K, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                attr = true;
-            }
+            (void)sbd_smem_attr((const void *)residual_tile<K, M>, ctx->device, smem);  // launch errors surface below
             residual_tile<K, M><<<nt, kBlock, smem, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag, delta, T,
                                                                   ldt, ctx->red.as<double>());
             return {nt, K + 1 + M};
@@ -1654,11 +1646,7 @@ struct GsL {
             const int TTA = tma_tile(k + 1);
             const size_t smem = 128 + sizeof(double) * 2 * (size_t)(k + 1) * TTA;
             const int nt = std::max(1, std::min<int>((int)((n + TTA - 1) / TTA), ctx->num_sms));
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(gs_tma<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-                attr = true;
-            }
+            SBD_CUDA(ctx, sbd_smem_attr((const void *)gs_tma<K>, ctx->device, 220 * 1024));
             gs_tma<K><<<nt, kBlock, smem, ctx->stream>>>(V, k, ldv, n, c, kdot, t, dst, scale, ctx->red.as<double>());
             finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, K + 1, kdot, K, kdot + 1, out);
             SBD_LAUNCHED(ctx, "gs_update");
@@ -1805,11 +1793,7 @@ int sbd_jacobi(sbd_ctx *ctx, const double *A, int k, int lda, double *evals, dou
     if (k < 1 || k > kJacMax) return sbd_fail(ctx, SBD_EINVAL, "jacobi size must be in [1, 64]");
     const int smem = (int)(sizeof(double) * (2 * kJacMax * (kJacMax + 1) + 4 * (kJacMax / 2)) +
                            sizeof(int) * 3 * kJacMax);
-    static bool attr_set = false;
-    if (!attr_set) {
-        SBD_CUDA(ctx, cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr_set = true;
-    }
+    SBD_CUDA(ctx, sbd_smem_attr((const void *)jacobi_kernel, ctx->device, (size_t)smem));
     jacobi_kernel<<<1, kJacThreads, smem, ctx->stream>>>(A, k, lda, evals, evecs, max_sweeps, info);
     SBD_LAUNCHED(ctx, "jacobi");
     return SBD_OK;

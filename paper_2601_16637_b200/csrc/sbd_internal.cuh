@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/sbd.h"
@@ -112,6 +115,20 @@ struct sbd_ctx {
     i64 own_hi() const { return row_hi < 0 ? sec[0].n : row_hi; }
     i64 own_rows() const { return own_hi() - own_lo(); }
 };
+
+// Dynamic shared memory above 48 KB must be opted into per kernel and per device
+// (a function attribute of the device's context): remember what each (kernel,
+// device) pair was given, so a second GPU in the same process is set up too.
+inline cudaError_t sbd_smem_attr(const void *func, int device, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, size_t> done;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = done.find({func, device});
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done[{func, device}] = bytes;
+    return e;
+}
 
 // error helpers (sbd_context.cu)
 int sbd_fail(sbd_ctx *ctx, int code, const std::string &msg);

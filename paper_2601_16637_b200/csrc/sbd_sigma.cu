@@ -819,12 +819,7 @@ int ensure_scratch(sbd_ctx *ctx) {
 
 template <int CPT, bool SENT>
 int launch_cross_tma(sbd_ctx *ctx, const CrossArgs &ca, size_t smem) {
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-        SBD_CUDA(ctx, cudaFuncSetAttribute(cross_kernel_tma<CPT, SENT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem));
-        smem_set = smem;
-    }
+    SBD_CUDA(ctx, sbd_smem_attr((const void *)cross_kernel_tma<CPT, SENT>, ctx->device, smem));
     cross_kernel_tma<CPT, SENT><<<(unsigned)ctx->num_sms, kCrossThreads, smem, ctx->stream>>>(ca);
     SBD_LAUNCHED(ctx, "cross_kernel_tma");
     return SBD_OK;
@@ -832,11 +827,7 @@ int launch_cross_tma(sbd_ctx *ctx, const CrossArgs &ca, size_t smem) {
 
 template <int CPT>
 int launch_cross_mc(sbd_ctx *ctx, const CrossArgs &ca, size_t smem) {
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
-        SBD_CUDA(ctx, cudaFuncSetAttribute(cross_kernel_mc<CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        smem_set = smem;
-    }
+    SBD_CUDA(ctx, sbd_smem_attr((const void *)cross_kernel_mc<CPT>, ctx->device, smem));
     cross_kernel_mc<CPT><<<(unsigned)ctx->num_sms, kCrossThreads, smem, ctx->stream>>>(ca);
     SBD_LAUNCHED(ctx, "cross_kernel_mc");
     return SBD_OK;
@@ -962,12 +953,7 @@ int launch_beta_side(sbd_ctx *ctx, const double *x_own, i64 r0, i64 r1) {
     a.J = A.J.as<double>();
     a.ldj = A.n;
     if (use_side_tma() && aligned16(a.X) && a.ldx % 2 == 0) {
-        static bool attr = false;
-        if (!attr) {
-            SBD_CUDA(ctx, cudaFuncSetAttribute(side_kernel_async<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)SideAsync<false>::smem()));
-            attr = true;
-        }
+        SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_async<false>, ctx->device, SideAsync<false>::smem()));
         a.tile0 = r0 / kTW;
         const i64 t1 = (r1 + kTW - 1) / kTW;
         dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)(t1 - a.tile0));
@@ -1005,12 +991,7 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
     a.a_s_off = (with_t0 && A.ns > 0 && B.ns > 0) ? A.s_off.as<int64_t>() : nullptr;
     const bool vec = (nb % 2 == 0) && aligned16(x_full) && aligned16(y) && (r0 % 2 == 0);
     if (vec && use_side_tma()) {
-        static bool attr = false;
-        if (!attr) {
-            SBD_CUDA(ctx, cudaFuncSetAttribute(side_kernel_async<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)SideAsync<true>::smem()));
-            attr = true;
-        }
+        SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_async<true>, ctx->device, SideAsync<true>::smem()));
         dim3 gt((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kTW - 1) / kTW));
         side_kernel_async<true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
     } else {
