@@ -91,8 +91,9 @@ struct sbd_ctx {
     Sector sec[2];
     i64 row_lo = 0, row_hi = -1;  // owned alpha rows (row_hi < 0: all)
     // scratch for sigma
-    DevBuf xt, yt;               // [n_beta][ld_t]
+    DevBuf xt, yt;               // [n_beta][ld_t]; yt blocked by 8 alpha rows when yt_blocked (sbd_sigma.cu)
     i64 ld_t = 0;
+    bool yt_blocked = false;
     DevBuf diag;                 // owned rows, cached
     bool diag_valid = false;
     DevBuf red;                  // reduction scratch

@@ -49,6 +49,10 @@ struct SideArgs {
     i64 ldyt;
     const int64_t *a_s_off;        // rows with alpha singles carry task 0 in Y (cross_kernel); null: no task 0
     i64 tile0;                     // first column tile (pipelined host path launches tile ranges)
+    // Y^T layout.  false: [n_beta][ld_t] (alpha row contiguous).  true (blocked): blocks of 8
+    // alpha rows, [ld_t / 8][n_beta][8] -- the alpha CTA's 8 rows x 256 columns are one
+    // contiguous 16 KB block instead of 256 scattered 64-byte pieces (L1-friendly reads)
+    bool ytb;
 };
 
 template <bool VEC>
@@ -144,7 +148,8 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
         {
             const int i = threadIdx.x >> 1, half = (threadIdx.x & 1) * 4;
             if (c0 + i < a.n_cols) {
-                const double2 *src = reinterpret_cast<const double2 *>(a.YT + (c0 + i) * a.ldyt + r0 + half);
+                const double2 *src = reinterpret_cast<const double2 *>(
+                    a.ytb ? a.YT + ((r0 >> 3) * a.n_cols + c0 + i) * 8 + half : a.YT + (c0 + i) * a.ldyt + r0 + half);
                 double2 u = src[0], v = src[1];
                 tile[i][half + 0] = u.x;
                 tile[i][half + 1] = u.y;
@@ -324,14 +329,16 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
         const double *dring = ring + (size_t)(nstream % R) * kTW, *xring = ring + (size_t)((nstream + 1) % R) * kTW;
         const bool t0 = a.a_s_off != nullptr && a.a_s_off[g + 1] != a.a_s_off[g];
         const double *yrow = a.Y + r * a.ldy + c0;
-        const double *ytc = a.YT + c0 * a.ldyt + r;
+        // Y^T[c0 + cc][r] = ytc[cc * yts]
+        const double *ytc = a.ytb ? a.YT + ((r >> 3) * a.n_cols + c0) * 8 + (r & 7) : a.YT + c0 * a.ldyt + r;
+        const i64 yts = a.ytb ? 8 : a.ldyt;
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
             const int cc = 2 * lane + 64 * h;
             if (ok[2 * h + 1]) {
                 const double2 d = *reinterpret_cast<const double2 *>(dring + cc);
                 const double2 x = *reinterpret_cast<const double2 *>(xring + cc);
-                const double t0v = __ldg(ytc + cc * a.ldyt), t1v = __ldg(ytc + (cc + 1) * a.ldyt);
+                const double t0v = __ldg(ytc + cc * yts), t1v = __ldg(ytc + (cc + 1) * yts);
                 acc[2 * h] = fma(d.x, x.x, acc[2 * h] + t0v);
                 acc[2 * h + 1] = fma(d.y, x.y, acc[2 * h + 1] + t1v);
                 if (t0) {
@@ -340,19 +347,29 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
                     acc[2 * h + 1] += p.y;
                 }
             } else if (ok[2 * h]) {
-                acc[2 * h] = fma(dring[cc], xring[cc], acc[2 * h] + __ldg(ytc + cc * a.ldyt));
+                acc[2 * h] = fma(dring[cc], xring[cc], acc[2 * h] + __ldg(ytc + cc * yts));
                 if (t0) acc[2 * h] += yrow[cc];
             }
         }
     }
 
     if (row_ok) {
-        double *yr = a.Y + r * a.ldy + c0;
+        if (!ALPHA && a.ytb) {  // blocked Y^T: element (r, c) at ((c >> 3) * n_rows + r) * 8 + (c & 7)
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const int cc = 2 * lane + 64 * h;
-            if (ok[2 * h + 1]) __stcs(reinterpret_cast<double2 *>(yr + cc), make_double2(acc[2 * h], acc[2 * h + 1]));
-            else if (ok[2 * h]) yr[cc] = acc[2 * h];
+            for (int h = 0; h < 4; ++h) {
+                const i64 c = c0 + 2 * lane + 64 * h;
+                double *p = a.Y + ((c >> 3) * a.n_rows + r) * 8 + (c & 7);
+                if (ok[2 * h + 1]) __stcs(reinterpret_cast<double2 *>(p), make_double2(acc[2 * h], acc[2 * h + 1]));
+                else if (ok[2 * h]) *p = acc[2 * h];
+            }
+        } else {
+            double *yr = a.Y + r * a.ldy + c0;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int cc = 2 * lane + 64 * h;
+                if (ok[2 * h + 1]) __stcs(reinterpret_cast<double2 *>(yr + cc), make_double2(acc[2 * h], acc[2 * h + 1]));
+                else if (ok[2 * h]) yr[cc] = acc[2 * h];
+            }
         }
     }
 }
@@ -768,6 +785,11 @@ __global__ void diag_kernel(i64 n_rows, i64 row_base, i64 nb, const u64 *__restr
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+bool yt_blocked_enabled() {  // SBD_YT_BLOCKED=0 keeps the row-contiguous Y^T layout (A/B)
+    const char *e = getenv("SBD_YT_BLOCKED");
+    return !(e && e[0] == '0');
+}
+
 bool use_side_tma() {  // SBD_SIDE_LDG=1 selects the register-staged stream (A/B measurements)
     const char *e = getenv("SBD_SIDE_LDG");
     return !(e && e[0] == '1');
@@ -955,12 +977,15 @@ int launch_beta_side(sbd_ctx *ctx, const double *x_own, i64 r0, i64 r1) {
     if (use_side_tma() && aligned16(a.X) && a.ldx % 2 == 0) {
         SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_async<false>, ctx->device, SideAsync<false>::smem()));
         a.tile0 = r0 / kTW;
+        a.ytb = yt_blocked_enabled();
+        ctx->yt_blocked = a.ytb;
         const i64 t1 = (r1 + kTW - 1) / kTW;
         dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)(t1 - a.tile0));
         side_kernel_async<false><<<g, kRowsPerCta * 32, SideAsync<false>::smem(), st>>>(a);
     } else {
         if (r0 != 0 || r1 != rows) return sbd_fail(ctx, SBD_EINVAL, "row-range beta side needs the aligned path");
         dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((rows + kColsPerWarp - 1) / kColsPerWarp));
+        ctx->yt_blocked = false;
         side_kernel<true, false><<<g, kRowsPerCta * 32, 0, st>>>(a);
     }
     SBD_LAUNCHED(ctx, "side_kernel<beta>");
@@ -985,7 +1010,8 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
     a.conn = A.conn.as<Conn>();
     a.J = B.J.as<double>();
     a.ldj = nb;
-    a.YT = ctx->yt.as<double>() + r0;
+    a.ytb = ctx->yt_blocked;  // the layout the beta side wrote
+    a.YT = ctx->yt.as<double>() + (a.ytb ? r0 * nb : r0);  // r0 is a multiple of 8 (kTW-aligned chunks)
     a.ldyt = ctx->ld_t;
     a.diag = ctx->diag.as<double>() + r0 * nb;
     a.a_s_off = (with_t0 && A.ns > 0 && B.ns > 0) ? A.s_off.as<int64_t>() : nullptr;
