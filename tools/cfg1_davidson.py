@@ -32,13 +32,19 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     sig_ms = e0.elapsed_time(e1) / 50
+    # first solve: includes the one-time loading of the Davidson kernels (CUDA lazy
+    # module loading); the second is the steady-state figure
+    t0 = time.perf_counter()
+    davidson_solve(app, app.diag_device)
+    torch.cuda.synchronize()
+    first = time.perf_counter() - t0
     t0 = time.perf_counter()
     res = davidson_solve(app, app.diag_device)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     ref = json.load(open(os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "cfg1_davidson.json")))
     print(json.dumps({"n_dets": app.n, "sigma_ms": sig_ms, "sigma_dets_per_s": app.n / sig_ms * 1e3,
-                      "davidson_s": wall, "iterations": res.stats.iterations, "energy": float(res.energies[0]),
+                      "davidson_s": wall, "davidson_first_call_s": first, "iterations": res.stats.iterations, "energy": float(res.energies[0]),
                       "reference_energy": ref["energy"], "abs_diff": abs(float(res.energies[0]) - ref["energy"]),
                       "reference_s": ref["seconds"], "reference_iterations": ref["iterations"]}, indent=1))
 
