@@ -4,11 +4,18 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...     (N > 1: one rank per GPU, NCCL)
 
+With --gpus N > 1 and no torchrun environment (WORLD_SIZE unset), bench.py
+re-launches itself under ``python -m torch.distributed.run`` with N ranks on
+127.0.0.1 and forwards rank 0's line.  --share-gpu puts every rank on cuda:0
+(functional runs on a one-GPU box: NCCL then uses its socket transport, so
+the numbers are not NVLink numbers).
+
 A *step* is one sigma build y = H x over the whole determinant space of the
 workload (BASELINE configs[1]: 26 orbitals, 7a7b, 1e4 x 1e4 random strings =
 1e8 determinants).  At N > 1 the same 1e8-det system is partitioned by alpha
-blocks (configs[2], strong scaling): every step all-gathers x over NCCL,
-overlapped with the local beta-beta work.  x (800 MB) is larger than L2, so
+blocks (configs[2], strong scaling): every step runs the reference ring's
+exchange pattern over NCCL (libsbd_b200's own communicator), overlapped with
+the local beta-beta work and the alpha passes over blocks that have landed.  x (800 MB) is larger than L2, so
 no flush is needed between steps.
 
 Printed: one JSON line (rank 0) with the device-timed value, the roofline of
@@ -124,6 +131,29 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _spawn(args) -> int:
+    """--gpus N without a torchrun environment: re-run this script as N ranks (rank 0 prints)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
+def _share_gpu_env(rank: int) -> None:
+    """Several NCCL ranks on one GPU: distinct host ids make NCCL use its socket transport."""
+    os.environ.update(NCCL_HOSTID=f"sbd-bench-rank-{rank}", NCCL_SOCKET_IFNAME="lo", NCCL_IB_DISABLE="1")
 
 
 def _dist_env():
@@ -305,11 +335,18 @@ def run_ours(args):
     import torch
 
     world, rank, local = _dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch.distributed as dist
 
+        if args.share_gpu:
+            local = 0
+            _share_gpu_env(rank)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # torch's group carries the NCCL id and the max-over-ranks timings; the per-sigma
+        # traffic is libsbd_b200's own NCCL communicator
+        dist.init_process_group(args.backend, device_id=torch.device("cuda", local) if args.backend == "nccl" else None)
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -337,8 +374,8 @@ def run_ours(args):
         cbar, bytes_total = app.sigma_model()
         ctx = app.context
     else:
-        dapp = DistributedApplier(basis, table, device=dev.index)
-        app = dapp.engine.app
+        dapp = DistributedApplier(basis, table, device=dev.index, exchange=args.exchange, group_steps=args.group_steps)
+        app = None
         n_own = dapp.n_own
         lo = dapp.lo
         x_own = torch.empty(n_own, dtype=torch.float64, device=dev)
@@ -347,9 +384,13 @@ def run_ours(args):
         def step():
             dapp.apply_device(x_own, y_own)
 
-        cbar, _ = app.sigma_model()
+        import ctypes
+
+        cb, by = ctypes.c_double(), ctypes.c_double()
+        dapp.engine.context("sbd_sigma_model", ctypes.byref(cb), ctypes.byref(by))
+        cbar = cb.value
         bytes_total = 8.0 * n * (3.0 + cbar)
-        ctx = app.context
+        ctx = dapp.engine.context
     torch.cuda.synchronize(dev)
     setup_s = time.perf_counter() - t_setup
     gen = torch.Generator(device=dev).manual_seed(12345 + rank)
@@ -402,6 +443,26 @@ def run_ours(args):
     achieved = bytes_rank / t_step / 1e9
     traffic, traffic_rec = _traffic()
     kernels = {}
+    overlap = None
+    if world > 1:  # a separate profiled pass (events per ring-step group): exposed communication
+        dapp.profile(True)
+        for _ in range(max(3, min(args.steps, 10))):
+            step()
+        torch.cuda.synchronize(dev)
+        rep_ = dapp.overlap_report()
+        dapp.profile(False)
+        info = dapp.engine.info()
+        overlap = {"sigma_ms": rep_.sigma_s * 1e3, "overlap_ratio": rep_.overlap_ratio,
+                   "exposed_ms_per_sigma": rep_.total_exposed_s * 1e3,
+                   "transfer_ms_per_sigma": rep_.total_transfer_s * 1e3,
+                   "compute_ms_per_sigma": rep_.total_compute_s * 1e3,
+                   "per_step_ms": [[st, c * 1e3, t * 1e3, e * 1e3, r] for st, c, t, e, r in rep_.per_step],
+                   "per_step_columns": ["step (0 = local, g = ring-step group)", "compute", "transfer", "exposed",
+                                        "ratio"],
+                   "exchange": dapp.exchange, "group_steps": args.group_steps,
+                   "recv_bytes_per_sigma_rank0": 8 * info["recv_rows"] * nb,
+                   "needed_fraction": info["needed_fraction"], "sigmas_profiled": rep_.n_sigma,
+                   "note": "profiled run, separate from the timed region"}
     if world == 1:
         from paper_2601_16637_b200 import _lib
 
@@ -455,7 +516,10 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         t_e2e = _max_over_ranks(e0.elapsed_time(e1) / 1e3 / reps, world, dev)
         e2e = {"value": n / t_e2e, "unit": "dets/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
-               "ms_per_step": t_e2e * 1e3, "path": "DistributedApplier.apply_device with per-rank pinned H2D/D2H"}
+               "h2d_bytes_per_rank": 8 * n_own, "d2h_bytes_per_rank": 8 * n_own,
+               "ms_per_step": t_e2e * 1e3,
+               "path": "DistributedApplier.apply_device, each rank copying its own rows (pinned H2D/D2H); "
+                       "bytes_per_step are whole-job totals"}
 
     # ---- device-resident Davidson, reference defaults ------------------------------------
     dav = None
@@ -490,7 +554,11 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_explicit:
         expl = explicit_bench(table, a, b, dev, stream, args, with_cpu=not args.no_cpu)
 
-    launches_per_step = 4  # transpose, beta side, task-0 cross, alpha side
+    if world == 1:
+        launches_per_step = 4  # transpose, beta side, task-0 cross, alpha side
+    else:  # transpose, beta side, own-rows alpha pass, one pass per ring-step group, task 0 (+ sparse packs)
+        ng = -(-(world - 1) // max(1, args.group_steps))
+        launches_per_step = 4 + ng + ((world - 1) if dapp.exchange == "sparse" else 0)
     line = {
         "metric": METRIC, "value": value, "unit": "dets/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": t_step * 1e3, "higher_is_better": True,
@@ -506,6 +574,7 @@ def run_ours(args):
                      "per_kernel_ncu": (traffic_rec or {}).get("per_kernel"),
                      "ncu_source": (traffic_rec or {}).get("source")},
         "kernels": kernels,
+        "overlap": overlap,
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
@@ -533,10 +602,41 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-explicit", action="store_true")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="torch.distributed backend for setup and timing reductions (N > 1)")
+    ap.add_argument("--share-gpu", action="store_true", help="all ranks on cuda:0 (functional runs on one GPU)")
+    ap.add_argument("--exchange", choices=["auto", "dense", "sparse"], default="auto")
+    ap.add_argument("--group-steps", type=int, default=2, help="ring steps per pipelined alpha pass")
+    ap.add_argument("--dry-run", action="store_true", help="start the ranks and report them, no GPU work")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _spawn(args)
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
+
+
+def run_dry(args):
+    """Launch check: every rank joins the group; rank 0 prints the world it saw."""
+    world, rank, _ = _dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    ranks = [0]
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        dist.init_process_group(args.backend)
+        t = torch.tensor([float(rank)])
+        dist.all_reduce(t)
+        ranks = [int(t.item())]
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "n_gpus": world, "dry_run": True, "rank_sum": ranks[0],
+                          "backend": args.backend}), flush=True)
+    return 0
 
 
 if __name__ == "__main__":

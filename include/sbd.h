@@ -126,9 +126,59 @@ int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full_dev, double *y_dev);
  * davidson.py:242). */
 int sbd_sigma_host(sbd_ctx *ctx, const double *x_full_host, double *y_host);
 
+/* Independent dense check rows (verify's matrix; oracle.assemble_dense, oracle.py:34-45):
+ * out[r * N + j] = <det(row0 + r)|H|det(j)> for r < nrows, every element evaluated
+ * from the two determinants' words (_hij_words, apply.py:152-177) -- no tables,
+ * no sigma kernels.  Needs only sbd_set_integrals + strings (or sbd_set_dets). */
+int sbd_dense_rows(sbd_ctx *ctx, int64_t row0, int64_t nrows, double *out_dev);
+
 /* Mean in-set alpha connections per alpha string (c-bar)
  * and the algorithmic sigma bytes 8*N_own*(3 + c-bar). */
 int sbd_sigma_model(sbd_ctx *ctx, double *cbar_alpha, double *bytes_per_sigma);
+
+/* ---- Multi-GPU: alpha-block partition, one context (process) per GPU ----
+ * Replaces DistributedApplier (distsim.py:130-316) and its ring
+ * (distsim.py:200-259) with NCCL over NVLink/NVSwitch, resolved at run time
+ * from libnccl.so.2 (the already-loaded one inside PyTorch processes).
+ *
+ *   sbd_nccl_unique_id  -- rank 0 makes the 128-byte id; the caller broadcasts it
+ *                          (ncclGetUniqueId);
+ *   sbd_dist_init       -- collective: joins the communicator and takes the
+ *                          make_partition block of `rank` (distsim.py:63-77),
+ *                          or block `rank` of the caller's alpha_edges, as
+ *                          the row window.  Call after sbd_set_strings, before
+ *                          (or after) sbd_build_tables.  nranks = 1 needs no id;
+ *   sbd_dist_plan       -- collective, optional (sbd_sigma_dist plans with the
+ *                          defaults 0, 0.6, 2): exchange 0 auto / 1 dense (whole
+ *                          blocks) / 2 sparse (only the referenced rows; auto picks
+ *                          sparse when the largest referenced fraction of remote
+ *                          rows is <= sparse_threshold); group_steps ring steps
+ *                          per pipelined alpha pass;
+ *   sbd_sigma_dist      -- collective: y_own = (H x)[own rows] from x_own (this
+ *                          rank's rows only), exchange overlapped with the beta
+ *                          side and the passes over already-landed blocks;
+ *   sbd_dist_allreduce  -- in-place all-reduce of n device doubles (0 sum, 1 max,
+ *                          2 min) on the context's stream;
+ *   sbd_dist_check      -- NCCL asynchronous error -> SBD_ECUDA;
+ *   sbd_dist_info       -- partition and plan (recv/send rows per sigma);
+ *   sbd_dist_set_profiling / sbd_dist_stats -- per ring step (0 = local work,
+ *                          g = group g) compute / transfer / exposed device
+ *                          milliseconds summed over the profiled sigmas
+ *                          (StepStat / overlap_stats, distsim.py:81-88,340-367).
+ * sbd_davidson on a partitioned context solves over the rank's rows with the
+ * dot products all-reduced (every rank calls it; x0 / evecs are local rows). */
+int sbd_nccl_unique_id(char *id_out /* 128 bytes */);
+int sbd_dist_init(sbd_ctx *ctx, int rank, int nranks, const char *id /* 128 bytes */,
+                  const int64_t *alpha_edges /* nranks + 1 block edges, or NULL: make_partition */);
+int sbd_dist_plan(sbd_ctx *ctx, int exchange, double sparse_threshold, int group_steps);
+int sbd_sigma_dist(sbd_ctx *ctx, const double *x_own_dev, double *y_own_dev);
+int sbd_dist_allreduce(sbd_ctx *ctx, double *buf_dev, int64_t n, int op);
+int sbd_dist_check(sbd_ctx *ctx);
+int sbd_dist_info(sbd_ctx *ctx, int *rank, int *nranks, int64_t *alpha_lo, int64_t *alpha_hi, int *sparse,
+                  double *needed_fraction, int64_t *recv_rows, int64_t *send_rows, int *n_groups);
+int sbd_dist_set_profiling(sbd_ctx *ctx, int on);
+int sbd_dist_stats(sbd_ctx *ctx, int64_t *n_sigma, int *n_steps, double *compute_ms, double *transfer_ms,
+                   double *exposed_ms, double *total_ms);
 
 /* ---- Davidson building blocks (davidson.py), all device-resident ---- */
 
@@ -230,8 +280,8 @@ typedef struct sbd_davidson_stats {
 int sbd_davidson_default_opts(sbd_davidson_opts *opts);
 
 /* Lowest n_roots eigenpairs of the context's Hamiltonian (product or explicit
- * basis; all rows must be owned -- multi-GPU solves go through the Python
- * DistributedApplier).  diag_dev: the preconditioner's diagonal (N doubles) or
+ * basis; all rows owned, or a partitioned context from sbd_dist_init, where
+ * every rank calls it and vectors are the rank's rows).  diag_dev: the preconditioner's diagonal (N doubles) or
  * NULL for the context's own H_ii (sbd_diag).  x0_dev: start vector (N doubles, normalised inside) or
  * NULL for e_argmin(diag) (davidson.py:219-227).  evals_host / res_norms_host:
  * n_roots doubles; evecs_dev: n_roots rows of ldu doubles (may be NULL).

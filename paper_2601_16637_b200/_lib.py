@@ -57,6 +57,16 @@ _SIGS = {
     "sbd_rotate": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _c_int],
     "sbd_combine": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _c_int, _vp, _c_i64],
     "sbd_jacobi": [_vp, _vp, _c_int, _c_int, _vp, _vp, _c_int, _vp],
+    "sbd_dense_rows": [_vp, _c_i64, _c_i64, _vp],
+    "sbd_nccl_unique_id": [_vp],
+    "sbd_dist_init": [_vp, _c_int, _c_int, _vp, _vp],
+    "sbd_dist_plan": [_vp, _c_int, _c_dbl, _c_int],
+    "sbd_sigma_dist": [_vp, _vp, _vp],
+    "sbd_dist_allreduce": [_vp, _vp, _c_i64, _c_int],
+    "sbd_dist_check": [_vp],
+    "sbd_dist_info": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "sbd_dist_set_profiling": [_vp, _c_int],
+    "sbd_dist_stats": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "sbd_davidson_default_opts": [_vp],
     "sbd_davidson": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _vp],
 }
@@ -125,6 +135,13 @@ def ptr(x) -> int:
     if isinstance(x, np.ndarray):
         return x.ctypes.data
     return x.data_ptr()
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (``sbd_nccl_unique_id``) for ``sbd_dist_init``."""
+    buf = ctypes.create_string_buffer(128)
+    check(load().sbd_nccl_unique_id(buf), None, "sbd_nccl_unique_id")
+    return buf.raw
 
 
 def call(name: str, *args, ctx=None):

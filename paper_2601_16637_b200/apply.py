@@ -236,6 +236,12 @@ class HamiltonianApplier:
 
         if x.dtype != torch.float64 or not x.is_cuda or x.numel() != self.n:
             raise ValueError(f"expected a CUDA float64 vector of length {self.n}")
+        if x.device != self._torch_device:
+            raise ValueError(f"x is on {x.device}, the applier on {self._torch_device}")
+        if out is not None and (out.dtype != torch.float64 or out.device != self._torch_device
+                                or out.numel() != self.n_own or not out.is_contiguous()):
+            raise ValueError(f"out must be a contiguous float64 tensor of {self.n_own} elements on "
+                             f"{self._torch_device}")
         self.apply_count += 1
         x = x.contiguous()
         y = torch.empty(self.n_own, dtype=torch.float64, device=x.device) if out is None else out

@@ -85,6 +85,7 @@ int sbd_destroy(sbd_ctx *ctx) {
         cudaStreamDestroy(ctx->copy_stream);
     }
     for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
+    sbd_dist_release(ctx);
     delete ctx;
     return SBD_OK;
 }
@@ -198,6 +199,7 @@ int sbd_build_tables(sbd_ctx *ctx) {
         if (rc) return rc;
     }
     ctx->diag_valid = false;
+    ctx->dist.planned = false;  // the exchange plan is built from the alpha table
     SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SBD_OK;
 }
@@ -252,6 +254,8 @@ int sbd_set_row_window(sbd_ctx *ctx, int64_t lo, int64_t hi) {
     SBD_CHECK_CTX(ctx);
     if (!ctx->sec[0].present) return sbd_fail(ctx, SBD_EINVAL, "alpha strings not set");
     if (ctx->explicit_mode) return sbd_fail(ctx, SBD_EINVAL, "row windows apply to product-mode bases only");
+    if (ctx->dist.on && ctx->dist.nranks > 1)
+        return sbd_fail(ctx, SBD_EINVAL, "the row window of a distributed context is its partition block");
     if (!(0 <= lo && lo <= hi && hi <= ctx->sec[0].n))
         return sbd_fail(ctx, SBD_EINVAL, "alpha window (" + std::to_string(lo) + ", " + std::to_string(hi) +
                                              ") exceeds basis");

@@ -1452,22 +1452,18 @@ inline bool vec_ok(const double *V, i64 ldv, const double *p, P... rest) {
     return al16(p) && vec_ok(V, ldv, rest...);
 }
 
+// Pass variants (read per launch, so tests can select each one in-process; tests/test_gpu_kernels.py):
+//   default      k <= 32: register passes (residual_reg, gs_reg, mix_reg); k > 32: TMA-staged passes
+//   SBD_DAV_TMA=1  TMA-staged passes for every k
+//   SBD_NO_TMA=1   no TMA: tile / generic passes
 inline bool use_tma() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SBD_NO_TMA");
-        v = (e && *e && *e != '0') ? 0 : 1;
-    }
-    return v == 1;
+    const char *e = getenv("SBD_NO_TMA");
+    return !(e && *e && *e != '0');
 }
 
-inline bool use_reg() {  // SBD_DAV_TMA=1 selects the TMA-staged passes (A/B measurements)
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("SBD_DAV_TMA");
-        v = (e && *e == '1') ? 0 : 1;
-    }
-    return v == 1;
+inline bool use_reg() {
+    const char *e = getenv("SBD_DAV_TMA");
+    return !(e && *e == '1');
 }
 
 // lanes per element pair for pass `which` (0 residual, 1 CGS); SBD_RES_SPLIT / SBD_GS_SPLIT

@@ -69,6 +69,42 @@ struct Sector {
     bool built = false;
 };
 
+// Alpha-block partition over ranks (sbd_dist.cu): NCCL communicator, the
+// exchange plan and the pipelined pass schedule of sbd_sigma_dist.
+//   x_work rows: segment 0 = the rank's own alpha rows, segment s (1..P-1) =
+//   the rows needed from peer (rank - s) mod P, received at ring step s.  The
+//   own rows' alpha connections are remapped to x_work rows and sorted by
+//   that row, so the connections of one segment are one contiguous range
+//   (seg_off[row * (P + 1) + s] .. [s + 1]) and a pass over the segments of
+//   the steps that have landed is one contiguous range per row.
+struct DistState {
+    bool on = false;
+    int rank = 0, nranks = 1;
+    void *comm = nullptr;             // ncclComm_t
+    cudaStream_t cs = nullptr;        // exchange stream
+    std::vector<i64> blk;             // make_partition edges, P + 1
+    bool planned = false;
+    int sparse = 0;                   // 1: only referenced rows travel
+    int group_steps = 2;              // ring steps per pipelined pass
+    double needed_fraction = 1.0;     // max over ranks of (referenced remote rows / remote rows)
+    std::vector<i64> seg_start;       // P + 1 (x_work row of each segment, last = work rows)
+    std::vector<i64> recv_cnt;        // rows received at step s (s = 1..P-1), index s
+    std::vector<i64> send_cnt, send_off;  // rows sent at step s to (rank + s) mod P, offsets in send_rows
+    DevBuf xw;                        // x_work [work rows][n_beta]
+    DevBuf conn;                      // own rows' Conn, remapped + sorted per row
+    DevBuf seg_off;                   // i64[rows][P + 1]
+    DevBuf sconn;                     // copy of alpha sconn, own entries remapped
+    DevBuf send_rows, send_buf;       // sparse: local rows to pack per step, packed rows
+    std::vector<cudaEvent_t> ev;      // sync events (one per group + start)
+    // profiling (sbd_dist_set_profiling): timing events per group, accumulated per sigma
+    bool profile = false;
+    std::vector<cudaEvent_t> tev;
+    bool tev_pending = false;
+    i64 n_sigma = 0;
+    std::vector<double> compute_ms, transfer_ms, exposed_ms;  // per step (0 = local, g = group g)
+    double total_ms = 0.0;
+};
+
 // device ingestion results (sbd_ingest.cu), first-seen order
 struct IngestState {
     DevBuf det_a, det_b, det_count, alpha, beta;
@@ -111,6 +147,7 @@ struct sbd_ctx {
     DevBuf grp_b, grp_perm;      // int32[n_det]: sorted B and caller index
     bool explicit_built = false;
     IngestState ingest;
+    DistState dist;
 
     i64 own_lo() const { return row_lo; }
     i64 own_hi() const { return row_hi < 0 ? sec[0].n : row_hi; }
@@ -163,6 +200,17 @@ int sbd_radix_sort(sbd_ctx *ctx, const u64 *keys, i64 n, int key_bits, DevBuf &s
 int sbd_build_explicit_index(sbd_ctx *ctx);                 // sbd_explicit.cu
 int sbd_explicit_diag(sbd_ctx *ctx, double *out);           // sbd_explicit.cu
 int sbd_explicit_sigma(sbd_ctx *ctx, const double *x, double *y);  // sbd_explicit.cu
+// sigma building blocks used by the partitioned sigma (sbd_sigma.cu)
+int sbd_require_sigma_ready(sbd_ctx *ctx);                  // tables built, scratch + diag ready
+int sbd_beta_side(sbd_ctx *ctx, const double *x_own);      // transpose + beta stream of the owned rows
+// alpha stream over the connections seg_off[row*stride + s_lo] .. [row*stride + s_hi] of each owned row;
+// epi: + diag o x + (B X^T)^T, y written; acc_in: y += (no epilogue)
+int sbd_alpha_pass(sbd_ctx *ctx, const double *X, double *y, const Conn *conn, const int64_t *seg_off, i64 stride,
+                   int s_lo, int s_hi, i64 xo_row0, bool epi, bool acc_in);
+int sbd_cross_add(sbd_ctx *ctx, const double *X, double *y, const SConn *sconn);  // y += task 0
+void sbd_dist_release(sbd_ctx *ctx);                        // sbd_dist.cu (called by sbd_destroy)
+int sbd_dist_allreduce_internal(sbd_ctx *ctx, double *buf, i64 n, int op);  // 0 sum, 1 max, 2 min; no-op on 1 rank
+int sbd_dist_check_internal(sbd_ctx *ctx);                  // NCCL asynchronous error -> SBD_ECUDA
 
 // x rows of up to kSellWhole strings are staged whole (H = 1, cluster kernel);
 // longer rows in chunks of at most kSellChunk strings (28 KB)

@@ -53,6 +53,13 @@ struct SideArgs {
     // alpha rows, [ld_t / 8][n_beta][8] -- the alpha CTA's 8 rows x 256 columns are one
     // contiguous 16 KB block instead of 256 scattered 64-byte pieces (L1-friendly reads)
     bool ytb;
+    // partitioned passes (DIST kernels, sbd_alpha_pass): local row r streams the connections
+    // seg_off[r * seg_stride + seg_lo] .. seg_off[r * seg_stride + seg_hi] of `conn`; its own x
+    // row is X[xo_row0 + r]; epi adds diag o x + (B X^T)^T and writes y, acc_in adds onto y
+    const int64_t *seg_off;
+    i64 seg_stride, xo_row0;
+    int seg_lo, seg_hi;
+    bool epi, acc_in;
 };
 
 template <bool VEC>
@@ -81,7 +88,7 @@ __device__ __forceinline__ void load4(const double *__restrict__ row, i64 c0, in
     }
 }
 
-template <bool VEC, bool ALPHA>
+template <bool VEC, bool ALPHA, bool DIST = false>
 __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const i64 r = (i64)blockIdx.x * kRowsPerCta + w;
@@ -94,7 +101,8 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
 
     if (row_ok) {
         const i64 g = a.row_base + r;
-        const i64 e0 = a.conn_off[g], e1 = a.conn_off[g + 1];
+        const i64 e0 = DIST ? a.seg_off[r * a.seg_stride + a.seg_lo] : a.conn_off[g];
+        const i64 e1 = DIST ? a.seg_off[r * a.seg_stride + a.seg_hi] : a.conn_off[g + 1];
         i64 e = e0;
         // batches of 4 connections: 8 independent 128-bit loads in flight per lane
         for (; e + 4 <= e1; e += 4) {
@@ -141,7 +149,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
         }
     }
 
-    if (ALPHA) {
+    if (ALPHA && (!DIST || a.epi)) {  // uniform per launch: every thread reaches the barrier
         // + (B X^T)^T : tile YT[c0:c0+128, r0:r0+8] through shared memory
         __shared__ double tile[kColsPerWarp][kRowsPerCta + 1];
         const i64 r0 = (i64)blockIdx.x * kRowsPerCta;
@@ -168,7 +176,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
             // diagonal term (apply.py:217)
             double dv[4], xo[4];
             load4<VEC>(a.diag + r * a.ldy, c0, lane, ok, dv);
-            load4<VEC>(a.X + g * a.ldx, c0, lane, ok, xo);
+            load4<VEC>(a.X + (DIST ? a.xo_row0 + r : g) * a.ldx, c0, lane, ok, xo);
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[j] = fma(dv[j], xo[j], acc[j]);
             // task 0, already in Y for rows with alpha singles (cross_kernel)
@@ -181,6 +189,12 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
         }
     }
 
+    if (DIST && a.acc_in && row_ok) {
+        double pv[4];
+        load4<VEC, false>(a.Y + r * a.ldy, c0, lane, ok, pv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] += pv[j];
+    }
     if (row_ok) {
         double *yr = a.Y + r * a.ldy;
         if (VEC) {
@@ -226,9 +240,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <bool ALPHA>
+template <bool ALPHA, bool DIST = false>
 __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async(SideArgs a) {
-    constexpr bool EPI = ALPHA;
+    const bool EPI = ALPHA && (!DIST || a.epi);  // uniform per launch
     constexpr int R = SideAsync<ALPHA>::kRing;
     extern __shared__ __align__(128) unsigned char ssm[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -250,7 +264,9 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
     i64 nstream = 0;
     if (row_ok) {
         const i64 g = a.row_base + r;
-        const i64 e0 = a.conn_off[g], n = a.conn_off[g + 1] - e0;
+        const i64 own = DIST ? a.xo_row0 + r : g;  // this row's own x row in X
+        const i64 e0 = DIST ? a.seg_off[r * a.seg_stride + a.seg_lo] : a.conn_off[g];
+        const i64 n = (DIST ? a.seg_off[r * a.seg_stride + a.seg_hi] : a.conn_off[g + 1]) - e0;
         // Alpha side: the two ring slots the stream frees last are refilled with the
         // epilogue's diag and own-x segments (ring positions n and n + 1), so their
         // HBM latency overlaps the stream's tail instead of following it.  The
@@ -270,7 +286,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
         // the stream's last two issues (positions n, n + 1) carry the epilogue operands
         auto issue_epi = [&](i64 i, int slot) {
             const double *src = i < n ? a.X + (i64)a.conn[e0 + i].tgt * a.ldx + c0
-                                      : (i == n ? a.diag + r * a.ldy + c0 : a.X + g * a.ldx + c0);
+                                      : (i == n ? a.diag + r * a.ldy + c0 : a.X + own * a.ldx + c0);
             if (i <= n + 1) {
                 double *dst = ring + (size_t)slot * kTW;
 #pragma unroll
@@ -320,7 +336,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
         cp_async_wait<0>();
     }
 
-    if (ALPHA && row_ok) {
+    if (EPI && row_ok) {
         // + (B X^T)^T: Y^T[c, r] read directly.  The CTA's 8 rows r0..r0+7 are 64
         // contiguous bytes of each Y^T column, so the 8 warps share one L1 line per
         // column and no block barrier (warps finish unevenly) is needed.
@@ -353,6 +369,20 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
         }
     }
 
+    if (DIST && a.acc_in && row_ok) {  // later pass of the partitioned sigma: add onto y
+        const double *yrow = a.Y + r * a.ldy + c0;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const int cc = 2 * lane + 64 * h;
+            if (ok[2 * h + 1]) {
+                const double2 p = __ldcs(reinterpret_cast<const double2 *>(yrow + cc));
+                acc[2 * h] += p.x;
+                acc[2 * h + 1] += p.y;
+            } else if (ok[2 * h]) {
+                acc[2 * h] += yrow[cc];
+            }
+        }
+    }
     if (row_ok) {
         if (!ALPHA && a.ytb) {  // blocked Y^T: element (r, c) at ((c >> 3) * n_rows + r) * 8 + (c & 7)
 #pragma unroll
@@ -887,7 +917,8 @@ bool cross_additive(const sbd_ctx *ctx) {
     return B.sell_groups > 0 && 2 * sell_nonzero_groups(B) < B.sell_groups;
 }
 
-int launch_cross(sbd_ctx *ctx, const double *x_full, double *y, bool additive = false) {
+int launch_cross(sbd_ctx *ctx, const double *x_full, double *y, bool additive = false,
+                 const SConn *sconn = nullptr) {
     const Sector &A = ctx->sec[0], &B = ctx->sec[1];
     CrossArgs ca{};
     ca.n_rows = ctx->own_rows();
@@ -896,7 +927,7 @@ int launch_cross(sbd_ctx *ctx, const double *x_full, double *y, bool additive = 
     ca.X = x_full;
     ca.Y = y;
     ca.a_s_off = A.s_off.as<int64_t>();
-    ca.a_sconn = A.sconn.as<SConn>();
+    ca.a_sconn = sconn ? sconn : A.sconn.as<SConn>();
     ca.a_row = A.s_row.as<int32_t>();
     ca.goff = B.sell_goff.as<int32_t>();
     ca.col = B.sell_col.as<int32_t>();
@@ -1011,7 +1042,9 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
     a.J = B.J.as<double>();
     a.ldj = nb;
     a.ytb = ctx->yt_blocked;  // the layout the beta side wrote
-    a.YT = ctx->yt.as<double>() + (a.ytb ? r0 * nb : r0);  // r0 is a multiple of 8 (kTW-aligned chunks)
+    // the blocked Y^T groups alpha rows by 8: a chunk must start on a block (kTW-aligned chunks do)
+    if (a.ytb && r0 % kRowsPerCta != 0) return sbd_fail(ctx, SBD_EINVAL, "alpha chunk start not a multiple of 8");
+    a.YT = ctx->yt.as<double>() + (a.ytb ? r0 * nb : r0);
     a.ldyt = ctx->ld_t;
     a.diag = ctx->diag.as<double>() + r0 * nb;
     a.a_s_off = (with_t0 && A.ns > 0 && B.ns > 0) ? A.s_off.as<int64_t>() : nullptr;
@@ -1029,6 +1062,50 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
     return SBD_OK;
 }
 
+// One pass of the partitioned alpha side (sbd_dist.cu): see SideArgs.seg_off.
+int launch_alpha_pass(sbd_ctx *ctx, const double *X, double *y, const Conn *conn, const int64_t *seg_off, i64 stride,
+                      int s_lo, int s_hi, i64 xo_row0, bool epi, bool acc_in) {
+    const Sector &B = ctx->sec[1];
+    const i64 nb = B.n, rows = ctx->own_rows();
+    if (rows <= 0 || nb == 0) return SBD_OK;
+    SideArgs a{};
+    a.n_rows = rows;
+    a.row_base = ctx->own_lo();
+    a.n_cols = nb;
+    a.col_base = 0;
+    a.X = X;
+    a.ldx = nb;
+    a.Y = y;
+    a.ldy = nb;
+    a.conn = conn;
+    a.J = B.J.as<double>();
+    a.ldj = nb;
+    a.ytb = ctx->yt_blocked;
+    a.YT = ctx->yt.as<double>();
+    a.ldyt = ctx->ld_t;
+    a.diag = ctx->diag.as<double>();
+    a.a_s_off = nullptr;  // task 0 is added after the last pass (sbd_cross_add)
+    a.seg_off = seg_off;
+    a.seg_stride = stride;
+    a.seg_lo = s_lo;
+    a.seg_hi = s_hi;
+    a.xo_row0 = xo_row0;
+    a.epi = epi;
+    a.acc_in = acc_in;
+    const bool vec = (nb % 2 == 0) && aligned16(X) && aligned16(y);
+    if (vec && use_side_tma()) {
+        SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_async<true, true>, ctx->device, SideAsync<true>::smem()));
+        dim3 gt((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kTW - 1) / kTW));
+        side_kernel_async<true, true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
+    } else {
+        dim3 g((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kColsPerWarp - 1) / kColsPerWarp));
+        if (vec) side_kernel<true, true, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
+        else side_kernel<false, true, true><<<g, kRowsPerCta * 32, 0, ctx->stream>>>(a);
+    }
+    SBD_LAUNCHED(ctx, "side_kernel<alpha pass>");
+    return SBD_OK;
+}
+
 int ensure_events(sbd_ctx *ctx, size_t n) {
     if (!ctx->copy_stream) SBD_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     while (ctx->events.size() < n) {
@@ -1040,6 +1117,29 @@ int ensure_events(sbd_ctx *ctx, size_t n) {
 }
 
 }  // namespace
+
+int sbd_require_sigma_ready(sbd_ctx *ctx) {
+    int rc = require_ready(ctx);
+    if (rc) return rc;
+    rc = require_product(ctx);
+    if (rc) return rc;
+    rc = ensure_scratch(ctx);
+    if (rc) return rc;
+    return ensure_diag(ctx);
+}
+
+int sbd_beta_side(sbd_ctx *ctx, const double *x_own) { return launch_beta_side(ctx, x_own, 0, ctx->own_rows()); }
+
+int sbd_alpha_pass(sbd_ctx *ctx, const double *X, double *y, const Conn *conn, const int64_t *seg_off, i64 stride,
+                   int s_lo, int s_hi, i64 xo_row0, bool epi, bool acc_in) {
+    return launch_alpha_pass(ctx, X, y, conn, seg_off, stride, s_lo, s_hi, xo_row0, epi, acc_in);
+}
+
+int sbd_cross_add(sbd_ctx *ctx, const double *X, double *y, const SConn *sconn) {
+    const Sector &A = ctx->sec[0], &B = ctx->sec[1];
+    if (ctx->own_rows() == 0 || B.n == 0 || A.ns == 0 || B.ns == 0) return SBD_OK;
+    return launch_cross(ctx, X, y, true, sconn);
+}
 
 extern "C" {
 

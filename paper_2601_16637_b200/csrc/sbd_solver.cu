@@ -151,6 +151,35 @@ __global__ void argmin_final_kernel(const double *pv, const i64 *pi, int nb, i64
     if (threadIdx.x == 0) v0[si[0] < n ? si[0] : 0] = 1.0;
 }
 
+// partitioned start vector: local best (value, global index) -> s[0], s[1]
+__global__ void argmin_local_kernel(const double *pv, const i64 *pi, int nb, i64 n, i64 goff, double *s) {
+    __shared__ double sv[kArgBlock];
+    __shared__ i64 si[kArgBlock];
+    double bv = INFINITY;
+    i64 bi = n;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) better(bv, bi, pv[i], pi[i]);
+    sv[threadIdx.x] = bv;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) better(sv[threadIdx.x], si[threadIdx.x], sv[threadIdx.x + w], si[threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        s[0] = sv[0];
+        s[1] = si[0] < n ? (double)(goff + si[0]) : INFINITY;
+        s[2] = sv[0];  // all-reduced (min) next
+    }
+}
+// after s[2] = global min value: candidate index s[3] (all-reduced min next)
+__global__ void argmin_candidate_kernel(double *s) { s[3] = s[0] == s[2] ? s[1] : INFINITY; }
+// s[3] = global argmin (first index on ties, davidson.py:219-221): set it if it is local
+__global__ void argmin_set_kernel(const double *s, i64 n, i64 goff, double *v0) {
+    const double gi = s[3];
+    if (gi >= (double)goff && gi < (double)(goff + n)) v0[(i64)gi - goff] = 1.0;
+    else if (!(gi < INFINITY) && goff == 0) v0[0] = 1.0;  // no finite diagonal anywhere: e_0
+}
+
 __device__ inline u64 splitmix64(u64 z) {
     z += 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -158,9 +187,11 @@ __device__ inline u64 splitmix64(u64 z) {
     return z ^ (z >> 31);
 }
 
-__global__ void random_normal_kernel(double *t, i64 n, u64 seed) {
+// element i of the local slice is global element goff + i: the draw does not depend on the partition
+__global__ void random_normal_kernel(double *t, i64 n, i64 goff, u64 seed) {
     for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-        u64 a = splitmix64(seed ^ (2 * (u64)i)), b = splitmix64(seed ^ (2 * (u64)i + 1));
+        const u64 gi = (u64)(goff + i);
+        u64 a = splitmix64(seed ^ (2 * gi)), b = splitmix64(seed ^ (2 * gi + 1));
         double u1 = ((a >> 11) + 1) * 0x1.0p-53;  // (0, 1]
         double u2 = (b >> 11) * 0x1.0p-53;
         t[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
@@ -189,6 +220,11 @@ struct Solver {
     Pinned host, hrs;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     u64 seed = 0x5BD1A6ull;
+    bool dist = false;  // partitioned context: vectors are this rank's rows, dots are all-reduced
+    i64 goff = 0;       // global index of local element 0
+
+    int AR(double *p, int cnt) { return dist ? sbd_dist_allreduce_internal(ctx, p, cnt, 0) : SBD_OK; }
+    int sigma(const double *x, double *y) { return dist ? sbd_sigma_dist(ctx, x, y) : sbd_sigma(ctx, x, y); }
 
     ~Solver() {
         if (ev0) cudaEventDestroy(ev0);
@@ -200,7 +236,7 @@ struct Solver {
     int readback(const double *src, int cnt, double *dst) {
         SBD_CUDA(ctx, cudaMemcpyAsync(dst, src, sizeof(double) * cnt, cudaMemcpyDeviceToHost, ctx->stream));
         SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-        return SBD_OK;
+        return dist ? sbd_dist_check_internal(ctx) : SBD_OK;
     }
 
     const double *dg = nullptr;  // diagonal used by the preconditioner
@@ -257,10 +293,19 @@ struct Solver {
             double *pv = part.as<double>();
             i64 *pi = reinterpret_cast<i64 *>(pv + nb);
             argmin_partial_kernel<<<nb, kArgBlock, 0, ctx->stream>>>(dg, n, pv, pi);
-            argmin_final_kernel<<<1, kArgBlock, 0, ctx->stream>>>(pv, pi, nb, n, V);
+            if (!dist) {
+                argmin_final_kernel<<<1, kArgBlock, 0, ctx->stream>>>(pv, pi, nb, n, V);
+            } else {  // global argmin over the ranks: min value, then the smallest index holding it
+                argmin_local_kernel<<<1, kArgBlock, 0, ctx->stream>>>(pv, pi, nb, n, goff, small);
+                if (int rc = sbd_dist_allreduce_internal(ctx, small + 2, 1, 2)) return rc;
+                argmin_candidate_kernel<<<1, 1, 0, ctx->stream>>>(small);
+                if (int rc = sbd_dist_allreduce_internal(ctx, small + 3, 1, 2)) return rc;
+                argmin_set_kernel<<<1, 1, 0, ctx->stream>>>(small, n, goff, V);
+            }
             SBD_LAUNCHED(ctx, "davidson start vector");
         } else {
             if (int rc = sbd_vdots(ctx, x0, 1, ld, n, x0, small)) return rc;
+            if (int rc = AR(small, 1)) return rc;
             if (int rc = readback(small, 1, host.p)) return rc;
             const double nrm = std::sqrt(std::max(host.p[0], 0.0));
             if (!(nrm > 0.0) || !std::isfinite(nrm)) return sbd_fail(ctx, SBD_EINVAL, "x0 must be nonzero and finite");
@@ -283,6 +328,7 @@ struct Solver {
             std::vector<double> c2h(k);
             if (!pre_c2) {
                 if (int rc = sbd_gs_update(ctx, V, k, ld, n, c, t, small2)) return rc;
+                if (int rc = AR(small2, k + 1)) return rc;
                 if (int rc = readback(small2, k + 1, hb)) return rc;
                 std::memcpy(c2h.data(), hb, sizeof(double) * k);
                 n2p = hb[k];
@@ -307,6 +353,7 @@ struct Solver {
         } else {
             if (int rc = sbd_gs_update_nodots(ctx, V, k, ld, n, c, t, small2)) return rc;
         }
+        if (int rc = AR(small2, 1)) return rc;
         if (int rc = readback(small2, 1, hb)) return rc;
         const double norm = std::sqrt(std::max(hb[0], 0.0));
         if (norm < 1e-12 * norm0 || norm == 0.0) return SBD_OK;
@@ -320,9 +367,11 @@ struct Solver {
     // c = V^T t and |t|^2 for a fresh direction t (one extra pass)
     int project(int k, double *t, double *t_norm2) {
         if (int rc = sbd_vdots2(ctx, V, k, ld, n, t, t, small)) return rc;
+        if (int rc = AR(small, k)) return rc;
         copy_small_kernel<<<1, kMaxK, 0, ctx->stream>>>(small, c, k);
         SBD_LAUNCHED(ctx, "davidson c");
         if (int rc = sbd_vdots(ctx, t, 1, ld, n, t, small + 2 * kMaxK)) return rc;
+        if (int rc = AR(small + 2 * kMaxK, 1)) return rc;
         if (int rc = readback(small + 2 * kMaxK, 1, host.p)) return rc;
         *t_norm2 = host.p[0];
         return SBD_OK;
@@ -344,12 +393,13 @@ struct Solver {
             };
             st->iterations = iteration;
             SBD_CUDA(ctx, cudaEventRecord(ev0, ctx->stream));
-            if (int rc = sbd_sigma(ctx, vec(V, k - 1), vec(W, k - 1))) return rc;
+            if (int rc = sigma(vec(V, k - 1), vec(W, k - 1))) return rc;
             SBD_CUDA(ctx, cudaEventRecord(ev1, ctx->stream));
             st->n_applies++;
 
             // T[:, k-1] = V^T w and the Gram row of v_{k-1}: one pass over V
             if (int rc = sbd_vdots2(ctx, V, k, ld, n, vec(W, k - 1), vec(V, k - 1), small)) return rc;
+            if (int rc = AR(small, 2 * k)) return rc;
             set_tg_kernel<<<1, kMaxK, 0, ctx->stream>>>(T, G, small, k, kmax);
             SBD_LAUNCHED(ctx, "davidson T");
             // Rayleigh-Ritz in place on T (davidson.py:251)
@@ -364,12 +414,15 @@ struct Solver {
             if (int rc = sbd_residual_precond_target(ctx, V, W, k, ld, n, Y, th, mk, jp, dg,
                                                      o.precond_delta, Tv, ld, small))
                 return rc;
+            if (int rc = AR(small, k + 1 + mk)) return rc;
             copy_small_kernel<<<1, kMaxK, 0, ctx->stream>>>(small, c, k);
             SBD_LAUNCHED(ctx, "davidson c");
             // speculative CGS pass 1 on the projected root, read back with the pack
             const bool spec = o.reorthogonalize && k < kmax && iteration < o.max_iters;
-            if (spec)
+            if (spec) {
                 if (int rc = sbd_gs_update(ctx, V, k, ld, n, c, vec(Tv, jp), small2)) return rc;
+                if (int rc = AR(small2, k + 1)) return rc;
+            }
             pack_kernel<<<1, 256, 0, ctx->stream>>>(jw, small, small2, info, G, kmax, k, mk, o.track_orthogonality,
                                                    spec ? 1 : 0, pack);
             SBD_LAUNCHED(ctx, "davidson pack");
@@ -464,7 +517,7 @@ struct Solver {
                 return rc;
             for (int attempts = 0; !ok && attempts < 3; ++attempts) {
                 st->breakdowns++;
-                random_normal_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(t, n, seed + 0x1000ull * st->breakdowns);
+                random_normal_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(t, n, goff, seed + 0x1000ull * st->breakdowns);
                 SBD_LAUNCHED(ctx, "davidson random direction");
                 double nn = 0.0;
                 if (int rc = project(k, t, &nn)) return rc;
@@ -529,16 +582,19 @@ int sbd_davidson(sbd_ctx *ctx, const sbd_davidson_opts *opts, const double *diag
     if (o.n_roots > kMaxRoots) return sbd_fail(ctx, SBD_EINVAL, "n_roots must be <= 8 on the B200 path");
     if (!ctx->have_integrals || !ctx->sec[0].present || !ctx->sec[1].present)
         return sbd_fail(ctx, SBD_EINVAL, "integrals and strings must be set first");
-    i64 n;
+    i64 n, nglob;
+    const bool dist = ctx->dist.on && ctx->dist.nranks > 1;
     if (ctx->explicit_mode) {
-        n = ctx->n_det;
+        n = nglob = ctx->n_det;
     } else {
-        if (ctx->own_rows() != ctx->sec[0].n)
-            return sbd_fail(ctx, SBD_EINVAL, "sbd_davidson needs all rows on this context (multi-GPU: DistributedApplier)");
-        n = ctx->sec[0].n * ctx->sec[1].n;
+        // a partitioned context (sbd_dist_init) solves over its own rows, all-reducing every dot product
+        if (!dist && ctx->own_rows() != ctx->sec[0].n)
+            return sbd_fail(ctx, SBD_EINVAL, "sbd_davidson: a row-windowed context must be partitioned (sbd_dist_init)");
+        n = ctx->own_rows() * ctx->sec[1].n;
+        nglob = ctx->sec[0].n * ctx->sec[1].n;
     }
-    if (n < 1) return sbd_fail(ctx, SBD_EINVAL, "empty problem");
-    if (n < o.n_roots) return sbd_fail(ctx, SBD_EINVAL, "cannot extract n_roots roots from this dimension");
+    if (nglob < 1) return sbd_fail(ctx, SBD_EINVAL, "empty problem");
+    if (nglob < o.n_roots) return sbd_fail(ctx, SBD_EINVAL, "cannot extract n_roots roots from this dimension");
     sbd_davidson_stats local;
     std::memset(&local, 0, sizeof(local));
     sbd_davidson_stats *st = stats ? stats : &local;
@@ -548,8 +604,10 @@ int sbd_davidson(sbd_ctx *ctx, const sbd_davidson_opts *opts, const double *diag
     s.ctx = ctx;
     s.o = o;
     s.n = n;
+    s.dist = dist;
+    s.goff = dist ? ctx->own_lo() * ctx->sec[1].n : 0;
     s.m = o.n_roots;
-    s.kmax = (int)std::min<i64>(o.max_subspace, n);
+    s.kmax = (int)std::min<i64>(o.max_subspace, nglob);
     s.keep = std::min(o.restart_keep, s.kmax);
     return s.run(diag_dev, x0_dev, evals_host, res_norms_host, evecs_dev, ldu > 0 ? ldu : n, st);
 }

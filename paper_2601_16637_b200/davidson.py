@@ -285,7 +285,10 @@ def davidson_solve(apply_h: Callable, diag, x0=None, opts: Optional[DavidsonOpti
     if _use_native(apply_h, allreduce, opts, native):
         with torch.cuda.device(dev):
             dd = diag if isinstance(diag, torch.Tensor) else torch.from_numpy(diag_np)
-            return _solve_native(apply_h, dd.to(dev, torch.float64).contiguous(), x0, opts, n, dev, return_device)
+            res = _solve_native(apply_h.context, n, dd.to(dev, torch.float64).contiguous(), x0, opts, dev,
+                                return_device)
+            apply_h.apply_count += res.stats.n_applies
+            return res
     with torch.cuda.device(dev):
         return _solve(apply_h, diag_dev if diag_dev is not None else torch.from_numpy(diag_np).to(dev),
                       x0, opts, n, n_loc, dev, return_device, allreduce, rank_offset, ctx)
@@ -305,8 +308,13 @@ def _use_native(apply_h, allreduce, opts, native) -> bool:
     return bool(native)
 
 
-def _solve_native(app, diag_dev, x0, opts, n, dev, return_device):
-    """C++ control loop (``sbd_davidson``, csrc/sbd_solver.cu) over the applier's context."""
+def _solve_native(ctx, n, diag_dev, x0, opts, dev, return_device):
+    """C++ control loop (``sbd_davidson``, csrc/sbd_solver.cu) over a context.
+
+    ``n`` is the context's own length: all rows for a single-GPU applier, the
+    rank's rows for a partitioned context (sbd_dist_init), whose dot products
+    the library all-reduces.
+    """
     import ctypes
 
     import torch
@@ -334,11 +342,9 @@ def _solve_native(app, diag_dev, x0, opts, n, dev, return_device):
     evals = np.full(m, np.nan)
     res = np.full(m, np.nan)
     U = torch.empty((m, n), **f64)
-    ctx = app.context
     ctx.bind_stream()
     ctx("sbd_davidson", ctypes.byref(o), _p(diag_dev), _p(v0), evals.ctypes.data, res.ctypes.data, _p(U), n,
         ctypes.byref(st))
-    app.apply_count += st.n_applies
     it, nf = st.iterations, st.n_found
     stats = DavidsonStats(iterations=it, converged=bool(st.converged), n_applies=st.n_applies,
                           restarts=st.restarts, breakdowns=st.breakdowns)

@@ -2,38 +2,42 @@
 
 The reference simulates P workers with Python threads passing ket blocks
 around a ring (``distsim.py:200-259``).  Here each rank is one process on one
-GPU (``torch.distributed``, NCCL over NVLink/NVSwitch):
+GPU and the whole partitioned operator lives in ``libsbd_b200.so``
+(``csrc/sbd_dist.cu``, NCCL over NVLink/NVSwitch inside the library):
 
 * partition: contiguous alpha blocks, the first ``rem`` blocks one row longer
   (``make_partition``, ``distsim.py:63-77``); rank r owns x, sigma, diag, V and
   W rows ``[lo_r, hi_r) x n_beta``;
-* per sigma, ONE exchange: an all-gather of the trial vector's blocks
-  (NVSwitch gives every peer full bandwidth, so no ring is needed), launched
-  first on NCCL's stream while the compute stream runs the beta-beta part
-  from the rank's own rows (``sbd_sigma_local``); the alpha-alpha and
-  alpha-beta parts (``sbd_sigma_remote``) start once the gather lands;
-* Davidson: vectors stay row-partitioned; the O(k) dot products of every
-  fused pass are all-reduced (a few hundred bytes per iteration).
-* sparse exchange (the successor of the reference ring): a rank
-  only reads the x rows its own rows connect to.  When those are a minority
-  of the remote rows (cfg4: ~40%), the all-gather is replaced by grouped
-  point-to-point transfers of exactly the referenced rows (request lists are
-  exchanged once at construction; each sigma packs, sends, receives and
-  scatters rows), cutting the per-sigma NVLink volume in proportion.
+* per sigma, the reference ring's exchange pattern -- at step s rank r sends to
+  (r + s) mod P and receives the block of (r - s) mod P -- on an exchange
+  stream, while the compute stream runs the beta-beta part and the alpha
+  pass over the rank's own rows, then one alpha pass per group of landed
+  steps (``y +=``), then task 0.  Only the last group's transfer can be
+  exposed (``sbd_dist_stats`` measures it: ``overlap_stats``);
+* sparse exchange: when the referenced remote rows are a
+  minority (cfg4: ~40%), only those rows travel, packed by the sender;
+* Davidson: vectors stay row-partitioned; the native control loop
+  (``sbd_davidson``) all-reduces the O(k) dot products of every fused pass.
 
 ``DistributedApplier(...).apply(x)`` keeps the reference signature (full
 numpy x on every rank in, full y out).  The device-resident path is
 ``apply_device`` / ``davidson``.
+
+``_rank_engine`` replaces the CUDA rank (tests on CPU): the same ring then
+runs over ``torch.distributed`` (gloo) in Python, block by block, as the
+CPU twin of the native schedule.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import ctypes
+from dataclasses import dataclass, field
 from typing import Optional
 
 import numpy as np
 
-__all__ = ["Partition", "PartitionError", "make_partition", "DistributedApplier", "Comm"]
+__all__ = ["Partition", "PartitionError", "make_partition", "DistributedApplier", "Comm", "OverlapReport",
+           "overlap_stats"]
 
 
 class PartitionError(ValueError):
@@ -60,8 +64,53 @@ def make_partition(n_alpha: int, n_workers: int) -> Partition:
     return Partition(n_workers, tuple((int(edges[w]), int(edges[w + 1])) for w in range(n_workers)))
 
 
+@dataclass
+class OverlapReport:
+    """Per-step overlap of one or more partitioned sigmas (reference ``OverlapReport``, distsim.py:81-88).
+
+    Step 0 is the rank-local work (beta side + the alpha pass over the own
+    rows); step g >= 1 is ring-step group g.  Times are device seconds per
+    sigma, averaged over ranks: ``compute`` the passes, ``transfer`` the
+    group's NCCL transfer, ``exposed`` the compute stream's wait for it.
+    """
+    n_workers: int
+    n_steps: int
+    overlap: bool
+    transfer_delay: float
+    per_step: list  # rows: (step, mean compute, mean transfer, mean exposed, ratio)
+    total_compute_s: float
+    total_transfer_s: float
+    total_exposed_s: float
+    overlap_ratio: float
+    sigma_s: float = 0.0           # mean device time of one sigma (first exchange launch -> last pass), max over ranks
+    n_sigma: int = 0
+    per_rank: list = field(default_factory=list)
+
+
+def overlap_stats(records, overlap: bool = True) -> OverlapReport:
+    """Aggregate per-rank step records (``DistributedApplier.step_records``) like distsim.py:340-367."""
+    p = len(records)
+    n_steps = max(len(r["compute_ms"]) for r in records)
+    per_step = []
+    for s in range(n_steps):
+        rows = [r for r in records if s < len(r["compute_ms"])]
+        ns = [max(r["n_sigma"], 1) for r in rows]
+        compute = float(np.mean([r["compute_ms"][s] / n for r, n in zip(rows, ns)])) / 1e3
+        transfer = float(np.mean([r["transfer_ms"][s] / n for r, n in zip(rows, ns)])) / 1e3
+        exposed = float(np.mean([r["exposed_ms"][s] / n for r, n in zip(rows, ns)])) / 1e3
+        total = compute + exposed
+        per_step.append((s, compute, transfer, exposed, 1.0 - (exposed / total if total > 0 else 0.0)))
+    tc, tt, te = (sum(row[i] for row in per_step) for i in (1, 2, 3))
+    denom = tc + te
+    sig = max(r["total_ms"] / max(r["n_sigma"], 1) for r in records) / 1e3
+    return OverlapReport(n_workers=p, n_steps=n_steps, overlap=overlap, transfer_delay=0.0, per_step=per_step,
+                         total_compute_s=tc, total_transfer_s=tt, total_exposed_s=te,
+                         overlap_ratio=1.0 - (te / denom if denom > 0 else 0.0), sigma_s=sig,
+                         n_sigma=int(min(r["n_sigma"] for r in records)), per_rank=list(records))
+
+
 class Comm:
-    """Collectives used by the partitioned path; NCCL native, gloo staged through host."""
+    """torch.distributed plumbing: object exchange at setup, the reference-protocol gathers, the CPU twin."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -75,34 +124,40 @@ class Comm:
     def _staged(self, t) -> bool:
         return self.backend == "gloo" and t.is_cuda
 
-    def allreduce(self, t) -> None:
+    def allreduce(self, t, op=None) -> None:
         if self.world == 1:
             return
+        op = self.dist.ReduceOp.SUM if op is None else op
         if self._staged(t):
             h = t.cpu()
-            self.dist.all_reduce(h, group=self.group)
+            self.dist.all_reduce(h, op=op, group=self.group)
             t.copy_(h)
         else:
-            self.dist.all_reduce(t, group=self.group)
+            self.dist.all_reduce(t, op=op, group=self.group)
 
-    def allgather_start(self, views, local):
-        """Start gathering ``local`` of every rank into ``views``; returns a waitable."""
+    def allgather_blocks(self, out, local, blocks, row) -> None:
+        """Gather every rank's ``local`` (its rows of ``blocks``, ``row`` elements each) into ``out``.
+
+        One padded ``all_gather_into_tensor`` (blocks differ by at most one row), unpadded into ``out``.
+        """
+        import torch
+
         if self.world == 1:
-            views[0].copy_(local)
-            return None
+            out.copy_(local)
+            return
+        mx = max(b - a for a, b in blocks) * row
+        dev = torch.device("cpu") if self.backend == "gloo" else local.device
+        send = torch.zeros(mx, dtype=local.dtype, device=dev)
+        send[: local.numel()] = local.to(dev)
+        recv = torch.empty(self.world * mx, dtype=local.dtype, device=dev)
         if self.backend == "gloo":
-            # gloo all_gather needs equal sizes: pad every block to the longest
-            import torch
-
-            mx = max(v.numel() for v in views)
-            send = torch.zeros(mx, dtype=local.dtype)
-            send[: local.numel()] = local.cpu()
-            recv = [torch.empty(mx, dtype=local.dtype) for _ in views]
-            self.dist.all_gather(recv, send, group=self.group)
-            for v, h in zip(views, recv):
-                v.copy_(h[: v.numel()])
-            return None
-        return self.dist.all_gather(views, local, group=self.group, async_op=True)
+            parts = list(recv.view(self.world, mx).unbind(0))
+            self.dist.all_gather(parts, send, group=self.group)
+        else:
+            self.dist.all_gather_into_tensor(recv, send, group=self.group)
+        rv = recv.view(self.world, mx)
+        for q, (a, b) in enumerate(blocks):
+            out[a * row:b * row].copy_(rv[q, :(b - a) * row])
 
     def barrier(self) -> None:
         if self.world > 1:
@@ -113,74 +168,106 @@ class Comm:
         self.dist.all_gather_object(out, obj, group=self.group)
         return out
 
-    def exchange_rows(self, sends: dict, recvs: dict):
-        """Point-to-point transfers {peer: tensor}; returns a list of waitables (empty when staged)."""
-        if self.backend == "gloo":  # gloo: host-staged, blocking
-            import torch
+    def broadcast_object(self, obj, src: int = 0):
+        lst = [obj]
+        self.dist.broadcast_object_list(lst, src=self._global(src), group=self.group)
+        return lst[0]
 
-            ops, host_recv = [], {}
-            for p, t in sends.items():
-                ops.append(self.dist.isend(t.cpu(), self._global(p), group=self.group))
-            for p, t in recvs.items():
-                host_recv[p] = torch.empty(t.shape, dtype=t.dtype)
-                ops.append(self.dist.irecv(host_recv[p], self._global(p), group=self.group))
-            for op in ops:
-                op.wait()
-            for p, t in recvs.items():
-                t.copy_(host_recv[p])
-            return []
-        ops = [self.dist.P2POp(self.dist.isend, t, self._global(p), group=self.group) for p, t in sends.items()]
-        ops += [self.dist.P2POp(self.dist.irecv, t, self._global(p), group=self.group) for p, t in recvs.items()]
-        return self.dist.batch_isend_irecv(ops) if ops else []
+    def sendrecv(self, send, to: int, recv, frm: int) -> None:
+        """Blocking ring step (CPU twin)."""
+        ops = [self.dist.P2POp(self.dist.isend, send, self._global(to), group=self.group),
+               self.dist.P2POp(self.dist.irecv, recv, self._global(frm), group=self.group)]
+        for w in self.dist.batch_isend_irecv(ops):
+            w.wait()
 
     def _global(self, rank: int) -> int:
         return rank if self.group is None else self.dist.get_global_rank(self.group, rank)
 
 
-class _CudaRank:
-    """This rank's slice of the operator on its GPU (a row-windowed HamiltonianApplier)."""
+_EXCHANGE = {"auto": 0, "allgather": 1, "dense": 1, "sparse": 2}
 
-    def __init__(self, basis, table, lo, hi, device):
-        from .apply import HamiltonianApplier
 
-        self.app = HamiltonianApplier(basis, table, row_window=(lo, hi), device=device)
-        self.device = self.app._torch_device
-        self.diag = self.app.diag_device
+class _NativeRank:
+    """This rank's partitioned context: tables, plan and NCCL inside libsbd_b200.so (sbd_dist_*)."""
 
-    def sigma_local(self, x_own):
+    def __init__(self, basis, table, comm: Comm, partition: Partition, device, exchange: str,
+                 sparse_threshold: float, group_steps: int):
+        import torch
+
         from . import _lib
 
-        self.app.context.bind_stream()
-        self.app.context("sbd_sigma_local", _lib.ptr(x_own))
-
-    def sigma_remote(self, x_full, y_own):
-        from . import _lib
-
-        self.app.context.bind_stream()
-        self.app.context("sbd_sigma_remote", _lib.ptr(x_full), _lib.ptr(y_own))
+        self.device = torch.device("cuda", int(device))
+        self.ctx = ctx = _lib.Context(self.device.index)
+        h = np.ascontiguousarray(table.h, dtype=np.float64)
+        eri = np.ascontiguousarray(table.eri, dtype=np.float64)
+        a = np.ascontiguousarray(basis.alpha_array(), dtype=np.uint64)
+        b = np.ascontiguousarray(basis.beta_array(), dtype=np.uint64)
+        with torch.cuda.device(self.device):
+            ctx("sbd_set_integrals", int(table.norb), _lib.ptr(h), _lib.ptr(eri), int(eri.size), float(table.e_core))
+            ctx("sbd_set_strings", 0, _lib.ptr(a), int(a.size), int(basis.n_alpha_elec))
+            ctx("sbd_set_strings", 1, _lib.ptr(b), int(b.size), int(basis.n_beta_elec))
+            uid = _lib.nccl_unique_id() if (comm.rank == 0 and comm.world > 1) else None
+            uid = comm.broadcast_object(uid) if comm.world > 1 else None
+            edges = np.array([lo for lo, _ in partition.alpha_blocks] + [partition.alpha_blocks[-1][1]],
+                             dtype=np.int64)
+            ctx("sbd_dist_init", comm.rank, comm.world, uid, _lib.ptr(edges))
+            ctx("sbd_build_tables")
+            ctx.bind_stream()
+            ctx("sbd_dist_plan", _EXCHANGE[exchange], float(sparse_threshold), int(group_steps))
+            lo, hi = partition.block_of(comm.rank)
+            self.n_own = (hi - lo) * b.size
+            self.diag = torch.empty(self.n_own, dtype=torch.float64, device=self.device)
+            ctx("sbd_diag", _lib.ptr(self.diag))
+            torch.cuda.synchronize(self.device)
+        self.n_alpha, self.n_beta = int(a.size), int(b.size)
 
     @property
     def context(self):
-        return self.app.context
+        return self.ctx
 
-    def alpha_targets(self, lo, hi):
-        """Alpha rows that rows [lo, hi) connect to (singles and doubles, in-set)."""
-        t = self.app.tables.alpha
-        parts = [t.s_tgt[t.s_off[lo]:t.s_off[hi]], t.d_tgt[t.d_off[lo]:t.d_off[hi]]]
-        return np.unique(np.concatenate(parts).astype(np.int64))
+    def sigma(self, x_own, y_own) -> None:
+        from . import _lib
+
+        self.ctx.bind_stream()
+        self.ctx("sbd_sigma_dist", _lib.ptr(x_own), _lib.ptr(y_own))
+
+    def info(self) -> dict:
+        vals = [ctypes.c_int(), ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_double(),
+                ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()]
+        self.ctx("sbd_dist_info", *[ctypes.byref(v) for v in vals])
+        keys = ("rank", "nranks", "alpha_lo", "alpha_hi", "sparse", "needed_fraction", "recv_rows", "send_rows",
+                "n_groups")
+        return {k: v.value for k, v in zip(keys, vals)}
+
+    def set_profiling(self, on: bool) -> None:
+        self.ctx("sbd_dist_set_profiling", int(bool(on)))
+
+    def step_record(self) -> dict:
+        n_sigma, n_steps, total = ctypes.c_int64(), ctypes.c_int(), ctypes.c_double()
+        buf = [np.zeros(64) for _ in range(3)]
+        self.ctx("sbd_dist_stats", ctypes.byref(n_sigma), ctypes.byref(n_steps), *[b.ctypes.data for b in buf],
+                 ctypes.byref(total))
+        k = n_steps.value
+        return {"n_sigma": n_sigma.value, "compute_ms": buf[0][:k].tolist(), "transfer_ms": buf[1][:k].tolist(),
+                "exposed_ms": buf[2][:k].tolist(), "total_ms": total.value}
 
 
 class DistributedApplier:
     """One rank of the alpha-block partitioned y = H x (reference ``distsim.py:130-316``).
 
-    Call on every rank of an initialised ``torch.distributed`` group.
-    ``overlap`` keeps its reference meaning (communication overlapped with
-    local work); ``transfer_delay`` has no device analogue and must be 0.
+    Call on every rank of an initialised ``torch.distributed`` group (any
+    backend: it only carries the NCCL unique id at setup and the
+    reference-protocol gathers; the per-sigma traffic is the library's own
+    NCCL communicator).  ``overlap=False`` makes every alpha pass wait for
+    the whole exchange (one group); ``transfer_delay`` has no device analogue
+    and must be 0.  ``exchange``: "auto" (sparse when the referenced fraction
+    of remote rows is at most ``sparse_threshold``), "allgather"/"dense" or
+    "sparse"; ``group_steps``: ring steps per pipelined alpha pass.
     """
 
     def __init__(self, basis, table, tables=None, partition: Optional[Partition] = None, n_workers: Optional[int] = None,
                  overlap: bool = True, transfer_delay: float = 0.0, group=None, device=None, _rank_engine=None,
-                 exchange: str = "auto", sparse_threshold: float = 0.6):
+                 exchange: str = "auto", sparse_threshold: float = 0.6, group_steps: int = 2):
         import torch
 
         if basis.mode != "product":
@@ -189,6 +276,10 @@ class DistributedApplier:
             raise ValueError("transfer_delay must be >= 0")
         if transfer_delay:
             raise ValueError("transfer_delay is a simulation knob; the B200 path uses real NVLink transfers")
+        if exchange not in _EXCHANGE:
+            raise ValueError(f"exchange must be 'auto', 'allgather', 'dense' or 'sparse', got {exchange!r}")
+        if group_steps < 1:
+            raise ValueError("group_steps must be >= 1")
         self.comm = Comm(group)
         world = self.comm.world
         if n_workers is not None and n_workers != world:
@@ -202,70 +293,27 @@ class DistributedApplier:
         self.rank = self.comm.rank
         self.lo, self.hi = self.partition.block_of(self.rank)
         self.n_own = (self.hi - self.lo) * self.n_beta
-        if _rank_engine is not None:
+        self.apply_count = 0
+        self.group_steps = group_steps if overlap else max(world - 1, 1)
+        if _rank_engine is not None:  # CPU twin of the schedule (tests): torch.distributed ring in Python
+            self.native = False
             self.engine = _rank_engine(basis, table, self.lo, self.hi)
-        else:
-            if device is None:
-                device = torch.cuda.current_device()
-            self.engine = _CudaRank(basis, table, self.lo, self.hi, device)
+            self.device = self.engine.device
+            self.diag_local = self.engine.diag
+            self.exchange = "dense"
+            return
+        self.native = True
+        if device is None:
+            device = torch.cuda.current_device()
+        self.engine = _NativeRank(basis, table, self.comm, self.partition, device, exchange, sparse_threshold,
+                                  self.group_steps)
         self.device = self.engine.device
         self.diag_local = self.engine.diag
-        self._x_full = torch.empty(self.n, dtype=torch.float64, device=self.device)
-        nb = self.n_beta
-        self._views = [self._x_full[a * nb:b * nb] for a, b in self.partition.alpha_blocks]
-        self.apply_count = 0
-        if exchange not in ("auto", "allgather", "sparse"):
-            raise ValueError(f"exchange must be 'auto', 'allgather' or 'sparse', got {exchange!r}")
-        self.exchange = "allgather"
-        self.remote_rows_needed = 0
-        if world > 1 and exchange != "allgather":
-            self._plan_sparse(exchange, sparse_threshold)
-
-    # -- sparse row exchange ------------------------------------------
-    def _plan_sparse(self, exchange, threshold):
-        import torch
-
-        blocks = self.partition.alpha_blocks
-        need = self.engine.alpha_targets(self.lo, self.hi)
-        need = need[(need < self.lo) | (need >= self.hi)]
-        owner = np.searchsorted(np.array([b for _, b in blocks]), need, side="right")
-        req = {int(p): need[owner == p] for p in np.unique(owner)}
-        everyone = self.comm.allgather_object(req)  # setup only: who needs which of my rows
-        n_alpha = blocks[-1][1]
-        # the decision must be the same on every rank: the largest needed fraction decides
-        frac = max(sum(v.size for v in r.values()) / max(n_alpha - (b - a), 1) for r, (a, b) in zip(everyone, blocks))
-        self.remote_rows_needed = int(need.size)
-        self.remote_rows_total = int(n_alpha - (self.hi - self.lo))
-        self.sparse_fraction = float(frac)
-        if exchange == "auto" and frac > threshold:
-            return  # dense enough: the all-gather moves about as much and is one collective
-        dev = self.device
-        nb = self.n_beta
-        self._recv_rows = {p: torch.from_numpy(rows).to(dev) for p, rows in req.items() if rows.size}
-        self._recv_buf = {p: torch.empty((rows.numel(), nb), dtype=torch.float64, device=dev)
-                          for p, rows in self._recv_rows.items()}
-        self._send_rows = {}
-        for q, r in enumerate(everyone):
-            if q != self.rank and self.rank in r and r[self.rank].size:
-                self._send_rows[q] = torch.from_numpy(r[self.rank] - self.lo).to(dev)
-        self._send_buf = {q: torch.empty((rows.numel(), nb), dtype=torch.float64, device=dev)
-                          for q, rows in self._send_rows.items()}
-        self.exchange = "sparse"
-
-    def _sparse_start(self, x_own):
-        nb = self.n_beta
-        xo = x_own.view(-1, nb)
-        for q, rows in self._send_rows.items():
-            self._send_buf[q].copy_(xo.index_select(0, rows))
-        return self.comm.exchange_rows(self._send_buf, self._recv_buf)
-
-    def _sparse_finish(self, x_own, works):
-        for w in works:
-            w.wait()
-        xf = self._x_full.view(-1, self.n_beta)
-        for p, rows in self._recv_rows.items():
-            xf.index_copy_(0, rows, self._recv_buf[p])
-        self._views[self.rank].copy_(x_own)
+        info = self.engine.info() if world > 1 else {"sparse": 0, "needed_fraction": 1.0, "recv_rows": 0}
+        self.exchange = "sparse" if info["sparse"] == 1 else "dense"
+        self.sparse_fraction = float(info["needed_fraction"])
+        self.remote_rows_needed = int(info["recv_rows"])
+        self.remote_rows_total = int(self.partition.alpha_blocks[-1][1] - (self.hi - self.lo))
 
     # -- device-resident path -----------------------------------------------------
     def apply_device(self, x_own, y_own=None):
@@ -275,29 +323,31 @@ class DistributedApplier:
         if x_own.numel() != self.n_own:
             raise ValueError(f"expected {self.n_own} local amplitudes, got {x_own.numel()}")
         y = torch.empty(self.n_own, dtype=torch.float64, device=self.device) if y_own is None else y_own
+        if y.numel() != self.n_own or y.dtype != torch.float64:
+            raise ValueError(f"out must be a float64 tensor of {self.n_own} elements")
         self.apply_count += 1
-        if self.exchange == "sparse":
-            works = self._sparse_start(x_own)                      # NCCL p2p, referenced rows only
-            if self.overlap:
-                self.engine.sigma_local(x_own)                     # compute stream, concurrently
-                self._sparse_finish(x_own, works)
-            else:
-                self._sparse_finish(x_own, works)
-                self.engine.sigma_local(x_own)
-            self.engine.sigma_remote(self._x_full, y)
-            return y
-        if self.overlap:
-            work = self.comm.allgather_start(self._views, x_own)  # NCCL stream
-            self.engine.sigma_local(x_own)                         # compute stream, concurrently
-            if work is not None:
-                work.wait()
+        if self.native:
+            x_own = x_own.contiguous()
+            self.engine.sigma(x_own, y)
         else:
-            work = self.comm.allgather_start(self._views, x_own)
-            if work is not None:
-                work.wait()
-            self.engine.sigma_local(x_own)
-        self.engine.sigma_remote(self._x_full, y)
+            self._ring_twin(x_own, y)
         return y
+
+    def _ring_twin(self, x_own, y):
+        """CPU twin of sbd_sigma_dist: own block first, then ring step s brings the block of (r - s) mod P."""
+        import torch
+
+        P, r, nb = self.comm.world, self.rank, self.n_beta
+        blocks = self.partition.alpha_blocks
+        self.engine.sigma_block(x_own, self.rank, y, first=True)
+        held = x_own
+        for s in range(1, P):
+            frm = (r - s) % P
+            a, b = blocks[frm]
+            recv = torch.empty((b - a) * nb, dtype=torch.float64, device=self.device)
+            self.comm.sendrecv(x_own, (r + s) % P, recv, frm)
+            held = recv
+            self.engine.sigma_block(held, frm, y, first=False)
 
     # -- reference protocol ---------------------------------------------------------
     def apply(self, x) -> np.ndarray:
@@ -310,13 +360,28 @@ class DistributedApplier:
         x_own = torch.from_numpy(np.ascontiguousarray(x[self.lo * nb:self.hi * nb])).to(self.device)
         y_own = self.apply_device(x_own)
         y_full = torch.empty(self.n, dtype=torch.float64, device=self.device)
-        views = [y_full[a * nb:b * nb] for a, b in self.partition.alpha_blocks]
-        w = self.comm.allgather_start(views, y_own)
-        if w is not None:
-            w.wait()
+        self.comm.allgather_blocks(y_full, y_own, self.partition.alpha_blocks, nb)
         return y_full.cpu().numpy()
 
     __call__ = apply
+
+    # -- overlap accounting (reference overlap_stats) ------------------------------
+    def profile(self, on: bool = True) -> None:
+        """Record per-step compute / transfer / exposed device times of every following sigma."""
+        if self.native and self.comm.world > 1:
+            self.engine.set_profiling(on)
+
+    def step_records(self) -> dict:
+        return self.engine.step_record() if (self.native and self.comm.world > 1) else {
+            "n_sigma": 0, "compute_ms": [], "transfer_ms": [], "exposed_ms": [], "total_ms": 0.0}
+
+    def overlap_report(self) -> OverlapReport:
+        """Collective: every rank's step records, aggregated (reference ``overlap_stats``)."""
+        recs = self.comm.allgather_object(self.step_records())
+        recs = [r for r in recs if r["compute_ms"]]
+        if not recs:
+            return OverlapReport(self.comm.world, 0, self.overlap, 0.0, [], 0.0, 0.0, 0.0, 1.0)
+        return overlap_stats(recs, self.overlap)
 
     # -- partitioned Davidson -------------------------------------------------------
     def global_argmin_start(self):
@@ -326,44 +391,45 @@ class DistributedApplier:
         d = self.diag_local
         loc_min = float(torch.min(d).item()) if d.numel() else float("inf")
         loc_idx = int(torch.argmin(d).item()) + self.lo * self.n_beta if d.numel() else self.n
-        # lexicographic (value, global index) minimum via two all-reduces
         t = torch.tensor([loc_min], dtype=torch.float64, device=self.device)
-        neg = -t
-        self._allreduce_max(neg)
-        gmin = -float(neg.item())
+        self.comm.allreduce(t, self.comm.dist.ReduceOp.MIN)
+        gmin = float(t.item())
         cand = torch.tensor([float(loc_idx if loc_min == gmin else self.n)], dtype=torch.float64, device=self.device)
-        negc = -cand
-        self._allreduce_max(negc)
-        gidx = int(-negc.item())
+        self.comm.allreduce(cand, self.comm.dist.ReduceOp.MIN)
+        gidx = int(cand.item())
         x0 = torch.zeros(self.n_own, dtype=torch.float64, device=self.device)
         if self.lo * self.n_beta <= gidx < self.hi * self.n_beta:
             x0[gidx - self.lo * self.n_beta] = 1.0
         return x0
 
-    def _allreduce_max(self, t):
-        if self.comm.world == 1:
-            return
-        if self.comm._staged(t):
-            h = t.cpu()
-            self.comm.dist.all_reduce(h, op=self.comm.dist.ReduceOp.MAX, group=self.comm.group)
-            t.copy_(h)
-        else:
-            self.comm.dist.all_reduce(t, op=self.comm.dist.ReduceOp.MAX, group=self.comm.group)
-
     def davidson(self, x0=None, opts=None):
-        """Lowest eigenpairs with V/W row-partitioned across ranks; vectors returned as local slices."""
-        from .davidson import davidson_solve
+        """Lowest eigenpairs with V/W row-partitioned across ranks; vectors returned as local slices.
 
-        if x0 is None:
-            x0_local = self.global_argmin_start()
-        else:
-            import torch
+        Native ranks run the C++ control loop (``sbd_davidson`` on the partitioned context, NCCL
+        all-reduces inside the library); the CPU twin runs the Python loop with torch all-reduces.
+        """
+        import torch
 
+        from .davidson import DavidsonOptions, _solve_native, davidson_solve
+
+        x0_local = None
+        if x0 is not None:
             xa = x0 if isinstance(x0, torch.Tensor) else torch.from_numpy(np.asarray(x0, dtype=np.float64))
             xa = xa.reshape(-1)
             nb = self.n_beta
             x0_local = xa[self.lo * nb:self.hi * nb] if xa.numel() == self.n else xa
             x0_local = x0_local.to(self.device, dtype=torch.float64)
+        if self.native:
+            opts = DavidsonOptions() if opts is None else opts
+            if opts.n_roots > self.n:
+                raise ValueError(f"cannot extract {opts.n_roots} roots from dimension {self.n}")
+            with torch.cuda.device(self.device):
+                res = _solve_native(self.engine.context, self.n_own, self.diag_local, x0_local, opts, self.device,
+                                    True)
+            self.apply_count += res.stats.n_applies
+            return res
+        if x0_local is None:
+            x0_local = self.global_argmin_start()
 
         def op(x_dev, y_dev):
             self.apply_device(x_dev, y_dev)

@@ -1,8 +1,12 @@
 """Multi-process (gloo, CPU) tests of the alpha-block partitioned path's host logic.
 
-Each rank's device engine is replaced by the CPU oracle (test infrastructure);
-everything else -- make_partition, the uneven all-gather into x_full, the
-reference-protocol apply() gather of y blocks, the global argmin start vector --
+Each rank's device engine is replaced by the CPU oracle (test infrastructure),
+which makes DistributedApplier run the CPU twin of the native schedule: the
+own block first (diag, beta side, alpha terms into the own rows), then ring
+step s brings the block of (r - s) mod P and its alpha terms are added
+(y +=), exactly the pass order of sbd_sigma_dist.  Everything else --
+make_partition, the ring's neighbour pattern, the padded all_gather of the
+y blocks for the reference-protocol apply(), the global argmin start vector --
 is the product code (paper_2601_16637_b200/distributed.py).  Mirrors the
 reference's P-invariance tests (test_distsim.py:69-81).
 """
@@ -41,19 +45,20 @@ class OracleRank:
         self.diag = torch.from_numpy(O.diag(self.inst, (lo, hi)))
         self.local_calls = 0
 
-    def sigma_local(self, x_own):
-        self.local_calls += 1
+    def sigma_block(self, x_block, q, y_own, first):
+        """Contribution of ket block q (the reference ring's per-step product, ket window = block q)."""
+        from paper_2601_16637_b200.distributed import make_partition
 
-    def alpha_targets(self, lo, hi):
-        t = self.inst.ta
-        return np.unique(np.concatenate([t["s_tgt"][t["s_off"][lo]:t["s_off"][hi]],
-                                         t["d_tgt"][t["d_off"][lo]:t["d_off"][hi]]]).astype(np.int64))
+        a, b = make_partition(self.inst.alpha.size, self.world).block_of(q)
+        part = self.O.sigma(self.inst, x_block.numpy(), bra=(self.lo, self.hi), ket=(a, b))
+        if first:
+            self.local_calls += 1
+            y_own.copy_(torch.from_numpy(part))
+        else:
+            y_own.add_(torch.from_numpy(part))
 
-    def sigma_remote(self, x_full, y_own):
-        y_own.copy_(torch.from_numpy(self.O.sigma(self.inst, x_full.numpy(), bra=(self.lo, self.hi))))
 
-
-def _worker(rank, world, port, case, q, exchange="allgather"):
+def _worker(rank, world, port, case, q):
     try:
         import sys
 
@@ -68,12 +73,11 @@ def _worker(rank, world, port, case, q, exchange="allgather"):
         norb, na, nb, nsa, nsb, seed = case
         table = random_integrals(norb, seed)
         basis = random_product_basis(norb, na, nb, nsa, nsb, seed + 1)
-        dapp = DistributedApplier(basis, table, _rank_engine=OracleRank, exchange=exchange)
-        if exchange == "sparse":  # rows a rank does not receive must never be read
-            dapp._x_full.fill_(float("nan"))
+        OracleRank.world = world
+        dapp = DistributedApplier(basis, table, _rank_engine=OracleRank)
         x = np.random.default_rng(seed).standard_normal(basis.dimension)
         y = dapp(x)
-        assert dapp.exchange == ("sparse" if exchange == "sparse" else "allgather")
+        assert dapp.exchange == "dense" and not dapp.native
         x0 = dapp.global_argmin_start()
         dist.barrier()
         q.put((rank, dapp.lo, dapp.hi, y, x0.numpy(), dapp.engine.local_calls))
@@ -84,14 +88,13 @@ def _worker(rank, world, port, case, q, exchange="allgather"):
         q.put((rank, "error", traceback.format_exc()))
 
 
-@pytest.mark.parametrize("exchange", ["allgather", "sparse"])
 @pytest.mark.parametrize("world,case", [
     (2, (8, 4, 3, 30, 25, 3)),   # even-ish split
     (3, (8, 4, 4, 31, 20, 5)),   # uneven alpha blocks (11, 10, 10)
     (2, (6, 3, 3, 3, 20, 7)),    # tiny alpha sector
     (4, (12, 4, 4, 60, 20, 9)),  # sparse connectivity: ranks need a fraction of the remote rows
 ])
-def test_partitioned_apply_matches_serial(world, case, exchange):
+def test_partitioned_apply_matches_serial(world, case):
     import oracle as O
 
     from paper_2601_16637_b200.distributed import make_partition
@@ -100,7 +103,7 @@ def test_partitioned_apply_matches_serial(world, case, exchange):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q, exchange)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in range(world)]
@@ -122,7 +125,7 @@ def test_partitioned_apply_matches_serial(world, case, exchange):
         assert (lo, hi) == part.block_of(rank)
         # every rank returns the full, gathered y (reference DistributedApplier.apply contract)
         assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max()
-        assert local_calls == 1  # overlap path: local beta-beta part issued once per apply
+        assert local_calls == 1  # the own block (diag + beta side) is applied once per sigma
         # start vector: e_{global argmin diag}, sliced to the rank's rows
         want = np.zeros((hi - lo) * nbeta)
         if lo * nbeta <= gidx < hi * nbeta:

@@ -153,3 +153,20 @@ def test_native_davidson_default_options_match_reference_defaults():
               "reorthogonalize", "track_orthogonality"):
         assert getattr(o, f) == getattr(d, f), f
     assert _lib.load().sbd_davidson_default_opts(None) == 1
+
+
+def test_bench_gpus_flag_starts_that_many_ranks():
+    """bench.py --gpus N (no torchrun env) re-launches itself as N ranks; rank 0 reports n_gpus = N."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--backend", "gloo", "--dry-run"], cwd=root,
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1  # only rank 0 prints
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["rank_sum"] == 1
