@@ -28,6 +28,7 @@
 // Profiling mode records per-step compute / transfer / exposed times
 // (the reference's StepStat / overlap_stats, distsim.py:81-88,340-367).
 #include <dlfcn.h>
+#include <unistd.h>
 #include <nccl.h>  // types only: the symbols are resolved at run time (dlopen)
 
 #include <algorithm>
@@ -417,7 +418,18 @@ int sbd_dist_init(sbd_ctx *ctx, int rank, int nranks, const char *id, const int6
         ncclUniqueId uid;
         std::memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
         ncclComm_t comm = nullptr;
-        SBD_NCCL(ctx, n.CommInitRank(&comm, nranks, uid, rank));
+        // NCCL announces its version on stdout during the first init; a library must not write to
+        // the caller's stdout (the CLI's JSON report goes there), so it goes to stderr instead
+        fflush(stdout);
+        const int saved = dup(1);
+        if (saved >= 0) dup2(2, 1);
+        const ncclResult_t r = n.CommInitRank(&comm, nranks, uid, rank);
+        fflush(stdout);
+        if (saved >= 0) {
+            dup2(saved, 1);
+            close(saved);
+        }
+        if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclCommInitRank");
         d.comm = comm;
         SBD_CUDA(ctx, cudaStreamCreateWithFlags(&d.cs, cudaStreamNonBlocking));
     }

@@ -97,3 +97,28 @@ def test_solve_from_fcidump_and_samples(tmp_path, capsys):
     app = HamiltonianApplier(basis, table)
     res = davidson_solve(app, app.diag, x0=start_vector(basis, report), opts=DavidsonOptions())
     np.testing.assert_allclose(rep["energies"], res.energies, atol=1e-10)
+
+
+@pytest.mark.gpu
+def test_solve_workers_2_under_torchrun_matches_one_worker(tmp_path):
+    """`solve --workers 2` under torchrun: each rank binds its GPU, joins the group and runs the
+    partitioned native solve; rank 0's report equals the one-worker report (reference test_cli.py:131-140).
+    SBD_SHARE_GPU=1 puts both ranks on the one GPU of the test box."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    args = ["solve", "--gen-random", "10,5,5,3", "--strings", "40", "--nroots", "2", "--json"]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["SBD_SHARE_GPU"] = "1"
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                          "--master-addr=127.0.0.1", "--master-port=29533", "-m", "paper_2601_16637_b200", *args,
+                          "--workers", "2"], cwd=root, capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    reps = [json.loads(out.stdout)]  # one report: rank 0's
+    assert reps[0]["workers"] == 2
+    one = subprocess.run([sys.executable, "-m", "paper_2601_16637_b200", *args], cwd=root, capture_output=True,
+                         text=True, timeout=600, env={k: v for k, v in env.items() if k != "SBD_SHARE_GPU"})
+    ref = json.loads(one.stdout)
+    np.testing.assert_allclose(reps[0]["energies"], ref["energies"], atol=1e-10)
+    assert abs(reps[0]["iterations"] - ref["iterations"]) <= 1
