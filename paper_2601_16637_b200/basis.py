@@ -34,6 +34,7 @@ __all__ = [
     "enumerate_singles",
     "enumerate_doubles",
     "ingest_samples",
+    "parse_sample_lines",
     "det_to_line",
 ]
 
@@ -193,44 +194,66 @@ def _parse_line(line: str, norb: int, line_no: int) -> Determinant:
     return Determinant(a, b)
 
 
+def parse_sample_lines(lines: Union[str, Iterable[str]], norb: int):
+    """Sampled 0/1 text lines -> (alpha uint64[n], beta uint64[n]) in file order (host text layer).
+
+    Reference line format (``basis.py:231-248``): 2*norb characters, leftmost =
+    orbital 0 of alpha; blank lines and '#' comments skipped; the first
+    malformed line raises SampleFormatError with its 1-based line number.
+    """
+    if isinstance(lines, str):
+        lines = lines.splitlines()
+    kept, nos = [], []
+    for line_no, raw in enumerate(lines, start=1):
+        line = raw.strip()
+        if not line or line[0] == "#":
+            continue
+        kept.append(line)
+        nos.append(line_no)
+    n = len(kept)
+    if n == 0:
+        return np.zeros(0, np.uint64), np.zeros(0, np.uint64)
+    w = 2 * norb
+    lens = np.fromiter(map(len, kept), dtype=np.int64, count=n)
+    text = "".join(kept)
+    ascii_ok = text.isascii()
+    if ascii_ok and (lens == w).all():
+        chars = np.frombuffer(text.encode("ascii"), dtype=np.uint8).reshape(n, w)
+        bad_rows = np.nonzero(((chars != 48) & (chars != 49)).any(axis=1))[0]
+        first_bad = int(bad_rows[0]) if bad_rows.size else n
+    else:
+        first_bad = 0  # locate the first malformed line the slow way below
+    if first_bad < n:
+        for line, line_no in zip(kept[first_bad:], nos[first_bad:]):
+            _parse_line(line, norb, line_no)  # raises at the first malformed line, reference order
+    bits = chars == 49
+    weights = np.zeros((n, 64), dtype=bool)
+
+    def pack(block):
+        weights[:, :norb] = block
+        return np.packbits(weights, axis=1, bitorder="little").view(np.uint64).reshape(n)
+
+    return pack(bits[:, :norb]).copy(), pack(bits[:, norb:]).copy()
+
+
 def ingest_samples(lines: Union[str, Iterable[str]], norb: int, n_alpha_elec: int,
-                   n_beta_elec: int, mode: str = "product"):
+                   n_beta_elec: int, mode: str = "product", device=None):
     """Sampled 0/1 lines -> (SelectedBasis, IngestReport); first-seen order kept.
 
     Contract of reference ``basis.py:251-313``: leftmost character is orbital
     0 of alpha; blank and '#' lines skipped; wrong popcounts filtered;
     duplicates dropped; product mode spans unique alpha x unique beta halves.
+    The text is parsed on the host (``parse_sample_lines``); filtering,
+    deduplication, multiplicities and the unique halves run on the GPU
+    (``sbd_ingest_samples`` via ``ingest_sample_arrays``).
     """
+    from .ingest import ingest_sample_arrays
+
     mode = mode.lower()
     if mode not in ("product", "explicit"):
         raise ValueError(f"mode must be 'product' or 'explicit', got {mode!r}")
-    if isinstance(lines, str):
-        lines = lines.splitlines()
-    counts: Counter = Counter()
-    uniq: dict = {}
-    a_seen: dict = {}
-    b_seen: dict = {}
-    n_lines = n_filtered = n_dup = 0
-    for line_no, raw in enumerate(lines, start=1):
-        line = raw.strip()
-        if not line or line[0] == "#":
-            continue
-        n_lines += 1
-        det = _parse_line(line, norb, line_no)
-        if popcount(det.alpha) != n_alpha_elec or popcount(det.beta) != n_beta_elec:
-            n_filtered += 1
-            continue
-        counts[det] += 1
-        if det in uniq:
-            n_dup += 1
-            continue
-        uniq[det] = None
-        a_seen.setdefault(det.alpha, None)
-        b_seen.setdefault(det.beta, None)
-    report = IngestReport(n_lines, n_filtered, n_dup, counts)
-    if mode == "product":
-        return SelectedBasis.product(a_seen, b_seen, norb, n_alpha_elec, n_beta_elec), report
-    return SelectedBasis.explicit(uniq, norb, n_alpha_elec, n_beta_elec), report
+    a, b = parse_sample_lines(lines, norb)
+    return ingest_sample_arrays(a, b, norb, n_alpha_elec, n_beta_elec, mode=mode, device=device)
 
 
 @dataclass

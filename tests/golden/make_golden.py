@@ -225,11 +225,82 @@ def make_explicit():
         json.dump(meta, f, indent=1, sort_keys=True)
 
 
+def _sample_lines(rng, norb, na, nb, n, pool, seed):
+    """Sample-file lines with the reference format's corner cases: '#' comments, blank and padded lines,
+    wrong electron counts (filtered) and heavy duplication (a small pool of strings)."""
+    from sbdiag.synth import random_product_basis
+
+    basis = random_product_basis(norb, na, nb, pool, pool, seed)
+    A, B = list(basis.alpha_strings), list(basis.beta_strings)
+    bits = lambda w: "".join("1" if w >> p & 1 else "0" for p in range(norb))  # noqa: E731
+    lines = ["# sampled configurations", ""]
+    for i in range(n):
+        r = rng.random()
+        if r < 0.03:
+            lines.append("# comment " + str(i))
+        elif r < 0.05:
+            lines.append("   ")
+        elif r < 0.12:  # one electron short in alpha or beta: filtered
+            a = A[rng.integers(len(A))] if rng.random() < 0.5 else (A[rng.integers(len(A))] & ~(1 << (A[0].bit_length() - 1)))
+            b = B[rng.integers(len(B))]
+            if bin(a).count("1") == na:
+                b = b & (b - 1)
+            lines.append(bits(a) + bits(b))
+        else:
+            pad = "  " if r > 0.95 else ""
+            lines.append(pad + bits(A[rng.integers(len(A))]) + bits(B[rng.integers(len(B))]) + pad)
+    return lines
+
+
+INGEST_CASES = [(6, 3, 3, 200, 4, 1), (10, 4, 3, 1500, 25, 2), (12, 6, 6, 2500, 120, 3), (20, 5, 5, 2000, 900, 4)]
+
+
+def make_ingest():
+    """Reference ingest_samples (basis.py:251-313) + the CLI start vector (cli.py:117-128) on sample files."""
+    from sbdiag.basis import ingest_samples
+    from sbdiag.cli import _start_vector
+
+    rng = np.random.default_rng(2024)
+    out = []
+    for norb, na, nb, n, pool, seed in INGEST_CASES:
+        lines = _sample_lines(rng, norb, na, nb, n, pool, seed)
+        case = dict(norb=norb, na=na, nb=nb, lines=lines, modes={})
+        out.append(case)
+        for mode in ("product", "explicit"):
+            basis, rep = ingest_samples(lines, norb, na, nb, mode)
+            x0 = _start_vector(basis, rep.det_counts)
+            nz = np.nonzero(x0)[0]
+            rec = dict(n_lines=rep.n_lines,
+                       n_filtered=rep.n_filtered, n_duplicates=rep.n_duplicates,
+                       det_counts=[[int(d.alpha), int(d.beta), int(c)] for d, c in rep.det_counts.items()],
+                       start_nz=nz.tolist(), start_val=x0[nz].tolist(), dimension=basis.dimension)
+            if mode == "product":
+                rec.update(alpha=[int(v) for v in basis.alpha_strings], beta=[int(v) for v in basis.beta_strings])
+            else:
+                rec.update(dets=[[int(d.alpha), int(d.beta)] for d in basis.dets])
+            case["modes"][mode] = rec
+    with open(os.path.join(HERE, "ingest.json"), "w") as f:
+        json.dump(out, f)
+    # files for the CLI --fcidump/--samples cases
+    from sbdiag.integrals import write_fcidump
+
+    table = synth.random_integrals(8, seed=11)
+    with open(os.path.join(HERE, "cli_case.fcidump"), "w") as f:
+        f.write(write_fcidump(table, nelec=7, ms2=1))
+    with open(os.path.join(HERE, "cli_case.samples"), "w") as f:
+        f.write("\n".join(_sample_lines(np.random.default_rng(5), 8, 4, 3, 400, 14, 12)) + "\n")
+
+
 CLI_CASES = [
     ["solve", "--gen-random", "8,4,4,3", "--strings", "30", "--json"],
     ["solve", "--gen-random", "10,5,4,7", "--strings", "60", "--nroots", "2", "--json"],
     ["solve", "--gen-random", "8,3,3,5", "--strings", "200", "--mode", "explicit", "--json"],
     ["verify", "--gen-random", "6,3,3,2", "--strings", "20", "--json"],
+    ["solve", "--fcidump", "{golden}/cli_case.fcidump", "--samples", "{golden}/cli_case.samples", "--nroots", "2",
+     "--json"],
+    ["solve", "--fcidump", "{golden}/cli_case.fcidump", "--samples", "{golden}/cli_case.samples", "--mode",
+     "explicit", "--json"],
+    ["verify", "--fcidump", "{golden}/cli_case.fcidump", "--samples", "{golden}/cli_case.samples", "--json"],
 ]
 
 
@@ -244,7 +315,7 @@ def make_cli():
     for argv in CLI_CASES:
         buf = io.StringIO()
         with contextlib.redirect_stdout(buf):
-            rc = main(list(argv))
+            rc = main([a.format(golden=HERE) for a in argv])
         rep = json.loads(buf.getvalue())
         for k in ("solve_seconds", "apply_seconds"):
             rep.pop(k, None)
@@ -254,7 +325,7 @@ def make_cli():
 
 
 if __name__ == "__main__":
-    jobs = dict(small=make_small, cli=make_cli, cfg1=make_cfg1, cfg2=make_cfg2, cfg4=make_cfg4, explicit=make_explicit,
+    jobs = dict(small=make_small, cli=make_cli, ingest=make_ingest, cfg1=make_cfg1, cfg2=make_cfg2, cfg4=make_cfg4, explicit=make_explicit,
                 **{"cfg1-davidson": make_cfg1_davidson})
     for arg in sys.argv[1:]:
         jobs[arg]()

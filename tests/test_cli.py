@@ -38,17 +38,24 @@ def test_parser_matches_reference_flags():
     assert (b.workers_list, b.repeats) == ("1", 2)
 
 
+def _n_cli_cases():
+    with open(GOLDEN) as f:
+        return len(json.load(f))
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", range(4))
+@pytest.mark.parametrize("case", range(_n_cli_cases()))
 def test_reports_match_reference_cli(case, capsys):
+    """Reference CLI reports: --gen-random instances and an FCIDUMP + sample-file instance (device ingestion)."""
     with open(GOLDEN) as f:
         ref = json.load(f)[case]
-    rc = main(list(ref["argv"]))
+    rc = main([a.format(golden=os.path.dirname(GOLDEN)) for a in ref["argv"]])
     rep = json.loads(capsys.readouterr().out)
     assert rc == ref["rc"]
     r = ref["report"]
     assert rep["schema_version"] == r["schema_version"] and rep["command"] == r["command"]
     assert rep["basis"] == r["basis"]
+    assert rep.get("ingest") == r.get("ingest")  # n_lines / n_filtered / n_duplicates of the sample file
     if r["command"] == "solve":
         np.testing.assert_allclose(rep["energies"], r["energies"], atol=1e-8)
         assert rep["converged"] == r["converged"]

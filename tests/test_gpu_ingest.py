@@ -1,7 +1,9 @@
-"""Device ingestion against the reference semantics of ingest_samples (basis.py:251-313).
+"""Device ingestion against the reference's own ingest_samples (basis.py:251-313).
 
-The host ``ingest_samples`` (same contract, tested in test_host.py) is the checker for small
-sample sets; a numpy restatement (np.unique + first indices) checks a 2e6-sample set.
+tests/golden/ingest.json holds the reference's outputs (make_golden.py ingest) on sample files with
+comments, blank and padded lines, filtered lines and duplicates, in both modes, plus the reference
+CLI's start vector (cli.py:117-128).  A numpy restatement (np.unique + first indices) checks a
+2e6-sample set.
 """
 
 from __future__ import annotations
@@ -25,25 +27,35 @@ def _samples(rng, norb, na, nb, n, pool, bad_frac=0.1):
     return a, b
 
 
-@pytest.mark.parametrize("mode", ["product", "explicit"])
-def test_ingest_matches_host_reference_semantics(mode):
-    from paper_2601_16637_b200 import det_to_line, ingest_sample_arrays, ingest_samples, start_vector
-    from paper_2601_16637_b200.basis import Determinant
+def _golden_ingest():
+    import json
+    import os
 
-    rng = np.random.default_rng(5)
-    norb, na, nb = 10, 4, 3
-    a, b = _samples(rng, norb, na, nb, 3000, pool=40)
-    lines = [det_to_line(Determinant(int(x), int(y)), norb) for x, y in zip(a, b)]
-    hb, hr = ingest_samples(lines, norb, na, nb, mode=mode)
-    db, dr = ingest_sample_arrays(a, b, norb, na, nb, mode=mode)
-    assert (dr.n_lines, dr.n_filtered, dr.n_duplicates) == (hr.n_lines, hr.n_filtered, hr.n_duplicates)
-    assert dr.det_counts == hr.det_counts
-    assert list(dr.det_counts) == list(hr.det_counts)  # first-seen order of the Counter too
+    with open(os.path.join(os.path.dirname(__file__), "golden", "ingest.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("case", range(4))
+@pytest.mark.parametrize("mode", ["product", "explicit"])
+def test_ingest_matches_reference(case, mode):
+    from paper_2601_16637_b200 import ingest_samples, start_vector
+
+    g = _golden_ingest()[case]
+    r = g["modes"][mode]
+    basis, rep = ingest_samples(g["lines"], g["norb"], g["na"], g["nb"], mode=mode)
+    assert (rep.n_lines, rep.n_filtered, rep.n_duplicates) == (r["n_lines"], r["n_filtered"], r["n_duplicates"])
+    # multiplicities, in the reference Counter's first-seen order
+    assert [[int(d.alpha), int(d.beta), int(c)] for d, c in rep.det_counts.items()] == r["det_counts"]
+    assert basis.dimension == r["dimension"]
     if mode == "product":
-        assert db.alpha_strings == hb.alpha_strings and db.beta_strings == hb.beta_strings
+        assert [int(v) for v in basis.alpha_strings] == r["alpha"]
+        assert [int(v) for v in basis.beta_strings] == r["beta"]
     else:
-        assert list(db.dets) == list(hb.dets)
-    np.testing.assert_array_equal(start_vector(db, dr), start_vector(hb, hr))
+        assert [[int(d.alpha), int(d.beta)] for d in basis.dets] == r["dets"]
+    x0 = start_vector(basis, rep)
+    want = np.zeros(basis.dimension)
+    want[r["start_nz"]] = r["start_val"]
+    np.testing.assert_array_equal(x0, want)
 
 
 def test_ingest_large_vs_numpy():

@@ -82,14 +82,21 @@ def test_basis_validation_and_index():
         SelectedBasis.explicit([(1, 1), (1, 1)], 2, 1, 1)
 
 
-def test_ingest_first_seen_order_and_counts():
-    from paper_2601_16637_b200 import ingest_samples
+def test_sample_line_parser():
+    """Host text layer of ingest_samples (reference basis.py:231-248): bit order, skips, error lines."""
+    from paper_2601_16637_b200.basis import SampleFormatError, parse_sample_lines
 
-    lines = ["# comment", "1100" + "0011", "1010" + "0101", "1100" + "0011", "1110" + "0011", ""]
-    basis, rep = ingest_samples(lines, 4, 2, 2)
-    assert basis.alpha_strings == [0b0011, 0b0101] and basis.beta_strings == [0b1100, 0b1010]
-    assert (rep.n_lines, rep.n_filtered, rep.n_duplicates) == (4, 1, 1)
-    assert sum(rep.det_counts.values()) == 3
+    lines = ["# comment", "1100" + "0011", "  1010" + "0101  ", "", "1100" + "0011", "1110" + "0011"]
+    a, b = parse_sample_lines(lines, 4)
+    assert a.tolist() == [0b0011, 0b0101, 0b0011, 0b0111] and b.tolist() == [0b1100, 0b1010, 0b1100, 0b1100]
+    a, b = parse_sample_lines("\n".join(["1" * 32 + "0" * 32, "0" * 63 + "1"]), 32)
+    assert a.tolist() == [(1 << 32) - 1, 0] and b.tolist() == [0, 1 << 31]
+    with pytest.raises(SampleFormatError, match="line 3"):
+        parse_sample_lines(["11000011", "#", "1100001"], 4)
+    with pytest.raises(SampleFormatError, match="line 2.*'2'"):
+        parse_sample_lines(["11000011", "11002011", "110"], 4)  # the earlier line's error wins
+    with pytest.raises(SampleFormatError, match="line 1"):
+        parse_sample_lines(["1100001\u00e9"], 4)
 
 
 def test_host_enumerators_match_golden(small_golden):
