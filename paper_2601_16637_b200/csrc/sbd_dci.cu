@@ -1,0 +1,380 @@
+// Task 0 in the dense regime as a contraction on the fp64 tensor cores.
+//
+// Reference: the alpha-single x beta-single opposite-spin doubles of
+// _product_row (apply.py:228-238):
+//   sigma[ia, ib] += sum_{k in aS(ia)} sum_{m in bS(ib)} s_k s_m (Pa_k | Pb_m) X[ja_k, jb_m]
+//
+// The SELL kernels (sbd_sigma.cu) evaluate that sum term by term: one shared
+// load, two shared gathers and one FMA per (k, m) pair, 36 x 36 = 1296 terms
+// per determinant for the full 12-orbital set.  When most candidate beta
+// singles are in the set (the full string space, cfg1), the same sum factors
+// through the pair index (the direct-CI form):
+//   G[q][jb]     = sum_k  s_k (Pa_k | Q_q) X[ja_k, jb]          (a GEMM, K = |aS(ia)|)
+//   sigma[ia,ib] = sum_m  s_m G[q(Pb_m)][jb_m]                  (36 gathers per determinant)
+// with q over the norb (norb - 1) / 2 off-diagonal orbital pairs.
+//
+// Kernel: one persistent CTA per SM walks its alpha rows; a row's beta
+// columns jb are cut into tiles of NT (128, or 64 when shared memory is short).  Per (row, tile):
+//   1. the row's K x NT slab of x (rows ja_k) is staged by cp.async, one
+//      tile ahead (double buffer);
+//   2. G tile (nqp x NT) = E (nqp x Kp, built per row from the pair-pair
+//      ERI matrix and the alpha phases) times the slab, on DMMA.8x8x4:
+//      warp w owns the 8 columns w*8.. of the tile and every row fragment;
+//   3. each thread owns beta positions ib and adds the G entries its beta
+//      singles point at inside this tile (lists sorted by jb, cut per tile),
+//      so every sigma element is summed by one thread in a fixed order: no
+//      atomics, bitwise reproducible.
+// The row is written once (or added, for the additive task-0 order).
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+#include "sbd_internal.cuh"
+#include "sbd_ptx.cuh"
+
+namespace {
+
+constexpr int kDciThreads = 512;          // 16 warps
+constexpr int kDciWarps = kDciThreads / 32;
+constexpr int kMaxSingles = 64;           // beta singles per string handled by the list builder
+constexpr size_t kDciSmemMax = 227 * 1024;
+// beta columns per tile: 128 (warp w owns the 8-column fragment w and every row fragment) or, when
+// that does not fit shared memory, 64 (warps w and w + 8 share fragment w % 8, halving the rows)
+template <int NT>
+struct Tile {
+    static constexpr int kLdX = NT + 4;    // slab row stride (doubles): B-fragment loads conflict-free
+    static constexpr int kLdG = NT + 8;    // G row stride: C-fragment double2 stores conflict-free
+    static constexpr int kNfr = NT / 8;    // column fragments
+    static constexpr int kMsplit = kDciWarps / kNfr;  // warps per column fragment
+};
+
+struct DciArgs {
+    i64 n_rows, row_base, nb;
+    const double *X;
+    double *Y;
+    const int64_t *a_s_off;
+    const SConn *a_sconn;
+    const double *eq;        // [npair][nqp]: (P | Q_q), zero for q >= nq
+    int nqp, kp_max, ld_e;   // ld_e = 4 (mod 16) doubles: A-fragment loads conflict-free
+    const uint32_t *ent;     // beta singles of each ib sorted by jb: (jb - t NT) << 16 | q << 1 | neg
+    const int32_t *toff;     // [nb][ntiles + 1]: first entry of tile t (absolute index into ent)
+    int ntiles;
+    bool add;
+};
+
+__host__ __device__ inline size_t dci_smem(int nt, int nqp, int kp_max, int ld_e) {
+    return sizeof(double) * ((size_t)nqp * ld_e + 2 * (size_t)kp_max * (nt + 4) + (size_t)nqp * (nt + 8));
+}
+__host__ __device__ inline int dci_ld_e(int kp) { return kp + (((4 - kp) % 16) + 16) % 16; }
+
+// Stage rows ja_k (k < K) of x, columns [t NT, t NT + NT), into `xs`; rows K..Kp-1 and
+// columns past nb are zero (E is zero there too, but the slab must not hold NaNs).
+template <int NT>
+__device__ __forceinline__ void dci_stage(const DciArgs &a, double *xs, i64 row, int t, int K, int Kp) {
+    const i64 e0 = a.a_s_off[row];
+    const i64 c0 = (i64)t * NT;
+    const int cols = (int)min((i64)NT, a.nb - c0);
+    constexpr int kChunks = NT / 2;  // 16-byte chunks per slab row
+    for (int c = threadIdx.x; c < Kp * kChunks; c += kDciThreads) {
+        const int k = c / kChunks, j = c % kChunks;
+        double *dst = xs + k * Tile<NT>::kLdX + 2 * j;
+        if (k < K && 2 * j < cols) {
+            const i64 ja = a.a_sconn[e0 + k].tgt;
+            cp_async16(dst, a.X + ja * a.nb + c0 + 2 * j);
+        } else {
+            *reinterpret_cast<double2 *>(dst) = make_double2(0.0, 0.0);
+        }
+    }
+}
+
+// next row of this CTA that has alpha singles (n_rows if none)
+__device__ __forceinline__ i64 dci_next_row(const DciArgs &a, i64 r) {
+    for (; r < a.n_rows; r += gridDim.x)
+        if (a.a_s_off[a.row_base + r + 1] > a.a_s_off[a.row_base + r]) return r;
+    return a.n_rows;
+}
+
+// MF: row fragments per warp (ceil(nqp / 8 / kMsplit))
+template <int NT, int MF, int PPT>
+__global__ void __launch_bounds__(kDciThreads, 1) cross_kernel_dci(DciArgs a) {
+    using T = Tile<NT>;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    double *es = reinterpret_cast<double *>(dsm);      // [nqp][ld_e]
+    double *xs0 = es + (size_t)a.nqp * a.ld_e;         // 2 x [kp_max][kLdX]
+    double *gs = xs0 + 2 * (size_t)a.kp_max * T::kLdX; // [nqp][kLdG]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nfr = warp % T::kNfr, mpart = warp / T::kNfr;  // column fragment; rows m = mpart + kMsplit j
+    const int mf = a.nqp / 8;
+
+    i64 r = dci_next_row(a, blockIdx.x);
+    if (r >= a.n_rows) return;
+    auto kof = [&](i64 rr) { return (int)(a.a_s_off[a.row_base + rr + 1] - a.a_s_off[a.row_base + rr]); };
+    int K = kof(r), Kp = (K + 3) & ~3;
+    int t = 0, buf = 0;
+    dci_stage<NT>(a, xs0, a.row_base + r, 0, K, Kp);
+    cp_async_commit();
+
+    double acc[PPT];
+#pragma unroll
+    for (int i = 0; i < PPT; ++i) acc[i] = 0.0;
+
+    while (true) {
+        // the item after this one: next tile of the row, else tile 0 of the CTA's next row
+        i64 rn = r;
+        int tn = t + 1;
+        if (tn == a.ntiles) {
+            rn = dci_next_row(a, r + gridDim.x);
+            tn = 0;
+        }
+        const int Kn = rn < a.n_rows ? kof(rn) : 0, Kpn = (Kn + 3) & ~3;
+        if (rn < a.n_rows) dci_stage<NT>(a, xs0 + (size_t)(buf ^ 1) * a.kp_max * T::kLdX, a.row_base + rn, tn, Kn, Kpn);
+        cp_async_commit();
+        if (t == 0) {  // E for this row: E[q][k] = s_k (Pa_k | Q_q); the previous row's GEMM is done
+            const i64 e0 = a.a_s_off[a.row_base + r];
+            for (int i = threadIdx.x; i < a.nqp * Kp; i += kDciThreads) {
+                const int q = i / Kp, k = i % Kp;
+                double v = 0.0;
+                if (k < K) {
+                    const SConn sa = a.a_sconn[e0 + k];
+                    v = __ldg(a.eq + (i64)(abs(sa.info) - 1) * a.nqp + q);
+                    if (sa.info < 0) v = -v;
+                }
+                es[q * a.ld_e + k] = v;
+            }
+        }
+        cp_async_wait<1>();
+        __syncthreads();  // slab `buf` and E visible; the previous gather is done with G
+
+        // G tile = E (nqp x Kp) * slab (Kp x NT): warp -> columns 8 nfr .. 8 nfr + 7, row fragments
+        // mpart, mpart + kMsplit, ...
+        {
+            const double *xs = xs0 + (size_t)buf * a.kp_max * T::kLdX;
+            double d[MF][2];
+#pragma unroll
+            for (int j = 0; j < MF; ++j) d[j][0] = d[j][1] = 0.0;
+            const double *bp = xs + (lane & 3) * T::kLdX + nfr * 8 + (lane >> 2);
+            const double *ap = es + (mpart * 8 + (lane >> 2)) * a.ld_e + (lane & 3);
+            for (int k0 = 0; k0 < Kp; k0 += 4) {
+                const double b = bp[k0 * T::kLdX];
+#pragma unroll
+                for (int j = 0; j < MF; ++j)
+                    if (mpart + j * T::kMsplit < mf)
+                        dmma_8x8x4(d[j][0], d[j][1], ap[j * T::kMsplit * 8 * a.ld_e + k0], b);
+            }
+#pragma unroll
+            for (int j = 0; j < MF; ++j) {
+                const int m = mpart + j * T::kMsplit;
+                if (m < mf)
+                    *reinterpret_cast<double2 *>(gs + (m * 8 + (lane >> 2)) * T::kLdG + nfr * 8 + 2 * (lane & 3)) =
+                        make_double2(d[j][0], d[j][1]);
+            }
+        }
+        __syncthreads();  // G tile complete
+
+        // gather: sigma[ib] += s_m G[q_m][jb_m] for the beta singles of ib that land in tile t
+#pragma unroll
+        for (int i = 0; i < PPT; ++i) {
+            const i64 ib = threadIdx.x + (i64)i * kDciThreads;
+            if (ib < a.nb) {
+                const int32_t *to = a.toff + ib * (a.ntiles + 1) + t;
+                const int lo = __ldg(to), hi = __ldg(to + 1);
+                double s = acc[i];
+                for (int e = lo; e < hi; ++e) {
+                    const uint32_t u = __ldg(a.ent + e);
+                    const double g = gs[((u >> 1) & 0x7fffu) * T::kLdG + (u >> 16)];
+                    s += (u & 1u) ? -g : g;
+                }
+                acc[i] = s;
+            }
+        }
+        if (t == a.ntiles - 1) {
+            double *yr = a.Y + r * a.nb;
+#pragma unroll
+            for (int i = 0; i < PPT; ++i) {
+                const i64 ib = threadIdx.x + (i64)i * kDciThreads;
+                if (ib < a.nb) {
+                    if (a.add) yr[ib] += acc[i];
+                    else yr[ib] = acc[i];
+                }
+                acc[i] = 0.0;
+            }
+        }
+        if (rn >= a.n_rows) break;
+        r = rn;
+        t = tn;
+        K = Kn;
+        Kp = Kpn;
+        buf ^= 1;
+    }
+    cp_async_wait<0>();
+}
+
+// Per beta string: its in-set singles sorted by target, packed for the gather, and the
+// first entry of every column tile.
+__global__ void dci_lists_kernel(i64 nb, const int64_t *__restrict__ s_off, const SConn *__restrict__ sconn,
+                                 const int32_t *__restrict__ qmap, int nt, int ntiles, uint32_t *__restrict__ ent,
+                                 int32_t *__restrict__ toff) {
+    const i64 ib = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ib >= nb) return;
+    const i64 s0 = s_off[ib];
+    const int n = (int)(s_off[ib + 1] - s0);
+    int32_t tg[kMaxSingles];
+    uint32_t code[kMaxSingles];
+    for (int i = 0; i < n; ++i) {
+        const SConn sc = sconn[s0 + i];
+        const int32_t jb = sc.tgt;
+        const uint32_t c = ((uint32_t)qmap[abs(sc.info) - 1] << 1) | (sc.info < 0 ? 1u : 0u);
+        int j = i;
+        while (j > 0 && tg[j - 1] > jb) {
+            tg[j] = tg[j - 1];
+            code[j] = code[j - 1];
+            --j;
+        }
+        tg[j] = jb;
+        code[j] = c;
+    }
+    int i = 0;
+    for (int t = 0; t <= ntiles; ++t) {
+        while (i < n && tg[i] < t * nt) ++i;
+        toff[ib * (ntiles + 1) + t] = (int32_t)(s0 + i);
+    }
+    for (int k = 0; k < n; ++k) ent[s0 + k] = ((uint32_t)(tg[k] % nt) << 16) | code[k];
+}
+
+// eq[P][q] = (P | Q_q) over the off-diagonal pairs Q_q, zero for q >= nq
+__global__ void dci_eq_kernel(i64 npair, int nq, int nqp, const int32_t *__restrict__ qpair,
+                              const double *__restrict__ eri, double *__restrict__ eq) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npair * nqp) return;
+    const i64 P = i / nqp;
+    const int q = (int)(i % nqp);
+    eq[i] = q < nq ? eri[tri_idx(P, qpair[q])] : 0.0;
+}
+
+int dci_build(sbd_ctx *ctx) {
+    DciState &d = ctx->dci;
+    if (d.valid) return SBD_OK;
+    const Sector &A = ctx->sec[0], &B = ctx->sec[1];
+    const int norb = ctx->norb;
+    d.nq = norb * (norb - 1) / 2;
+    d.nqp = std::max(8, (d.nq + 7) / 8 * 8);
+    std::vector<int32_t> qmap(ctx->npair, 0), qpair(d.nq);
+    int q = 0;
+    for (int p = 1; p < norb; ++p)
+        for (int r = 0; r < p; ++r) {
+            qmap[tri_idx(p, r)] = q;
+            qpair[q++] = (int32_t)tri_idx(p, r);
+        }
+    // largest single count per alpha / beta string (host copies of the offsets)
+    auto max_count = [&](const Sector &s, int &mx) -> int {
+        std::vector<int64_t> off(s.n + 1);
+        SBD_CUDA(ctx, cudaMemcpy(off.data(), s.s_off.p, sizeof(int64_t) * (s.n + 1), cudaMemcpyDeviceToHost));
+        mx = 0;
+        for (i64 i = 0; i < s.n; ++i) mx = std::max(mx, (int)(off[i + 1] - off[i]));
+        return SBD_OK;
+    };
+    int ka = 0, kb = 0;
+    int rc = max_count(A, ka);
+    if (rc) return rc;
+    rc = max_count(B, kb);
+    if (rc) return rc;
+    d.kp_max = std::max(4, (ka + 3) & ~3);
+    d.kb_max = kb;
+    d.ld_e = dci_ld_e(d.kp_max);  // = 4 mod 16
+    d.nt = dci_smem(128, d.nqp, d.kp_max, d.ld_e) <= kDciSmemMax ? 128 : 64;
+    d.ntiles = (int)((B.n + d.nt - 1) / d.nt);
+    DevBuf qm, qp;
+    SBD_CUDA(ctx, qm.ensure(sizeof(int32_t) * qmap.size()));
+    SBD_CUDA(ctx, qp.ensure(sizeof(int32_t) * std::max<size_t>(1, qpair.size())));
+    SBD_CUDA(ctx, cudaMemcpy(qm.p, qmap.data(), sizeof(int32_t) * qmap.size(), cudaMemcpyHostToDevice));
+    if (d.nq) SBD_CUDA(ctx, cudaMemcpy(qp.p, qpair.data(), sizeof(int32_t) * qpair.size(), cudaMemcpyHostToDevice));
+    SBD_CUDA(ctx, d.eq.ensure(sizeof(double) * ctx->npair * d.nqp));
+    dci_eq_kernel<<<grid_for(ctx->npair * d.nqp, 256), 256, 0, ctx->stream>>>(ctx->npair, d.nq, d.nqp,
+                                                                               qp.as<int32_t>(), ctx->eri.as<double>(),
+                                                                               d.eq.as<double>());
+    SBD_LAUNCHED(ctx, "dci_eq_kernel");
+    if (kb <= kMaxSingles) {
+        SBD_CUDA(ctx, d.ent.ensure(sizeof(uint32_t) * std::max<i64>(1, B.ns)));
+        SBD_CUDA(ctx, d.toff.ensure(sizeof(int32_t) * B.n * (d.ntiles + 1)));
+        dci_lists_kernel<<<grid_for(B.n, 128), 128, 0, ctx->stream>>>(B.n, B.s_off.as<int64_t>(), B.sconn.as<SConn>(),
+                                                                      qm.as<int32_t>(), d.nt, d.ntiles, d.ent.as<uint32_t>(),
+                                                                      d.toff.as<int32_t>());
+        SBD_LAUNCHED(ctx, "dci_lists_kernel");
+    }
+    SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // qm/qp are released on return
+    d.valid = true;
+    return SBD_OK;
+}
+
+template <int NT, int MF, int PPT>
+int launch_dci(sbd_ctx *ctx, const DciArgs &a, size_t smem) {
+    SBD_CUDA(ctx, sbd_smem_attr((const void *)cross_kernel_dci<NT, MF, PPT>, ctx->device, smem));
+    cross_kernel_dci<NT, MF, PPT><<<(unsigned)ctx->num_sms, kDciThreads, smem, ctx->stream>>>(a);
+    SBD_LAUNCHED(ctx, "cross_kernel_dci");
+    return SBD_OK;
+}
+
+template <int NT, int MF>
+int launch_dci_ppt(sbd_ctx *ctx, const DciArgs &a, size_t smem) {
+    const i64 ppt = (a.nb + kDciThreads - 1) / kDciThreads;
+    if (ppt <= 2) return launch_dci<NT, MF, 2>(ctx, a, smem);
+    if (ppt <= 4) return launch_dci<NT, MF, 4>(ctx, a, smem);
+    return launch_dci<NT, MF, 8>(ctx, a, smem);
+}
+
+}  // namespace
+
+// Whether the direct-CI task 0 serves this context (SBD_CROSS_DCI=0/1 forces it off / on where it can run).
+bool sbd_dci_eligible(sbd_ctx *ctx, const double *x_full) {
+    const Sector &A = ctx->sec[0], &B = ctx->sec[1];
+    const char *env = getenv("SBD_CROSS_DCI");
+    if (env && env[0] == '0') return false;
+    const int norb = ctx->norb, nq = norb * (norb - 1) / 2;
+    const int nqp = std::max(8, (nq + 7) / 8 * 8);
+    if (nqp > 128 || B.n % 2 != 0 || B.n > (i64)kDciThreads * 8 || B.n * (i64)((B.n + 63) / 64 + 1) >= (1ll << 31) ||
+        B.ns >= (1ll << 31) || (reinterpret_cast<uintptr_t>(x_full) & 15) != 0 || A.ns == 0 || B.ns == 0)
+        return false;
+    const int na = A.n_elec, nbe = B.n_elec;
+    if ((i64)na * (norb - na) > 64 || (i64)nbe * (norb - nbe) > kMaxSingles) return false;
+    const int kp = std::max(4, (na * (norb - na) + 3) & ~3);
+    if (dci_smem(64, nqp, kp, dci_ld_e(kp)) > kDciSmemMax) return false;
+    if (env && env[0] == '1') return true;
+    // tensor-core FMAs (nqp per beta column) against SELL terms (in-set beta singles per string):
+    // the contraction runs ~14x faster per FMA than the gathered terms (cfg1 measurement)
+    const double cbar_b = (double)B.ns / (double)std::max<i64>(1, B.n);
+    return 8.0 * cbar_b >= (double)nqp;
+}
+
+int sbd_cross_dci(sbd_ctx *ctx, const double *x_full, double *y, bool additive, const SConn *sconn) {
+    int rc = dci_build(ctx);
+    if (rc) return rc;
+    const DciState &d = ctx->dci;
+    const Sector &A = ctx->sec[0], &B = ctx->sec[1];
+    if (d.kb_max > kMaxSingles) return sbd_fail(ctx, SBD_EINVAL, "direct-CI task 0: too many beta singles per string");
+    DciArgs a{};
+    a.n_rows = ctx->own_rows();
+    a.row_base = ctx->own_lo();
+    a.nb = B.n;
+    a.X = x_full;
+    a.Y = y;
+    a.a_s_off = A.s_off.as<int64_t>();
+    a.a_sconn = sconn ? sconn : A.sconn.as<SConn>();
+    a.eq = d.eq.as<double>();
+    a.nqp = d.nqp;
+    a.kp_max = d.kp_max;
+    a.ld_e = d.ld_e;
+    a.ent = d.ent.as<uint32_t>();
+    a.toff = d.toff.as<int32_t>();
+    a.ntiles = d.ntiles;
+    a.add = additive;
+    const size_t smem = dci_smem(d.nt, d.nqp, d.kp_max, d.ld_e);
+    const int mf = d.nqp / 8;
+    if (d.nt == 128) {
+        if (mf <= 4) return launch_dci_ppt<128, 4>(ctx, a, smem);
+        if (mf <= 8) return launch_dci_ppt<128, 8>(ctx, a, smem);
+        if (mf <= 12) return launch_dci_ppt<128, 12>(ctx, a, smem);
+        return launch_dci_ppt<128, 16>(ctx, a, smem);
+    }
+    if (mf <= 8) return launch_dci_ppt<64, 4>(ctx, a, smem);
+    return launch_dci_ppt<64, 8>(ctx, a, smem);
+}

@@ -105,6 +105,15 @@ struct DistState {
     double total_ms = 0.0;
 };
 
+// direct-CI task 0 (sbd_dci.cu): pair-pair ERI block and the beta singles re-sorted for the gather
+struct DciState {
+    bool valid = false;
+    int nq = 0, nqp = 0, kp_max = 0, kb_max = 0, ld_e = 0, nt = 128, ntiles = 0;
+    DevBuf eq;    // f64 [npair][nqp]
+    DevBuf ent;   // u32 [beta singles], per beta string sorted by target
+    DevBuf toff;  // int32 [n_beta][ntiles + 1]
+};
+
 // device ingestion results (sbd_ingest.cu), first-seen order
 struct IngestState {
     DevBuf det_a, det_b, det_count, alpha, beta;
@@ -148,6 +157,7 @@ struct sbd_ctx {
     bool explicit_built = false;
     IngestState ingest;
     DistState dist;
+    DciState dci;
 
     i64 own_lo() const { return row_lo; }
     i64 own_hi() const { return row_hi < 0 ? sec[0].n : row_hi; }
@@ -208,6 +218,9 @@ int sbd_beta_side(sbd_ctx *ctx, const double *x_own);      // transpose + beta s
 int sbd_alpha_pass(sbd_ctx *ctx, const double *X, double *y, const Conn *conn, const int64_t *seg_off, i64 stride,
                    int s_lo, int s_hi, i64 xo_row0, bool epi, bool acc_in);
 int sbd_cross_add(sbd_ctx *ctx, const double *X, double *y, const SConn *sconn);  // y += task 0
+// direct-CI task 0 on the fp64 tensor cores (sbd_dci.cu): dense string sets
+bool sbd_dci_eligible(sbd_ctx *ctx, const double *x_full);
+int sbd_cross_dci(sbd_ctx *ctx, const double *x_full, double *y, bool additive, const SConn *sconn);
 void sbd_dist_release(sbd_ctx *ctx);                        // sbd_dist.cu (called by sbd_destroy)
 int sbd_dist_allreduce_internal(sbd_ctx *ctx, double *buf, i64 n, int op);  // 0 sum, 1 max, 2 min; no-op on 1 rank
 int sbd_dist_check_internal(sbd_ctx *ctx);                  // NCCL asynchronous error -> SBD_ECUDA

@@ -233,13 +233,6 @@ struct SideAsync {
     static constexpr size_t smem() { return sizeof(double) * (size_t)kRowsPerCta * kRing * kTW; }
 };
 
-__device__ __forceinline__ void cp_async16(void *dst_smem, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
 template <bool ALPHA, bool DIST = false>
 __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async(SideArgs a) {
     const bool EPI = ALPHA && (!DIST || a.epi);  // uniform per launch
@@ -919,6 +912,7 @@ bool cross_additive(const sbd_ctx *ctx) {
 
 int launch_cross(sbd_ctx *ctx, const double *x_full, double *y, bool additive = false,
                  const SConn *sconn = nullptr) {
+    if (sbd_dci_eligible(ctx, x_full)) return sbd_cross_dci(ctx, x_full, y, additive, sconn);
     const Sector &A = ctx->sec[0], &B = ctx->sec[1];
     CrossArgs ca{};
     ca.n_rows = ctx->own_rows();

@@ -230,3 +230,4 @@ def test_native_driver_explicit_basis(explicit_golden, explicit_meta):
         assert nat.converged and nat.stats.iterations == py.stats.iterations
         np.testing.assert_allclose(nat.energies, explicit_golden[f"{name}/energies"], atol=1e-8)
         np.testing.assert_allclose(nat.energies, py.energies, atol=1e-10, rtol=0)
+

@@ -219,3 +219,38 @@ def test_dense_rows_match_oracle_elements():
     ref = O.dense(inst)
     assert np.abs(dense - ref).max() <= 1e-12 * np.abs(ref).max()
     assert np.array_equal(dense, dense.T) or np.abs(dense - dense.T).max() <= 1e-14 * np.abs(dense).max()
+
+
+@pytest.mark.parametrize("env", [{"SBD_CROSS_DCI": "1"}, {"SBD_CROSS_DCI": "1", "SBD_CROSS_ADD": "1"}],
+                         ids=["dci", "dci-additive"])
+def test_direct_ci_task0_vs_oracle(env, monkeypatch):
+    """Task 0 as the fp64 tensor-core contraction (sbd_dci.cu), forced on every shape it serves:
+    K not a multiple of 4, 1-8 beta positions per thread, 9-15 row fragments (norb 12-16), partial
+    last column tile, row windows, host (pipelined) and device paths."""
+    import torch
+
+    from paper_2601_16637_b200 import HamiltonianApplier, SelectedBasis
+    from paper_2601_16637_b200.synth import random_integrals, random_product_strings
+
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    cases = [(12, 6, 6, 924, 924, 1), (12, 5, 6, 500, 862, 2), (13, 4, 5, 300, 1286, 3), (14, 7, 3, 400, 364, 4),
+             (16, 3, 8, 200, 3000, 5), (14, 3, 7, 200, 3000, 8), (9, 2, 3, 36, 84, 6), (12, 1, 11, 12, 12, 7)]
+    for norb, na, nb, nsa, nsb, seed in cases:
+        a, _ = random_product_strings(norb, na, na, nsa, 1, seed)
+        _, b = random_product_strings(norb, nb, nb, 1, nsb, seed + 50)
+        table = random_integrals(norb, seed)
+        basis = SelectedBasis.product(a.tolist(), b.tolist(), norb, na, nb)
+        inst = O.Instance.make(norb, table.h, table.eri, table.e_core, a, b)
+        x = np.random.default_rng(seed).standard_normal(basis.dimension)
+        ref = O.sigma(inst, x)
+        app = HamiltonianApplier(basis, table)
+        yh = app(x)
+        yd = app.sigma_device(torch.from_numpy(x).cuda()).cpu().numpy()
+        for y in (yh, yd):
+            assert np.abs(y - ref).max() <= 1e-10 * np.abs(ref).max(), (norb, na, nb, nsa, nsb)
+        assert np.array_equal(app.sigma_device(torch.from_numpy(x).cuda()).cpu().numpy(), yd)  # reproducible
+        lo, hi = nsa // 3, nsa // 3 + max(1, nsa // 4)
+        win = HamiltonianApplier(basis, table, row_window=(lo, hi))
+        yw = win(x)
+        assert np.abs(yw - ref[lo * nsb:hi * nsb]).max() <= 1e-10 * np.abs(ref).max()
