@@ -254,6 +254,9 @@ typedef struct sbd_davidson_opts {
     double precond_delta;    /* 1e-6 */
     int reorthogonalize;     /* 1 */
     int track_orthogonality; /* 1: ortho_hist[i] = ||G - I||_F from the fused Gram row */
+    int selective_reorth;    /* 0 (reference: always two passes).  1: skip the second
+                                Gram-Schmidt pass when |t1| >= |t0| / sqrt(2) after the first
+                                ("twice is enough"); B200 extension, reported separately */
 } sbd_davidson_opts;
 
 /* DavidsonStats (davidson.py:56-68).  The history pointers are optional

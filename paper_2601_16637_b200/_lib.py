@@ -76,7 +76,7 @@ class DavidsonOptsC(ctypes.Structure):
     """``sbd_davidson_opts`` (include/sbd.h)."""
     _fields_ = [("n_roots", _c_int), ("tol_residual", _c_dbl), ("max_iters", _c_int), ("max_subspace", _c_int),
                 ("restart_keep", _c_int), ("precond_delta", _c_dbl), ("reorthogonalize", _c_int),
-                ("track_orthogonality", _c_int)]
+                ("track_orthogonality", _c_int), ("selective_reorth", _c_int)]
 
 
 class DavidsonStatsC(ctypes.Structure):

@@ -14,7 +14,7 @@
 // with q over the norb (norb - 1) / 2 off-diagonal orbital pairs.
 //
 // Kernel: one persistent CTA per SM walks its alpha rows; a row's beta
-// columns jb are cut into tiles of NT (128, or 64 when shared memory is short).  Per (row, tile):
+// columns jb are cut into tiles of NT (64, or 32 when shared memory is short).  Per (row, tile):
 //   1. the row's K x NT slab of x (rows ja_k) is staged by cp.async, one
 //      tile ahead (double buffer);
 //   2. G tile (nqp x NT) = E (nqp x Kp, built per row from the pair-pair
@@ -34,12 +34,12 @@
 
 namespace {
 
-constexpr int kDciThreads = 512;          // 16 warps
+constexpr int kDciThreads = 256;          // 8 warps; two CTAs per SM when shared memory allows
 constexpr int kDciWarps = kDciThreads / 32;
 constexpr int kMaxSingles = 64;           // beta singles per string handled by the list builder
 constexpr size_t kDciSmemMax = 227 * 1024;
-// beta columns per tile: 128 (warp w owns the 8-column fragment w and every row fragment) or, when
-// that does not fit shared memory, 64 (warps w and w + 8 share fragment w % 8, halving the rows)
+// beta columns per tile: 64 (warp w owns the 8-column fragment w and every row fragment) or, when
+// that does not fit shared memory, 32 (warps w and w + 4 share fragment w % 4, halving the rows)
 template <int NT>
 struct Tile {
     static constexpr int kLdX = NT + 4;    // slab row stride (doubles): B-fragment loads conflict-free
@@ -96,7 +96,7 @@ __device__ __forceinline__ i64 dci_next_row(const DciArgs &a, i64 r) {
 
 // MF: row fragments per warp (ceil(nqp / 8 / kMsplit))
 template <int NT, int MF, int PPT>
-__global__ void __launch_bounds__(kDciThreads, 1) cross_kernel_dci(DciArgs a) {
+__global__ void __launch_bounds__(kDciThreads, 2) cross_kernel_dci(DciArgs a) {
     using T = Tile<NT>;
     extern __shared__ __align__(128) unsigned char dsm[];
     double *es = reinterpret_cast<double *>(dsm);      // [nqp][ld_e]
@@ -154,12 +154,16 @@ __global__ void __launch_bounds__(kDciThreads, 1) cross_kernel_dci(DciArgs a) {
             for (int j = 0; j < MF; ++j) d[j][0] = d[j][1] = 0.0;
             const double *bp = xs + (lane & 3) * T::kLdX + nfr * 8 + (lane >> 2);
             const double *ap = es + (mpart * 8 + (lane >> 2)) * a.ld_e + (lane & 3);
+            const int stride_a = T::kMsplit * 8 * a.ld_e;
             for (int k0 = 0; k0 < Kp; k0 += 4) {
+                // all operands of the k-step first (one shared-memory round trip), then the DMMAs
                 const double b = bp[k0 * T::kLdX];
+                double av[MF];
+#pragma unroll
+                for (int j = 0; j < MF; ++j) av[j] = mpart + j * T::kMsplit < mf ? ap[j * stride_a + k0] : 0.0;
 #pragma unroll
                 for (int j = 0; j < MF; ++j)
-                    if (mpart + j * T::kMsplit < mf)
-                        dmma_8x8x4(d[j][0], d[j][1], ap[j * T::kMsplit * 8 * a.ld_e + k0], b);
+                    if (mpart + j * T::kMsplit < mf) dmma_8x8x4(d[j][0], d[j][1], av[j], b);
             }
 #pragma unroll
             for (int j = 0; j < MF; ++j) {
@@ -281,7 +285,7 @@ int dci_build(sbd_ctx *ctx) {
     d.kp_max = std::max(4, (ka + 3) & ~3);
     d.kb_max = kb;
     d.ld_e = dci_ld_e(d.kp_max);  // = 4 mod 16
-    d.nt = dci_smem(128, d.nqp, d.kp_max, d.ld_e) <= kDciSmemMax ? 128 : 64;
+    d.nt = dci_smem(64, d.nqp, d.kp_max, d.ld_e) <= kDciSmemMax ? 64 : 32;
     d.ntiles = (int)((B.n + d.nt - 1) / d.nt);
     DevBuf qm, qp;
     SBD_CUDA(ctx, qm.ensure(sizeof(int32_t) * qmap.size()));
@@ -309,7 +313,8 @@ int dci_build(sbd_ctx *ctx) {
 template <int NT, int MF, int PPT>
 int launch_dci(sbd_ctx *ctx, const DciArgs &a, size_t smem) {
     SBD_CUDA(ctx, sbd_smem_attr((const void *)cross_kernel_dci<NT, MF, PPT>, ctx->device, smem));
-    cross_kernel_dci<NT, MF, PPT><<<(unsigned)ctx->num_sms, kDciThreads, smem, ctx->stream>>>(a);
+    const unsigned per_sm = 2 * (smem + 1024) <= 228 * 1024 ? 2 : 1;  // two CTAs: one gathers while one multiplies
+    cross_kernel_dci<NT, MF, PPT><<<(unsigned)ctx->num_sms * per_sm, kDciThreads, smem, ctx->stream>>>(a);
     SBD_LAUNCHED(ctx, "cross_kernel_dci");
     return SBD_OK;
 }
@@ -319,7 +324,8 @@ int launch_dci_ppt(sbd_ctx *ctx, const DciArgs &a, size_t smem) {
     const i64 ppt = (a.nb + kDciThreads - 1) / kDciThreads;
     if (ppt <= 2) return launch_dci<NT, MF, 2>(ctx, a, smem);
     if (ppt <= 4) return launch_dci<NT, MF, 4>(ctx, a, smem);
-    return launch_dci<NT, MF, 8>(ctx, a, smem);
+    if (ppt <= 8) return launch_dci<NT, MF, 8>(ctx, a, smem);
+    return launch_dci<NT, MF, 16>(ctx, a, smem);
 }
 
 }  // namespace
@@ -331,13 +337,13 @@ bool sbd_dci_eligible(sbd_ctx *ctx, const double *x_full) {
     if (env && env[0] == '0') return false;
     const int norb = ctx->norb, nq = norb * (norb - 1) / 2;
     const int nqp = std::max(8, (nq + 7) / 8 * 8);
-    if (nqp > 128 || B.n % 2 != 0 || B.n > (i64)kDciThreads * 8 || B.n * (i64)((B.n + 63) / 64 + 1) >= (1ll << 31) ||
+    if (nqp > 128 || B.n % 2 != 0 || B.n > (i64)kDciThreads * 16 || B.n * (i64)((B.n + 31) / 32 + 1) >= (1ll << 31) ||
         B.ns >= (1ll << 31) || (reinterpret_cast<uintptr_t>(x_full) & 15) != 0 || A.ns == 0 || B.ns == 0)
         return false;
     const int na = A.n_elec, nbe = B.n_elec;
     if ((i64)na * (norb - na) > 64 || (i64)nbe * (norb - nbe) > kMaxSingles) return false;
     const int kp = std::max(4, (na * (norb - na) + 3) & ~3);
-    if (dci_smem(64, nqp, kp, dci_ld_e(kp)) > kDciSmemMax) return false;
+    if (dci_smem(32, nqp, kp, dci_ld_e(kp)) > kDciSmemMax) return false;
     if (env && env[0] == '1') return true;
     // tensor-core FMAs (nqp per beta column) against SELL terms (in-set beta singles per string):
     // the contraction runs ~14x faster per FMA than the gathered terms (cfg1 measurement)
@@ -369,12 +375,12 @@ int sbd_cross_dci(sbd_ctx *ctx, const double *x_full, double *y, bool additive, 
     a.add = additive;
     const size_t smem = dci_smem(d.nt, d.nqp, d.kp_max, d.ld_e);
     const int mf = d.nqp / 8;
-    if (d.nt == 128) {
-        if (mf <= 4) return launch_dci_ppt<128, 4>(ctx, a, smem);
-        if (mf <= 8) return launch_dci_ppt<128, 8>(ctx, a, smem);
-        if (mf <= 12) return launch_dci_ppt<128, 12>(ctx, a, smem);
-        return launch_dci_ppt<128, 16>(ctx, a, smem);
+    if (d.nt == 64) {
+        if (mf <= 4) return launch_dci_ppt<64, 4>(ctx, a, smem);
+        if (mf <= 8) return launch_dci_ppt<64, 8>(ctx, a, smem);
+        if (mf <= 12) return launch_dci_ppt<64, 12>(ctx, a, smem);
+        return launch_dci_ppt<64, 16>(ctx, a, smem);
     }
-    if (mf <= 8) return launch_dci_ppt<64, 4>(ctx, a, smem);
-    return launch_dci_ppt<64, 8>(ctx, a, smem);
+    if (mf <= 8) return launch_dci_ppt<32, 4>(ctx, a, smem);
+    return launch_dci_ppt<32, 8>(ctx, a, smem);
 }

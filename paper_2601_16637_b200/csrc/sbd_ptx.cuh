@@ -42,6 +42,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
+// order this thread's (and, after an mbarrier wait, the releasing threads') generic-proxy
+// shared-memory accesses before subsequent async-proxy (TMA) accesses
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // global -> shared bulk copy, completion counted on `bar` (bytes % 16 == 0, 16-B aligned ends)
 __device__ __forceinline__ void tma_load_1d(void *dst_smem, const void *src_gmem, uint32_t bytes, uint64_t *bar) {
     asm volatile(
@@ -116,6 +122,10 @@ __device__ __forceinline__ void tma_load_1d_multicast(void *dst_smem, const void
 // ---- per-thread asynchronous copies (LDGSTS) --------------------------------
 __device__ __forceinline__ void cp_async16(void *dst_smem, const void *src_gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem) : "memory");
+}
+// same, allocating in L1 (repeated segments of neighbouring rows hit L1 instead of L2)
+__device__ __forceinline__ void cp_async16_ca(void *dst_smem, const void *src_gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>

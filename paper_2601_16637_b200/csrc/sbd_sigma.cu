@@ -49,6 +49,11 @@ struct SideArgs {
     i64 ldyt;
     const int64_t *a_s_off;        // rows with alpha singles carry task 0 in Y (cross_kernel); null: no task 0
     i64 tile0;                     // first column tile (pipelined host path launches tile ranges)
+    i64 n_tiles;                   // column tiles of the launch (persistent kernel)
+    // beta side: output row of processing slot p is perm[p] (sorted string order: neighbouring slots
+    // share connection targets); null = identity.  ca: stream segments allocate in L1.
+    const int32_t *perm;
+    bool ca;
     // Y^T layout.  false: [n_beta][ld_t] (alpha row contiguous).  true (blocked): blocks of 8
     // alpha rows, [ld_t / 8][n_beta][8] -- the alpha CTA's 8 rows x 256 columns are one
     // contiguous 16 KB block instead of 256 scattered 64-byte pieces (L1-friendly reads)
@@ -225,6 +230,8 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
 // is the only synchronisation (no barriers in the stream).
 constexpr int kTW = 256;
 
+constexpr double kPersistMaxCbar = 0.0;  // default threshold (connections per string) for the persistent side kernels
+constexpr int kPersistCtas = 3;  // persistent side kernels: resident CTAs per SM (<= 80 registers, no spills)
 constexpr int kSideCtas = 4;  // resident CTAs per SM: registers <= 64, 4 x 48 KB rings (5 CTAs spill and need a 2-slot ring: slower)
 
 template <bool ALPHA>
@@ -240,10 +247,11 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
     extern __shared__ __align__(128) unsigned char ssm[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *ring = reinterpret_cast<double *>(ssm) + (size_t)w * R * kTW;
-    const i64 r = (i64)blockIdx.x * kRowsPerCta + w;
+    const i64 rp = (i64)blockIdx.x * kRowsPerCta + w;
     const i64 c0 = ((i64)blockIdx.y + a.tile0) * kTW;
     const i64 ncol = min((i64)kTW, a.n_cols - c0);
-    const bool row_ok = r < a.n_rows;
+    const bool row_ok = rp < a.n_rows;
+    const i64 r = (!ALPHA && a.perm != nullptr && row_ok) ? (i64)a.perm[rp] : rp;
     bool ok[8], pair[4];
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
@@ -270,9 +278,15 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
             if (i < n) {
                 const double *src = a.X + (i64)a.conn[e0 + i].tgt * a.ldx + c0;
                 double *dst = ring + (size_t)slot * kTW;
+                if (a.ca) {
 #pragma unroll
-                for (int h = 0; h < 4; ++h)
-                    if (pair[h]) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
+                    for (int h = 0; h < 4; ++h)
+                        if (pair[h]) cp_async16_ca(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 4; ++h)
+                        if (pair[h]) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
+                }
             }
             cp_async_commit();
         };
@@ -282,9 +296,15 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
                                       : (i == n ? a.diag + r * a.ldy + c0 : a.X + own * a.ldx + c0);
             if (i <= n + 1) {
                 double *dst = ring + (size_t)slot * kTW;
+                if (a.ca && i < n) {
 #pragma unroll
-                for (int h = 0; h < 4; ++h)
-                    if (pair[h]) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
+                    for (int h = 0; h < 4; ++h)
+                        if (pair[h]) cp_async16_ca(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 4; ++h)
+                        if (pair[h]) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
+                }
             }
             cp_async_commit();
         };
@@ -395,6 +415,191 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
             }
         }
     }
+}
+
+// Persistent variant of side_kernel_async for the sparse regime (few connections
+// per row).  There, a (row, tile) item is a handful of dependent phases -- the
+// connection records, a few 2 KB segments, the epilogue operands -- and a warp
+// that owns one item spends most of its life waiting.  Here the grid is
+// num_SMs x kSideCtas CTAs; CTA c walks the item blocks j = c, c + G, ... in
+// tile-major order (all SMs stay on one column tile at a time, as in the
+// one-item grid), warp w taking row 8 (j mod nrb) + w.  The warp's ring is
+// one continuous stream over its items: item k's connection segments, then
+// (alpha side) its diag, own-x and, for rows carrying task 0, y segments, then
+// item k + 1's segments -- so the next item's loads are in flight while this
+// item's epilogue runs.  All R ring slots hold loads in flight (consume a
+// slot, then refill it); the diag slot is read together with the own-x slot,
+// so its refill is deferred by one position (an empty group keeps the
+// wait_group accounting).  Targets of the issue side come from one
+// warp-cooperative load per 32 connections.
+struct PItem {
+    i64 e0;
+    int r, c0;  // local row (-1: past the end), first column
+    int n, np;  // connections, positions (n + epilogue operands)
+};
+
+template <bool ALPHA>
+__device__ __forceinline__ PItem persist_item(const SideArgs &a, int k, int nrb, int w) {
+    PItem it{};
+    const int j = (int)blockIdx.x + k * (int)gridDim.x;
+    it.r = (j % nrb) * kRowsPerCta + w;
+    it.c0 = (int)((a.tile0 + j / nrb) * kTW);
+    if (it.r >= a.n_rows) {
+        it.n = it.np = 0;
+        it.r = -1;
+        return it;
+    }
+    const i64 g = a.row_base + it.r;
+    it.e0 = a.conn_off[g];
+    it.n = (int)(a.conn_off[g + 1] - it.e0);
+    const bool t0 = ALPHA && a.a_s_off != nullptr && a.a_s_off[g + 1] != a.a_s_off[g];
+    it.np = it.n + (ALPHA ? 2 + (t0 ? 1 : 0) : 0);
+    return it;
+}
+
+template <bool ALPHA>
+__global__ void __launch_bounds__(kRowsPerCta * 32, kPersistCtas) side_kernel_persist(SideArgs a) {
+    constexpr int R = SideAsync<ALPHA>::kRing;
+    extern __shared__ __align__(128) unsigned char ssm[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *ring = reinterpret_cast<double *>(ssm) + (size_t)w * R * kTW;
+    const int nrb = (int)((a.n_rows + kRowsPerCta - 1) / kRowsPerCta);
+    const int nk = (int)((nrb * a.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);  // items of this warp
+    if (nk <= 0) return;
+
+    // ---- issue side: item ki, position pi; targets of the item's connections in `win`
+    int ki = 0;
+    int pi = 0;
+    PItem is = persist_item<ALPHA>(a, 0, nrb, w);
+    int win = 0, wbase = -32;
+    auto issue = [&](int slot) {
+        while (ki < nk && pi >= is.np) {
+            if (++ki < nk) is = persist_item<ALPHA>(a, ki, nrb, w);
+            pi = 0;
+            wbase = -32;
+        }
+        if (ki < nk) {
+            const double *src;
+            if (pi < is.n) {
+                if (pi >= wbase + 32) {  // next 32 targets, one load per lane
+                    wbase = pi & ~31;
+                    win = wbase + lane < is.n ? __ldg(&a.conn[is.e0 + wbase + lane].tgt) : 0;
+                }
+                src = a.X + (i64)__shfl_sync(0xffffffffu, win, pi - wbase) * a.ldx + is.c0;
+            } else if (pi == is.n) {
+                src = a.diag + (i64)is.r * a.ldy + is.c0;
+            } else if (pi == is.n + 1) {
+                src = a.X + (a.row_base + is.r) * a.ldx + is.c0;
+            } else {
+                src = a.Y + (i64)is.r * a.ldy + is.c0;
+            }
+            const int ncol = (int)min((i64)kTW, a.n_cols - is.c0);
+            double *dst = ring + (size_t)slot * kTW;
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+                if (2 * lane + 64 * h < ncol) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
+            ++pi;
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < R; ++s) issue(s);
+
+    // ---- consume side
+    int slot = 0, dslot = 0;
+    for (int kc = 0; kc < nk; ++kc) {
+        const PItem ic = persist_item<ALPHA>(a, kc, nrb, w);
+        if (ic.r < 0) continue;  // rows past the end: no positions, nothing stored
+        const int ncol = (int)min((i64)kTW, a.n_cols - ic.c0);
+        double acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+        for (int pc = 0; pc < ic.np; ++pc) {
+            // groups map 1:1 to positions; the diag position commits none and the own-x position
+            // two, so the own-x segment (one group newer than usual) needs one more completed group
+            if (ALPHA && pc == ic.n + 1) cp_async_wait<R - 2>();
+            else cp_async_wait<R - 1>();
+            const double *src = ring + (size_t)slot * kTW;
+            if (pc < ic.n) {
+                const Conn cn = a.conn[ic.e0 + pc];
+                double2 v[4];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) v[h] = *reinterpret_cast<const double2 *>(src + 2 * lane + 64 * h);
+                if (cn.info == 0) {
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        acc[2 * h] = fma(cn.c, v[h].x, acc[2 * h]);
+                        acc[2 * h + 1] = fma(cn.c, v[h].y, acc[2 * h + 1]);
+                    }
+                } else {
+                    const int P = abs(cn.info) - 1;
+                    const double sg = cn.info > 0 ? 1.0 : -1.0;
+                    const double *jr = a.J + (i64)P * a.ldj + a.col_base + ic.c0;
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        const int cc = 2 * lane + 64 * h;
+                        const double j0 = cc < ncol ? __ldg(jr + cc) : 0.0, j1 = cc + 1 < ncol ? __ldg(jr + cc + 1) : 0.0;
+                        acc[2 * h] = fma(fma(sg, j0, cn.c), v[h].x, acc[2 * h]);
+                        acc[2 * h + 1] = fma(fma(sg, j1, cn.c), v[h].y, acc[2 * h + 1]);
+                    }
+                }
+                issue(slot);
+            } else if (pc == ic.n) {  // diag: kept in its slot until the own-x segment lands (refill deferred)
+                dslot = slot;
+            } else if (pc == ic.n + 1) {  // diag o x
+                const double *dsrc = ring + (size_t)dslot * kTW;
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int cc = 2 * lane + 64 * h;
+                    const double2 d = *reinterpret_cast<const double2 *>(dsrc + cc);
+                    const double2 x = *reinterpret_cast<const double2 *>(src + cc);
+                    acc[2 * h] = fma(d.x, x.x, acc[2 * h]);
+                    acc[2 * h + 1] = fma(d.y, x.y, acc[2 * h + 1]);
+                }
+                issue(dslot);
+                issue(slot);
+            } else {  // task 0 already in y (cross kernel ran first)
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const double2 p = *reinterpret_cast<const double2 *>(src + 2 * lane + 64 * h);
+                    acc[2 * h] += p.x;
+                    acc[2 * h + 1] += p.y;
+                }
+                issue(slot);
+            }
+            if (++slot == R) slot = 0;
+        }
+        const i64 r = ic.r;
+        if (ALPHA) {  // + (B X^T)^T
+            const double *ytc = a.ytb ? a.YT + ((r >> 3) * a.n_cols + ic.c0) * 8 + (r & 7) : a.YT + ic.c0 * a.ldyt + r;
+            const i64 yts = a.ytb ? 8 : a.ldyt;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int cc = 2 * lane + 64 * h;
+                if (cc < ncol) acc[2 * h] += __ldg(ytc + cc * yts);
+                if (cc + 1 < ncol) acc[2 * h + 1] += __ldg(ytc + (cc + 1) * yts);
+            }
+        }
+        if (!ALPHA && a.ytb) {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int cc = 2 * lane + 64 * h;
+                const i64 c = ic.c0 + cc;
+                double *p = a.Y + ((c >> 3) * a.n_rows + r) * 8 + (c & 7);
+                if (cc + 1 < ncol) __stcs(reinterpret_cast<double2 *>(p), make_double2(acc[2 * h], acc[2 * h + 1]));
+                else if (cc < ncol) *p = acc[2 * h];
+            }
+        } else {
+            double *yr = a.Y + r * a.ldy + ic.c0;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int cc = 2 * lane + 64 * h;
+                if (cc + 1 < ncol) __stcs(reinterpret_cast<double2 *>(yr + cc), make_double2(acc[2 * h], acc[2 * h + 1]));
+                else if (cc < ncol) yr[cc] = acc[2 * h];
+            }
+        }
+    }
+    cp_async_wait<0>();
 }
 
 // Task 0, the alpha-single x beta-single opposite-spin doubles (apply.py:235-238):
@@ -558,7 +763,10 @@ __global__ void __launch_bounds__(kCrossThreads, 1) cross_kernel_tma(CrossArgs a
         }
         for (i64 item = 0; item < nitems; ++item) {
             const int s = (int)(item % kCrossStages);
-            if (item >= kCrossStages) mbar_wait(&empty[s], (uint32_t)(((item / kCrossStages) - 1) & 1));
+            if (item >= kCrossStages) {
+                mbar_wait(&empty[s], (uint32_t)(((item / kCrossStages) - 1) & 1));
+                fence_proxy_async_smem();  // consumers' generic-proxy reads before the async-proxy refill
+            }
             const SConn sa = a.a_sconn[e];
             const i64 c0 = h * a.chunk, cols = min(a.chunk, a.nb - c0);
             double *dst = st0 + s * sdbl;
@@ -673,6 +881,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCrossThreads, 1) cr
                 mbar_arrive_expect_tx(&full[s], bx + bv);                       // armed for the whole item
                 mbar_arrive_remote(peer_other + (uint32_t)(s * sizeof(uint64_t)));  // my side free + armed
                 mbar_wait_cluster(&peer[s], use & 1);                           // the peer's side too
+                fence_proxy_async_smem();  // generic-proxy reads of the stage before the async-proxy refill
                 const SConn sa = a.a_sconn[e0 + item];
                 const double *row = a.X + (i64)sa.tgt * a.nb;
                 if (item + kMcPrefetch < nitems && xn > 0)  // next-but-one rows: L2 hits for the TMA
@@ -811,6 +1020,19 @@ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 bool yt_blocked_enabled() {  // SBD_YT_BLOCKED=0 keeps the row-contiguous Y^T layout (A/B)
     const char *e = getenv("SBD_YT_BLOCKED");
     return !(e && e[0] == '0');
+}
+
+// Persistent cross-item side kernels (side_kernel_persist): SBD_SIDE_PERSIST=0/1 forces them off/on;
+// by default they serve sectors with few connections per string (sparse regime).
+bool use_side_persist(const Sector &S) {
+    const char *e = getenv("SBD_SIDE_PERSIST");
+    if (e && *e) return e[0] == '1';
+    return S.n > 0 && (double)(S.ns + S.nd) < kPersistMaxCbar * (double)S.n;
+}
+
+bool env_on(const char *name, bool dflt) {
+    const char *e = getenv(name);
+    return (e && *e) ? e[0] == '1' : dflt;
 }
 
 bool use_side_tma() {  // SBD_SIDE_LDG=1 selects the register-staged stream (A/B measurements)
@@ -1003,10 +1225,21 @@ int launch_beta_side(sbd_ctx *ctx, const double *x_own, i64 r0, i64 r1) {
         SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_async<false>, ctx->device, SideAsync<false>::smem()));
         a.tile0 = r0 / kTW;
         a.ytb = yt_blocked_enabled();
+        // sorted processing order (SBD_PERM_BETA) and L1-allocating segments (SBD_SIDE_CA)
+        a.perm = env_on("SBD_PERM_BETA", false) ? B.perm.as<int32_t>() : nullptr;
+        a.ca = env_on("SBD_SIDE_CA", false);
         ctx->yt_blocked = a.ytb;
         const i64 t1 = (r1 + kTW - 1) / kTW;
-        dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)(t1 - a.tile0));
-        side_kernel_async<false><<<g, kRowsPerCta * 32, SideAsync<false>::smem(), st>>>(a);
+        a.n_tiles = t1 - a.tile0;
+        if (use_side_persist(B)) {
+            SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_persist<false>, ctx->device, SideAsync<false>::smem()));
+            const i64 items = (nb + kRowsPerCta - 1) / kRowsPerCta * a.n_tiles;
+            const unsigned grid = (unsigned)std::max<i64>(1, std::min<i64>(items, (i64)ctx->num_sms * kPersistCtas));
+            side_kernel_persist<false><<<grid, kRowsPerCta * 32, SideAsync<false>::smem(), st>>>(a);
+        } else {
+            dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)a.n_tiles);
+            side_kernel_async<false><<<g, kRowsPerCta * 32, SideAsync<false>::smem(), st>>>(a);
+        }
     } else {
         if (r0 != 0 || r1 != rows) return sbd_fail(ctx, SBD_EINVAL, "row-range beta side needs the aligned path");
         dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((rows + kColsPerWarp - 1) / kColsPerWarp));
@@ -1036,6 +1269,7 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
     a.J = B.J.as<double>();
     a.ldj = nb;
     a.ytb = ctx->yt_blocked;  // the layout the beta side wrote
+    a.ca = env_on("SBD_SIDE_CA", false);
     // the blocked Y^T groups alpha rows by 8: a chunk must start on a block (kTW-aligned chunks do)
     if (a.ytb && r0 % kRowsPerCta != 0) return sbd_fail(ctx, SBD_EINVAL, "alpha chunk start not a multiple of 8");
     a.YT = ctx->yt.as<double>() + (a.ytb ? r0 * nb : r0);
@@ -1043,7 +1277,14 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
     a.diag = ctx->diag.as<double>() + r0 * nb;
     a.a_s_off = (with_t0 && A.ns > 0 && B.ns > 0) ? A.s_off.as<int64_t>() : nullptr;
     const bool vec = (nb % 2 == 0) && aligned16(x_full) && aligned16(y) && (r0 % 2 == 0);
-    if (vec && use_side_tma()) {
+    if (vec && use_side_tma() && use_side_persist(A)) {
+        SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_persist<true>, ctx->device, SideAsync<true>::smem()));
+        a.tile0 = 0;
+        a.n_tiles = (nb + kTW - 1) / kTW;
+        const i64 items = (rows + kRowsPerCta - 1) / kRowsPerCta * a.n_tiles;
+        const unsigned grid = (unsigned)std::max<i64>(1, std::min<i64>(items, (i64)ctx->num_sms * kPersistCtas));
+        side_kernel_persist<true><<<grid, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
+    } else if (vec && use_side_tma()) {
         SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_async<true>, ctx->device, SideAsync<true>::smem()));
         dim3 gt((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kTW - 1) / kTW));
         side_kernel_async<true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);

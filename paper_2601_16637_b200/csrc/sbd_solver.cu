@@ -336,6 +336,15 @@ struct Solver {
                 std::memcpy(c2h.data(), pre_c2, sizeof(double) * k);
                 n2p = pre_n2p;
             }
+            if (o.selective_reorth && n2p >= 0.5 * t_norm2) {  // |t1| >= |t0| / sqrt(2): one pass is enough
+                const double norm = std::sqrt(std::max(n2p, 0.0));
+                if (norm < 1e-12 * norm0 || norm == 0.0) return SBD_OK;
+                set_scalar_kernel<<<1, 1, 0, ctx->stream>>>(scale, 1.0 / norm);
+                SBD_LAUNCHED(ctx, "davidson scale");
+                if (int rc = sbd_scale_copy(ctx, t, vec(V, k), n, scale)) return rc;
+                *ok = true;
+                return SBD_OK;
+            }
             double cc = 0.0;
             for (int i = 0; i < k; ++i) cc += c2h[i] * c2h[i];
             const double n2 = n2p - cc;  // |t' - V c2|^2 for orthonormal V
@@ -563,6 +572,7 @@ int sbd_davidson_default_opts(sbd_davidson_opts *o) {
     o->precond_delta = 1e-6;
     o->reorthogonalize = 1;
     o->track_orthogonality = 1;
+    o->selective_reorth = 0;
     return SBD_OK;
 }
 

@@ -58,6 +58,9 @@ class DavidsonOptions:
     track_orthogonality: bool = True
     # B200 extension: per-phase CUDA-event timing in stats.phase_ms (tracing)
     profile: bool = False
+    # B200 extension (off = reference): skip the second Gram-Schmidt pass when the first kept
+    # |t1| >= |t0| / sqrt(2) ("twice is enough"), saving one pass over V in most iterations
+    selective_reorth: bool = False
 
     def __post_init__(self):
         if not 1 <= self.n_roots <= self.restart_keep <= self.max_subspace:
@@ -335,7 +338,8 @@ def _solve_native(ctx, n, diag_dev, x0, opts, dev, return_device):
     o = _lib.DavidsonOptsC(n_roots=m, tol_residual=float(opts.tol_residual), max_iters=mi,
                            max_subspace=opts.max_subspace, restart_keep=opts.restart_keep,
                            precond_delta=float(opts.precond_delta), reorthogonalize=int(opts.reorthogonalize),
-                           track_orthogonality=int(opts.track_orthogonality))
+                           track_orthogonality=int(opts.track_orthogonality),
+                           selective_reorth=int(opts.selective_reorth))
     st = _lib.DavidsonStatsC(theta_hist=hist["theta"].ctypes.data, res_hist=hist["res"].ctypes.data,
                              ortho_hist=hist["ortho"].ctypes.data, apply_ms_hist=hist["apply"].ctypes.data,
                              iter_ms_hist=hist["iter"].ctypes.data, restart_iters=restart_iters.ctypes.data)
@@ -638,6 +642,13 @@ def _orthogonalize_device(eng, V, k, ld, n_loc, t, c, t_norm2, opts, small, scal
             c2, n2p = hv[:k], float(hv[k])
         else:
             c2, n2p = pre
+        if opts.selective_reorth and n2p >= 0.5 * t_norm2:  # |t'| >= |t| / sqrt(2): one pass is enough
+            norm = float(np.sqrt(max(n2p, 0.0)))
+            if norm < 1e-12 * norm0 or norm == 0.0:
+                return False
+            scale.fill_(1.0 / norm)
+            eng("sbd_scale_copy", _p(t), _p(V[k]), n_loc, _p(scale))
+            return True
         n2 = n2p - float(c2 @ c2)  # |t' - V c2|^2 for orthonormal V
         c2d = small[:k].clone()
         if n2p > 0.0 and n2 > 0.5 * n2p:

@@ -112,12 +112,18 @@ def test_partitioned_sigma_and_davidson_match_single_gpu(world, case, kw, env, m
     app = HamiltonianApplier(basis, table)
     x = np.random.default_rng(seed).standard_normal(basis.dimension)
     ref = app(x)
+    import oracle as O  # the gathered partitioned sigma against the CPU restatement too, not only the 1-GPU path
+
+    inst = O.Instance.make(norb, table.h, table.eri, table.e_core, basis.alpha_array(), basis.beta_array())
+    ref_o = O.sigma(inst, x)
+    assert np.abs(ref - ref_o).max() <= 1e-10 * np.abs(ref_o).max()
     single = davidson_solve(app, app.diag, opts=DavidsonOptions(n_roots=nroots, max_subspace=16, restart_keep=4))
     vec = np.zeros((len(single.energies), basis.dimension))
     for rank, y, e, it, conv, lo, hi, v, determ, exch, info, rep in out:
         want_sparse = kw.get("exchange") == "sparse" or (kw.get("exchange") == "auto"
                                                           and info["needed_fraction"] <= 0.6)
         assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max()   # P-invariance
+        assert np.abs(y - ref_o).max() <= 1e-10 * np.abs(ref_o).max()  # parity with the oracle
         assert determ                                               # repeated sigma: bitwise equal
         assert exch == ("sparse" if want_sparse else "dense")
         assert info["nranks"] == world and (info["alpha_lo"], info["alpha_hi"]) == (lo, hi)

@@ -178,6 +178,13 @@ SIGMA_VARIANTS = [
     {"SBD_CROSS_UNSTAGED": "1"},
     {"SBD_CROSS_ADD": "1"},
     {"SBD_CROSS_ADD": "0", "SBD_YT_BLOCKED": "0"},
+    {"SBD_SIDE_PERSIST": "1"},
+    {"SBD_SIDE_PERSIST": "1", "SBD_YT_BLOCKED": "0"},
+    {"SBD_SIDE_PERSIST": "1", "SBD_CROSS_ADD": "1"},
+    {"SBD_SIDE_PERSIST": "0"},
+    {"SBD_PERM_BETA": "1", "SBD_SIDE_CA": "1"},
+    {"SBD_PERM_BETA": "1", "SBD_YT_BLOCKED": "0"},
+    {"SBD_CONN_SORT": "0"},
 ]
 
 

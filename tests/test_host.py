@@ -157,7 +157,7 @@ def test_native_davidson_default_options_match_reference_defaults():
     assert _lib.load().sbd_davidson_default_opts(ctypes.byref(o)) == 0
     d = DavidsonOptions()
     for f in ("n_roots", "tol_residual", "max_iters", "max_subspace", "restart_keep", "precond_delta",
-              "reorthogonalize", "track_orthogonality"):
+              "reorthogonalize", "track_orthogonality", "selective_reorth"):
         assert getattr(o, f) == getattr(d, f), f
     assert _lib.load().sbd_davidson_default_opts(None) == 1
 
