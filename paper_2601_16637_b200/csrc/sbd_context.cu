@@ -200,6 +200,7 @@ int sbd_build_tables(sbd_ctx *ctx) {
     }
     ctx->diag_valid = false;
     ctx->dci.valid = false;
+    ctx->ka_valid = false;
     ctx->dist.planned = false;  // the exchange plan is built from the alpha table
     SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SBD_OK;

@@ -34,19 +34,18 @@
 
 namespace {
 
-constexpr int kDciThreads = 256;          // 8 warps; two CTAs per SM when shared memory allows
-constexpr int kDciWarps = kDciThreads / 32;
+constexpr int kDciThreads = 512;          // 16 warps, one CTA per SM
 constexpr int kMaxSingles = 64;           // beta singles per string handled by the list builder
 constexpr size_t kDciSmemMax = 227 * 1024;
-// beta columns per tile: 64 (warp w owns the 8-column fragment w and every row fragment) or, when
-// that does not fit shared memory, 32 (warps w and w + 4 share fragment w % 4, halving the rows)
-template <int NT>
-struct Tile {
-    static constexpr int kLdX = NT + 4;    // slab row stride (doubles): B-fragment loads conflict-free
-    static constexpr int kLdG = NT + 8;    // G row stride: C-fragment double2 stores conflict-free
-    static constexpr int kNfr = NT / 8;    // column fragments
-    static constexpr int kMsplit = kDciWarps / kNfr;  // warps per column fragment
-};
+// Tile: NT = 128 beta columns.  The 16 warps form a 4 x 4 grid over (row fragments, column
+// fragments): warp (mg, ng) owns row fragments m = mg + 4 j and the four column fragments
+// 4 ng .. 4 ng + 3, and keeps its E fragments in registers for the whole alpha row (E changes per
+// row, the slab per tile), so a k-step costs 4 shared loads for 4 MFW DMMAs.
+constexpr int kNT = 128;
+constexpr int kLdX = kNT + 4;    // slab row stride (doubles): B-fragment loads conflict-free
+constexpr int kLdG = kNT + 8;    // G row stride: C-fragment double2 stores conflict-free
+constexpr int kNFW = 4;          // column fragments per warp
+constexpr int kMG = 4;           // warp groups along the row fragments
 
 struct DciArgs {
     i64 n_rows, row_base, nb;
@@ -62,22 +61,21 @@ struct DciArgs {
     bool add;
 };
 
-__host__ __device__ inline size_t dci_smem(int nt, int nqp, int kp_max, int ld_e) {
-    return sizeof(double) * ((size_t)nqp * ld_e + 2 * (size_t)kp_max * (nt + 4) + (size_t)nqp * (nt + 8));
+__host__ __device__ inline size_t dci_smem(int nqp, int kp_max, int ld_e) {
+    return sizeof(double) * ((size_t)nqp * ld_e + 2 * (size_t)kp_max * kLdX + (size_t)nqp * kLdG);
 }
 __host__ __device__ inline int dci_ld_e(int kp) { return kp + (((4 - kp) % 16) + 16) % 16; }
 
 // Stage rows ja_k (k < K) of x, columns [t NT, t NT + NT), into `xs`; rows K..Kp-1 and
 // columns past nb are zero (E is zero there too, but the slab must not hold NaNs).
-template <int NT>
 __device__ __forceinline__ void dci_stage(const DciArgs &a, double *xs, i64 row, int t, int K, int Kp) {
     const i64 e0 = a.a_s_off[row];
-    const i64 c0 = (i64)t * NT;
-    const int cols = (int)min((i64)NT, a.nb - c0);
-    constexpr int kChunks = NT / 2;  // 16-byte chunks per slab row
+    const i64 c0 = (i64)t * kNT;
+    const int cols = (int)min((i64)kNT, a.nb - c0);
+    constexpr int kChunks = kNT / 2;  // 16-byte chunks per slab row
     for (int c = threadIdx.x; c < Kp * kChunks; c += kDciThreads) {
         const int k = c / kChunks, j = c % kChunks;
-        double *dst = xs + k * Tile<NT>::kLdX + 2 * j;
+        double *dst = xs + k * kLdX + 2 * j;
         if (k < K && 2 * j < cols) {
             const i64 ja = a.a_sconn[e0 + k].tgt;
             cp_async16(dst, a.X + ja * a.nb + c0 + 2 * j);
@@ -94,16 +92,15 @@ __device__ __forceinline__ i64 dci_next_row(const DciArgs &a, i64 r) {
     return a.n_rows;
 }
 
-// MF: row fragments per warp (ceil(nqp / 8 / kMsplit))
-template <int NT, int MF, int PPT>
-__global__ void __launch_bounds__(kDciThreads, 2) cross_kernel_dci(DciArgs a) {
-    using T = Tile<NT>;
+// MFW: row fragments per warp (ceil(nqp / 8 / kMG)); KS: k-steps held in registers (Kp / 4 <= KS)
+template <int MFW, int KS, int PPT>
+__global__ void __launch_bounds__(kDciThreads, 1) cross_kernel_dci(DciArgs a) {
     extern __shared__ __align__(128) unsigned char dsm[];
-    double *es = reinterpret_cast<double *>(dsm);      // [nqp][ld_e]
-    double *xs0 = es + (size_t)a.nqp * a.ld_e;         // 2 x [kp_max][kLdX]
-    double *gs = xs0 + 2 * (size_t)a.kp_max * T::kLdX; // [nqp][kLdG]
+    double *es = reinterpret_cast<double *>(dsm);     // [nqp][ld_e]
+    double *xs0 = es + (size_t)a.nqp * a.ld_e;        // 2 x [kp_max][kLdX]
+    double *gs = xs0 + 2 * (size_t)a.kp_max * kLdX;   // [nqp][kLdG]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nfr = warp % T::kNfr, mpart = warp / T::kNfr;  // column fragment; rows m = mpart + kMsplit j
+    const int mg = warp / kMG, ng = warp % kMG;
     const int mf = a.nqp / 8;
 
     i64 r = dci_next_row(a, blockIdx.x);
@@ -111,12 +108,13 @@ __global__ void __launch_bounds__(kDciThreads, 2) cross_kernel_dci(DciArgs a) {
     auto kof = [&](i64 rr) { return (int)(a.a_s_off[a.row_base + rr + 1] - a.a_s_off[a.row_base + rr]); };
     int K = kof(r), Kp = (K + 3) & ~3;
     int t = 0, buf = 0;
-    dci_stage<NT>(a, xs0, a.row_base + r, 0, K, Kp);
+    dci_stage(a, xs0, a.row_base + r, 0, K, Kp);
     cp_async_commit();
 
     double acc[PPT];
 #pragma unroll
     for (int i = 0; i < PPT; ++i) acc[i] = 0.0;
+    double af[MFW][KS];  // this warp's E fragments for the current row
 
     while (true) {
         // the item after this one: next tile of the row, else tile 0 of the CTA's next row
@@ -127,7 +125,7 @@ __global__ void __launch_bounds__(kDciThreads, 2) cross_kernel_dci(DciArgs a) {
             tn = 0;
         }
         const int Kn = rn < a.n_rows ? kof(rn) : 0, Kpn = (Kn + 3) & ~3;
-        if (rn < a.n_rows) dci_stage<NT>(a, xs0 + (size_t)(buf ^ 1) * a.kp_max * T::kLdX, a.row_base + rn, tn, Kn, Kpn);
+        if (rn < a.n_rows) dci_stage(a, xs0 + (size_t)(buf ^ 1) * a.kp_max * kLdX, a.row_base + rn, tn, Kn, Kpn);
         cp_async_commit();
         if (t == 0) {  // E for this row: E[q][k] = s_k (Pa_k | Q_q); the previous row's GEMM is done
             const i64 e0 = a.a_s_off[a.row_base + r];
@@ -144,33 +142,45 @@ __global__ void __launch_bounds__(kDciThreads, 2) cross_kernel_dci(DciArgs a) {
         }
         cp_async_wait<1>();
         __syncthreads();  // slab `buf` and E visible; the previous gather is done with G
+        if (t == 0) {  // E fragments of this warp into registers, for all tiles of the row
+            const double *ap = es + (mg * 8 + (lane >> 2)) * a.ld_e + (lane & 3);
+#pragma unroll
+            for (int j = 0; j < MFW; ++j)
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks)
+                    af[j][ks] = (mg + kMG * j < mf && 4 * ks < Kp) ? ap[j * kMG * 8 * a.ld_e + 4 * ks] : 0.0;
+        }
 
-        // G tile = E (nqp x Kp) * slab (Kp x NT): warp -> columns 8 nfr .. 8 nfr + 7, row fragments
-        // mpart, mpart + kMsplit, ...
+        // G tile = E (nqp x Kp) * slab (Kp x NT)
         {
-            const double *xs = xs0 + (size_t)buf * a.kp_max * T::kLdX;
-            double d[MF][2];
+            const double *xs = xs0 + (size_t)buf * a.kp_max * kLdX;
+            double d[MFW][kNFW][2];
 #pragma unroll
-            for (int j = 0; j < MF; ++j) d[j][0] = d[j][1] = 0.0;
-            const double *bp = xs + (lane & 3) * T::kLdX + nfr * 8 + (lane >> 2);
-            const double *ap = es + (mpart * 8 + (lane >> 2)) * a.ld_e + (lane & 3);
-            const int stride_a = T::kMsplit * 8 * a.ld_e;
-            for (int k0 = 0; k0 < Kp; k0 += 4) {
-                // all operands of the k-step first (one shared-memory round trip), then the DMMAs
-                const double b = bp[k0 * T::kLdX];
-                double av[MF];
+            for (int j = 0; j < MFW; ++j)
 #pragma unroll
-                for (int j = 0; j < MF; ++j) av[j] = mpart + j * T::kMsplit < mf ? ap[j * stride_a + k0] : 0.0;
+                for (int n = 0; n < kNFW; ++n) d[j][n][0] = d[j][n][1] = 0.0;
+            const double *bp = xs + (lane & 3) * kLdX + ng * (8 * kNFW) + (lane >> 2);
 #pragma unroll
-                for (int j = 0; j < MF; ++j)
-                    if (mpart + j * T::kMsplit < mf) dmma_8x8x4(d[j][0], d[j][1], av[j], b);
+            for (int ks = 0; ks < KS; ++ks) {
+                if (4 * ks < Kp) {
+                    double b[kNFW];
+#pragma unroll
+                    for (int n = 0; n < kNFW; ++n) b[n] = bp[4 * ks * kLdX + 8 * n];
+#pragma unroll
+                    for (int j = 0; j < MFW; ++j)
+                        if (mg + kMG * j < mf)
+#pragma unroll
+                            for (int n = 0; n < kNFW; ++n) dmma_8x8x4(d[j][n][0], d[j][n][1], af[j][ks], b[n]);
+                }
             }
 #pragma unroll
-            for (int j = 0; j < MF; ++j) {
-                const int m = mpart + j * T::kMsplit;
+            for (int j = 0; j < MFW; ++j) {
+                const int m = mg + kMG * j;
                 if (m < mf)
-                    *reinterpret_cast<double2 *>(gs + (m * 8 + (lane >> 2)) * T::kLdG + nfr * 8 + 2 * (lane & 3)) =
-                        make_double2(d[j][0], d[j][1]);
+#pragma unroll
+                    for (int n = 0; n < kNFW; ++n)
+                        *reinterpret_cast<double2 *>(gs + (m * 8 + (lane >> 2)) * kLdG + ng * (8 * kNFW) + 8 * n +
+                                                     2 * (lane & 3)) = make_double2(d[j][n][0], d[j][n][1]);
             }
         }
         __syncthreads();  // G tile complete
@@ -185,7 +195,7 @@ __global__ void __launch_bounds__(kDciThreads, 2) cross_kernel_dci(DciArgs a) {
                 double s = acc[i];
                 for (int e = lo; e < hi; ++e) {
                     const uint32_t u = __ldg(a.ent + e);
-                    const double g = gs[((u >> 1) & 0x7fffu) * T::kLdG + (u >> 16)];
+                    const double g = gs[((u >> 1) & 0x7fffu) * kLdG + (u >> 16)];
                     s += (u & 1u) ? -g : g;
                 }
                 acc[i] = s;
@@ -285,8 +295,8 @@ int dci_build(sbd_ctx *ctx) {
     d.kp_max = std::max(4, (ka + 3) & ~3);
     d.kb_max = kb;
     d.ld_e = dci_ld_e(d.kp_max);  // = 4 mod 16
-    d.nt = dci_smem(64, d.nqp, d.kp_max, d.ld_e) <= kDciSmemMax ? 64 : 32;
-    d.ntiles = (int)((B.n + d.nt - 1) / d.nt);
+    d.nt = kNT;
+    d.ntiles = (int)((B.n + kNT - 1) / kNT);
     DevBuf qm, qp;
     SBD_CUDA(ctx, qm.ensure(sizeof(int32_t) * qmap.size()));
     SBD_CUDA(ctx, qp.ensure(sizeof(int32_t) * std::max<size_t>(1, qpair.size())));
@@ -310,22 +320,28 @@ int dci_build(sbd_ctx *ctx) {
     return SBD_OK;
 }
 
-template <int NT, int MF, int PPT>
+template <int MFW, int KS, int PPT>
 int launch_dci(sbd_ctx *ctx, const DciArgs &a, size_t smem) {
-    SBD_CUDA(ctx, sbd_smem_attr((const void *)cross_kernel_dci<NT, MF, PPT>, ctx->device, smem));
-    const unsigned per_sm = 2 * (smem + 1024) <= 228 * 1024 ? 2 : 1;  // two CTAs: one gathers while one multiplies
-    cross_kernel_dci<NT, MF, PPT><<<(unsigned)ctx->num_sms * per_sm, kDciThreads, smem, ctx->stream>>>(a);
+    SBD_CUDA(ctx, sbd_smem_attr((const void *)cross_kernel_dci<MFW, KS, PPT>, ctx->device, smem));
+    cross_kernel_dci<MFW, KS, PPT><<<(unsigned)ctx->num_sms, kDciThreads, smem, ctx->stream>>>(a);
     SBD_LAUNCHED(ctx, "cross_kernel_dci");
     return SBD_OK;
 }
 
-template <int NT, int MF>
+template <int MFW, int KS>
 int launch_dci_ppt(sbd_ctx *ctx, const DciArgs &a, size_t smem) {
     const i64 ppt = (a.nb + kDciThreads - 1) / kDciThreads;
-    if (ppt <= 2) return launch_dci<NT, MF, 2>(ctx, a, smem);
-    if (ppt <= 4) return launch_dci<NT, MF, 4>(ctx, a, smem);
-    if (ppt <= 8) return launch_dci<NT, MF, 8>(ctx, a, smem);
-    return launch_dci<NT, MF, 16>(ctx, a, smem);
+    if (ppt <= 2) return launch_dci<MFW, KS, 2>(ctx, a, smem);
+    if (ppt <= 4) return launch_dci<MFW, KS, 4>(ctx, a, smem);
+    return launch_dci<MFW, KS, 8>(ctx, a, smem);
+}
+
+// (row fragments per warp, k-steps in registers) instantiated: up to 36 alpha singles per string and
+// MFW * KS <= 32 doubles of E per thread (no spills at 512 threads: cfg1 is MFW 3, KS 9)
+bool dci_shape(int nqp, int kp, int *mfw, int *ks) {
+    *mfw = (nqp / 8 + kMG - 1) / kMG;
+    *ks = kp <= 16 ? 4 : 9;
+    return kp <= 36 && *mfw <= 4 && *mfw * *ks <= 32;
 }
 
 }  // namespace
@@ -337,13 +353,14 @@ bool sbd_dci_eligible(sbd_ctx *ctx, const double *x_full) {
     if (env && env[0] == '0') return false;
     const int norb = ctx->norb, nq = norb * (norb - 1) / 2;
     const int nqp = std::max(8, (nq + 7) / 8 * 8);
-    if (nqp > 128 || B.n % 2 != 0 || B.n > (i64)kDciThreads * 16 || B.n * (i64)((B.n + 31) / 32 + 1) >= (1ll << 31) ||
+    if (nqp > 128 || B.n % 2 != 0 || B.n > (i64)kDciThreads * 8 || B.n * (i64)((B.n + 31) / 32 + 1) >= (1ll << 31) ||
         B.ns >= (1ll << 31) || (reinterpret_cast<uintptr_t>(x_full) & 15) != 0 || A.ns == 0 || B.ns == 0)
         return false;
     const int na = A.n_elec, nbe = B.n_elec;
     if ((i64)na * (norb - na) > 64 || (i64)nbe * (norb - nbe) > kMaxSingles) return false;
     const int kp = std::max(4, (na * (norb - na) + 3) & ~3);
-    if (dci_smem(32, nqp, kp, dci_ld_e(kp)) > kDciSmemMax) return false;
+    int mfw, ks;
+    if (!dci_shape(nqp, kp, &mfw, &ks) || dci_smem(nqp, kp, dci_ld_e(kp)) > kDciSmemMax) return false;
     if (env && env[0] == '1') return true;
     // tensor-core FMAs (nqp per beta column) against SELL terms (in-set beta singles per string):
     // the contraction runs ~14x faster per FMA than the gathered terms (cfg1 measurement)
@@ -373,14 +390,14 @@ int sbd_cross_dci(sbd_ctx *ctx, const double *x_full, double *y, bool additive, 
     a.toff = d.toff.as<int32_t>();
     a.ntiles = d.ntiles;
     a.add = additive;
-    const size_t smem = dci_smem(d.nt, d.nqp, d.kp_max, d.ld_e);
-    const int mf = d.nqp / 8;
-    if (d.nt == 64) {
-        if (mf <= 4) return launch_dci_ppt<64, 4>(ctx, a, smem);
-        if (mf <= 8) return launch_dci_ppt<64, 8>(ctx, a, smem);
-        if (mf <= 12) return launch_dci_ppt<64, 12>(ctx, a, smem);
-        return launch_dci_ppt<64, 16>(ctx, a, smem);
+    const size_t smem = dci_smem(d.nqp, d.kp_max, d.ld_e);
+    int mfw, ks;
+    if (!dci_shape(d.nqp, d.kp_max, &mfw, &ks)) return sbd_fail(ctx, SBD_EINVAL, "direct-CI task 0: shape not served");
+    if (ks == 4) {
+        if (mfw <= 2) return launch_dci_ppt<2, 4>(ctx, a, smem);
+        if (mfw == 3) return launch_dci_ppt<3, 4>(ctx, a, smem);
+        return launch_dci_ppt<4, 4>(ctx, a, smem);
     }
-    if (mf <= 8) return launch_dci_ppt<32, 4>(ctx, a, smem);
-    return launch_dci_ppt<32, 8>(ctx, a, smem);
+    if (mfw <= 2) return launch_dci_ppt<2, 9>(ctx, a, smem);
+    return launch_dci_ppt<3, 9>(ctx, a, smem);
 }

@@ -15,7 +15,6 @@
 // the reference's entry order; targets are mapped back to caller indices
 // through the sort permutation.
 #include <algorithm>
-#include <cstdlib>
 #include <vector>
 
 #include "sbd_internal.cuh"
@@ -493,30 +492,6 @@ int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s) {
     return SBD_OK;
 }
 
-// Each string's connections in ascending target order (insertion sort, one thread per string):
-// rows processed next to each other then walk shared targets at about the same time, so the
-// same-spin streams re-read them from L1 instead of L2 (see side_kernel_async).
-static __global__ void sort_conn_kernel(i64 n, const int64_t *__restrict__ off, Conn *__restrict__ conn) {
-    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    Conn *c = conn + off[i];
-    const i64 m = off[i + 1] - off[i];
-    for (i64 k = 1; k < m; ++k) {
-        const Conn v = c[k];
-        i64 j = k;
-        while (j > 0 && c[j - 1].tgt > v.tgt) {
-            c[j] = c[j - 1];
-            --j;
-        }
-        c[j] = v;
-    }
-}
-
-static bool conn_sorted_enabled() {  // SBD_CONN_SORT=0/1 (A/B); default: on
-    const char *e = getenv("SBD_CONN_SORT");
-    return !(e && e[0] == '0');
-}
-
 int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other) {
     (void)other;
     const i64 n = s.n;
@@ -538,10 +513,6 @@ int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other) {
         s.d_p1.as<int16_t>(), s.d_p2.as<int16_t>(), s.d_phase.as<int8_t>(), s.conn_off.as<int64_t>(),
         s.conn.as<Conn>(), s.sconn.as<SConn>(), s.s_row.as<int32_t>(), s.energy.as<double>());
     SBD_LAUNCHED(ctx, "coefficients");
-    if (conn_sorted_enabled()) {
-        sort_conn_kernel<<<grid_for(n, 128), 128, 0, st>>>(n, s.conn_off.as<int64_t>(), s.conn.as<Conn>());
-        SBD_LAUNCHED(ctx, "sort_conn_kernel");
-    }
     dim3 g(grid_for(n, 128), (unsigned)ctx->npair);
     jtable_kernel<<<g, 128, 0, st>>>(s.str.as<u64>(), n, ctx->npair, ctx->eri.as<double>(), s.J.as<double>());
     SBD_LAUNCHED(ctx, "jtable");

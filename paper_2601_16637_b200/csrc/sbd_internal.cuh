@@ -141,6 +141,8 @@ struct sbd_ctx {
     bool yt_blocked = false;
     DevBuf diag;                 // owned rows, cached
     bool diag_valid = false;
+    DevBuf ka, erow;             // inline-diagonal tables of the alpha side (sbd_sigma.cu ensure_ka)
+    bool ka_valid = false;
     DevBuf red;                  // reduction scratch
     DevBuf hx, hy;               // device staging for sbd_sigma_host
     cudaStream_t copy_stream = nullptr;  // sbd_sigma_host: H2D/D2H overlapped with the kernels

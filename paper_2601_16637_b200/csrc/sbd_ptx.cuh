@@ -123,10 +123,6 @@ __device__ __forceinline__ void tma_load_1d_multicast(void *dst_smem, const void
 __device__ __forceinline__ void cp_async16(void *dst_smem, const void *src_gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem) : "memory");
 }
-// same, allocating in L1 (repeated segments of neighbouring rows hit L1 instead of L2)
-__device__ __forceinline__ void cp_async16_ca(void *dst_smem, const void *src_gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem) : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {

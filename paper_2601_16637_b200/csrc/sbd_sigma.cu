@@ -49,15 +49,17 @@ struct SideArgs {
     i64 ldyt;
     const int64_t *a_s_off;        // rows with alpha singles carry task 0 in Y (cross_kernel); null: no task 0
     i64 tile0;                     // first column tile (pipelined host path launches tile ranges)
-    i64 n_tiles;                   // column tiles of the launch (persistent kernel)
-    // beta side: output row of processing slot p is perm[p] (sorted string order: neighbouring slots
-    // share connection targets); null = identity.  ca: stream segments allocate in L1.
-    const int32_t *perm;
-    bool ca;
     // Y^T layout.  false: [n_beta][ld_t] (alpha row contiguous).  true (blocked): blocks of 8
     // alpha rows, [ld_t / 8][n_beta][8] -- the alpha CTA's 8 rows x 256 columns are one
     // contiguous 16 KB block instead of 256 scattered 64-byte pieces (L1-friendly reads)
     bool ytb;
+    // inline diagonal (alpha side): diag[r, c] = erow[g] + eb[c] + sum_{q in beta string c} ka[g][q] is
+    // recomputed in the epilogue instead of read (8 B/det less HBM); null = read `diag`
+    const double *ka;              // [n_alpha][norb]: ka[g][q] = sum_{p in alpha string g} (pp|qq)
+    const double *erow;            // [n_alpha]: e_core + alpha same-spin energy
+    const double *eb;              // [n_beta]: beta same-spin energy
+    const u64 *bstr;               // [n_beta]: beta strings
+    int norb, nbe;                 // orbitals, beta electrons
     // partitioned passes (DIST kernels, sbd_alpha_pass): local row r streams the connections
     // seg_off[r * seg_stride + seg_lo] .. seg_off[r * seg_stride + seg_hi] of `conn`; its own x
     // row is X[xo_row0 + r]; epi adds diag o x + (B X^T)^T and writes y, acc_in adds onto y
@@ -230,9 +232,14 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
 // is the only synchronisation (no barriers in the stream).
 constexpr int kTW = 256;
 
-constexpr double kPersistMaxCbar = 0.0;  // default threshold (connections per string) for the persistent side kernels
-constexpr int kPersistCtas = 3;  // persistent side kernels: resident CTAs per SM (<= 80 registers, no spills)
+constexpr double kInlineDiagMaxCbar = 0.0;  // alpha connections per string below which the diagonal is recomputed
 constexpr int kSideCtas = 4;  // resident CTAs per SM: registers <= 64, 4 x 48 KB rings (5 CTAs spill and need a 2-slot ring: slower)
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 
 template <bool ALPHA>
 struct SideAsync {
@@ -247,11 +254,10 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
     extern __shared__ __align__(128) unsigned char ssm[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *ring = reinterpret_cast<double *>(ssm) + (size_t)w * R * kTW;
-    const i64 rp = (i64)blockIdx.x * kRowsPerCta + w;
+    const i64 r = (i64)blockIdx.x * kRowsPerCta + w;
     const i64 c0 = ((i64)blockIdx.y + a.tile0) * kTW;
     const i64 ncol = min((i64)kTW, a.n_cols - c0);
-    const bool row_ok = rp < a.n_rows;
-    const i64 r = (!ALPHA && a.perm != nullptr && row_ok) ? (i64)a.perm[rp] : rp;
+    const bool row_ok = r < a.n_rows;
     bool ok[8], pair[4];
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
@@ -278,33 +284,23 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
             if (i < n) {
                 const double *src = a.X + (i64)a.conn[e0 + i].tgt * a.ldx + c0;
                 double *dst = ring + (size_t)slot * kTW;
-                if (a.ca) {
 #pragma unroll
-                    for (int h = 0; h < 4; ++h)
-                        if (pair[h]) cp_async16_ca(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
-                } else {
-#pragma unroll
-                    for (int h = 0; h < 4; ++h)
-                        if (pair[h]) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
-                }
+                for (int h = 0; h < 4; ++h)
+                    if (pair[h]) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
             }
             cp_async_commit();
         };
-        // the stream's last two issues (positions n, n + 1) carry the epilogue operands
+        // the stream's last two issues (positions n, n + 1) carry the epilogue operands (diag, own x);
+        // with the inline diagonal only the own x (position n)
+        const bool inl = a.ka != nullptr;
         auto issue_epi = [&](i64 i, int slot) {
             const double *src = i < n ? a.X + (i64)a.conn[e0 + i].tgt * a.ldx + c0
-                                      : (i == n ? a.diag + r * a.ldy + c0 : a.X + own * a.ldx + c0);
-            if (i <= n + 1) {
+                                      : ((i == n && !inl) ? a.diag + r * a.ldy + c0 : a.X + own * a.ldx + c0);
+            if (i <= n + (inl ? 0 : 1)) {
                 double *dst = ring + (size_t)slot * kTW;
-                if (a.ca && i < n) {
 #pragma unroll
-                    for (int h = 0; h < 4; ++h)
-                        if (pair[h]) cp_async16_ca(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
-                } else {
-#pragma unroll
-                    for (int h = 0; h < 4; ++h)
-                        if (pair[h]) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
-                }
+                for (int h = 0; h < 4; ++h)
+                    if (pair[h]) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
             }
             cp_async_commit();
         };
@@ -354,18 +350,50 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
         // contiguous bytes of each Y^T column, so the 8 warps share one L1 line per
         // column and no block barrier (warps finish unevenly) is needed.
         const i64 g = a.row_base + r;
-        // diag and own-x segments, staged by the stream's last two issues
-        const double *dring = ring + (size_t)(nstream % R) * kTW, *xring = ring + (size_t)((nstream + 1) % R) * kTW;
+        // diag and own-x segments, staged by the stream's last two issues (inline diagonal: own x only)
+        const bool inl = a.ka != nullptr;
+        const double *dring = ring + (size_t)(nstream % R) * kTW;
+        const double *xring = ring + (size_t)((nstream + (inl ? 0 : 1)) % R) * kTW;
         const bool t0 = a.a_s_off != nullptr && a.a_s_off[g + 1] != a.a_s_off[g];
         const double *yrow = a.Y + r * a.ldy + c0;
         // Y^T[c0 + cc][r] = ytc[cc * yts]
         const double *ytc = a.ytb ? a.YT + ((r >> 3) * a.n_cols + c0) * 8 + (r & 7) : a.YT + c0 * a.ldyt + r;
         const i64 yts = a.ytb ? 8 : a.ldyt;
+        // inline diagonal: this row's ka (and its total at [norb]) in the ring slot no position used last
+        double *kr = ring + (size_t)((nstream + 1) % R) * kTW;
+        double erow = 0.0;
+        if (inl) {
+            erow = a.erow[g];
+            double t = 0.0;
+            for (int q = lane; q < a.norb; q += 32) {
+                const double v = __ldg(a.ka + g * a.norb + q);
+                kr[q] = v;
+                t += v;
+            }
+            t = warp_sum_d(t);
+            if (lane == 0) kr[a.norb] = t;
+            __syncwarp();
+        }
+        // inline diagonal of column c: beta electrons summed directly, or all orbitals minus the holes
+        auto dcol = [&](i64 c) -> double {
+            u64 bw = __ldg(a.bstr + c);
+            double e = erow + __ldg(a.eb + c);
+            if (2 * a.nbe <= a.norb) {
+                for (; bw; bw &= bw - 1) e += kr[__ffsll((long long)bw) - 1];
+            } else {
+                double hole = 0.0;
+                for (u64 hw = ~bw & (a.norb == 64 ? ~0ull : ((1ull << a.norb) - 1)); hw; hw &= hw - 1)
+                    hole += kr[__ffsll((long long)hw) - 1];
+                e += kr[a.norb] - hole;  // kr[norb] = sum over all orbitals
+            }
+            return e;
+        };
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
             const int cc = 2 * lane + 64 * h;
             if (ok[2 * h + 1]) {
-                const double2 d = *reinterpret_cast<const double2 *>(dring + cc);
+                const double2 d = inl ? make_double2(dcol(c0 + cc), dcol(c0 + cc + 1))
+                                      : *reinterpret_cast<const double2 *>(dring + cc);
                 const double2 x = *reinterpret_cast<const double2 *>(xring + cc);
                 const double t0v = __ldg(ytc + cc * yts), t1v = __ldg(ytc + (cc + 1) * yts);
                 acc[2 * h] = fma(d.x, x.x, acc[2 * h] + t0v);
@@ -376,7 +404,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
                     acc[2 * h + 1] += p.y;
                 }
             } else if (ok[2 * h]) {
-                acc[2 * h] = fma(dring[cc], xring[cc], acc[2 * h] + __ldg(ytc + cc * yts));
+                acc[2 * h] = fma(inl ? dcol(c0 + cc) : dring[cc], xring[cc], acc[2 * h] + __ldg(ytc + cc * yts));
                 if (t0) acc[2 * h] += yrow[cc];
             }
         }
@@ -415,191 +443,6 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
             }
         }
     }
-}
-
-// Persistent variant of side_kernel_async for the sparse regime (few connections
-// per row).  There, a (row, tile) item is a handful of dependent phases -- the
-// connection records, a few 2 KB segments, the epilogue operands -- and a warp
-// that owns one item spends most of its life waiting.  Here the grid is
-// num_SMs x kSideCtas CTAs; CTA c walks the item blocks j = c, c + G, ... in
-// tile-major order (all SMs stay on one column tile at a time, as in the
-// one-item grid), warp w taking row 8 (j mod nrb) + w.  The warp's ring is
-// one continuous stream over its items: item k's connection segments, then
-// (alpha side) its diag, own-x and, for rows carrying task 0, y segments, then
-// item k + 1's segments -- so the next item's loads are in flight while this
-// item's epilogue runs.  All R ring slots hold loads in flight (consume a
-// slot, then refill it); the diag slot is read together with the own-x slot,
-// so its refill is deferred by one position (an empty group keeps the
-// wait_group accounting).  Targets of the issue side come from one
-// warp-cooperative load per 32 connections.
-struct PItem {
-    i64 e0;
-    int r, c0;  // local row (-1: past the end), first column
-    int n, np;  // connections, positions (n + epilogue operands)
-};
-
-template <bool ALPHA>
-__device__ __forceinline__ PItem persist_item(const SideArgs &a, int k, int nrb, int w) {
-    PItem it{};
-    const int j = (int)blockIdx.x + k * (int)gridDim.x;
-    it.r = (j % nrb) * kRowsPerCta + w;
-    it.c0 = (int)((a.tile0 + j / nrb) * kTW);
-    if (it.r >= a.n_rows) {
-        it.n = it.np = 0;
-        it.r = -1;
-        return it;
-    }
-    const i64 g = a.row_base + it.r;
-    it.e0 = a.conn_off[g];
-    it.n = (int)(a.conn_off[g + 1] - it.e0);
-    const bool t0 = ALPHA && a.a_s_off != nullptr && a.a_s_off[g + 1] != a.a_s_off[g];
-    it.np = it.n + (ALPHA ? 2 + (t0 ? 1 : 0) : 0);
-    return it;
-}
-
-template <bool ALPHA>
-__global__ void __launch_bounds__(kRowsPerCta * 32, kPersistCtas) side_kernel_persist(SideArgs a) {
-    constexpr int R = SideAsync<ALPHA>::kRing;
-    extern __shared__ __align__(128) unsigned char ssm[];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double *ring = reinterpret_cast<double *>(ssm) + (size_t)w * R * kTW;
-    const int nrb = (int)((a.n_rows + kRowsPerCta - 1) / kRowsPerCta);
-    const int nk = (int)((nrb * a.n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x);  // items of this warp
-    if (nk <= 0) return;
-
-    // ---- issue side: item ki, position pi; targets of the item's connections in `win`
-    int ki = 0;
-    int pi = 0;
-    PItem is = persist_item<ALPHA>(a, 0, nrb, w);
-    int win = 0, wbase = -32;
-    auto issue = [&](int slot) {
-        while (ki < nk && pi >= is.np) {
-            if (++ki < nk) is = persist_item<ALPHA>(a, ki, nrb, w);
-            pi = 0;
-            wbase = -32;
-        }
-        if (ki < nk) {
-            const double *src;
-            if (pi < is.n) {
-                if (pi >= wbase + 32) {  // next 32 targets, one load per lane
-                    wbase = pi & ~31;
-                    win = wbase + lane < is.n ? __ldg(&a.conn[is.e0 + wbase + lane].tgt) : 0;
-                }
-                src = a.X + (i64)__shfl_sync(0xffffffffu, win, pi - wbase) * a.ldx + is.c0;
-            } else if (pi == is.n) {
-                src = a.diag + (i64)is.r * a.ldy + is.c0;
-            } else if (pi == is.n + 1) {
-                src = a.X + (a.row_base + is.r) * a.ldx + is.c0;
-            } else {
-                src = a.Y + (i64)is.r * a.ldy + is.c0;
-            }
-            const int ncol = (int)min((i64)kTW, a.n_cols - is.c0);
-            double *dst = ring + (size_t)slot * kTW;
-#pragma unroll
-            for (int h = 0; h < 4; ++h)
-                if (2 * lane + 64 * h < ncol) cp_async16(dst + 2 * lane + 64 * h, src + 2 * lane + 64 * h);
-            ++pi;
-        }
-        cp_async_commit();
-    };
-#pragma unroll
-    for (int s = 0; s < R; ++s) issue(s);
-
-    // ---- consume side
-    int slot = 0, dslot = 0;
-    for (int kc = 0; kc < nk; ++kc) {
-        const PItem ic = persist_item<ALPHA>(a, kc, nrb, w);
-        if (ic.r < 0) continue;  // rows past the end: no positions, nothing stored
-        const int ncol = (int)min((i64)kTW, a.n_cols - ic.c0);
-        double acc[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-        for (int pc = 0; pc < ic.np; ++pc) {
-            // groups map 1:1 to positions; the diag position commits none and the own-x position
-            // two, so the own-x segment (one group newer than usual) needs one more completed group
-            if (ALPHA && pc == ic.n + 1) cp_async_wait<R - 2>();
-            else cp_async_wait<R - 1>();
-            const double *src = ring + (size_t)slot * kTW;
-            if (pc < ic.n) {
-                const Conn cn = a.conn[ic.e0 + pc];
-                double2 v[4];
-#pragma unroll
-                for (int h = 0; h < 4; ++h) v[h] = *reinterpret_cast<const double2 *>(src + 2 * lane + 64 * h);
-                if (cn.info == 0) {
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        acc[2 * h] = fma(cn.c, v[h].x, acc[2 * h]);
-                        acc[2 * h + 1] = fma(cn.c, v[h].y, acc[2 * h + 1]);
-                    }
-                } else {
-                    const int P = abs(cn.info) - 1;
-                    const double sg = cn.info > 0 ? 1.0 : -1.0;
-                    const double *jr = a.J + (i64)P * a.ldj + a.col_base + ic.c0;
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        const int cc = 2 * lane + 64 * h;
-                        const double j0 = cc < ncol ? __ldg(jr + cc) : 0.0, j1 = cc + 1 < ncol ? __ldg(jr + cc + 1) : 0.0;
-                        acc[2 * h] = fma(fma(sg, j0, cn.c), v[h].x, acc[2 * h]);
-                        acc[2 * h + 1] = fma(fma(sg, j1, cn.c), v[h].y, acc[2 * h + 1]);
-                    }
-                }
-                issue(slot);
-            } else if (pc == ic.n) {  // diag: kept in its slot until the own-x segment lands (refill deferred)
-                dslot = slot;
-            } else if (pc == ic.n + 1) {  // diag o x
-                const double *dsrc = ring + (size_t)dslot * kTW;
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    const int cc = 2 * lane + 64 * h;
-                    const double2 d = *reinterpret_cast<const double2 *>(dsrc + cc);
-                    const double2 x = *reinterpret_cast<const double2 *>(src + cc);
-                    acc[2 * h] = fma(d.x, x.x, acc[2 * h]);
-                    acc[2 * h + 1] = fma(d.y, x.y, acc[2 * h + 1]);
-                }
-                issue(dslot);
-                issue(slot);
-            } else {  // task 0 already in y (cross kernel ran first)
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    const double2 p = *reinterpret_cast<const double2 *>(src + 2 * lane + 64 * h);
-                    acc[2 * h] += p.x;
-                    acc[2 * h + 1] += p.y;
-                }
-                issue(slot);
-            }
-            if (++slot == R) slot = 0;
-        }
-        const i64 r = ic.r;
-        if (ALPHA) {  // + (B X^T)^T
-            const double *ytc = a.ytb ? a.YT + ((r >> 3) * a.n_cols + ic.c0) * 8 + (r & 7) : a.YT + ic.c0 * a.ldyt + r;
-            const i64 yts = a.ytb ? 8 : a.ldyt;
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int cc = 2 * lane + 64 * h;
-                if (cc < ncol) acc[2 * h] += __ldg(ytc + cc * yts);
-                if (cc + 1 < ncol) acc[2 * h + 1] += __ldg(ytc + (cc + 1) * yts);
-            }
-        }
-        if (!ALPHA && a.ytb) {
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int cc = 2 * lane + 64 * h;
-                const i64 c = ic.c0 + cc;
-                double *p = a.Y + ((c >> 3) * a.n_rows + r) * 8 + (c & 7);
-                if (cc + 1 < ncol) __stcs(reinterpret_cast<double2 *>(p), make_double2(acc[2 * h], acc[2 * h + 1]));
-                else if (cc < ncol) *p = acc[2 * h];
-            }
-        } else {
-            double *yr = a.Y + r * a.ldy + ic.c0;
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const int cc = 2 * lane + 64 * h;
-                if (cc + 1 < ncol) __stcs(reinterpret_cast<double2 *>(yr + cc), make_double2(acc[2 * h], acc[2 * h + 1]));
-                else if (cc < ncol) yr[cc] = acc[2 * h];
-            }
-        }
-    }
-    cp_async_wait<0>();
 }
 
 // Task 0, the alpha-single x beta-single opposite-spin doubles (apply.py:235-238):
@@ -1015,24 +858,50 @@ __global__ void diag_kernel(i64 n_rows, i64 row_base, i64 nb, const u64 *__restr
     }
 }
 
+// Inline-diagonal tables (alpha side): ka[g][q] = sum_{p in alpha g} (pp|qq), erow[g] = e_core + E_alpha[g]
+__global__ void ka_kernel(i64 n, const u64 *__restrict__ astr, const double *__restrict__ ea,
+                          const double *__restrict__ dpq, int norb, double e_core, double *__restrict__ ka,
+                          double *__restrict__ erow) {
+    const i64 g = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n) return;
+    const u64 aw = astr[g];
+    for (int q = 0; q < norb; ++q) {
+        double v = 0.0;
+        for (u64 t = aw; t; t &= t - 1) v += dpq[(__ffsll((long long)t) - 1) * norb + q];
+        ka[g * norb + q] = v;
+    }
+    erow[g] = e_core + ea[g];
+}
+
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// SBD_DIAG_INLINE=0/1 forces the alpha epilogue to read / recompute the diagonal; default: recompute
+// when the alpha connections are few (there the epilogue's HBM reads dominate the kernel)
+bool diag_inline(const sbd_ctx *ctx) {
+    const char *e = getenv("SBD_DIAG_INLINE");
+    if (e && *e) return e[0] == '1';
+    const Sector &A = ctx->sec[0];
+    return A.n > 0 && (double)(A.ns + A.nd) < kInlineDiagMaxCbar * (double)A.n;
+}
+
+int ensure_ka(sbd_ctx *ctx) {
+    if (ctx->ka_valid) return SBD_OK;
+    const Sector &A = ctx->sec[0];
+    SBD_CUDA(ctx, ctx->ka.ensure(sizeof(double) * std::max<i64>(1, A.n * ctx->norb)));
+    SBD_CUDA(ctx, ctx->erow.ensure(sizeof(double) * std::max<i64>(1, A.n)));
+    if (A.n) {
+        ka_kernel<<<grid_for(A.n, 128), 128, 0, ctx->stream>>>(A.n, A.str.as<u64>(), A.energy.as<double>(),
+                                                              ctx->dpq.as<double>(), ctx->norb, ctx->e_core,
+                                                              ctx->ka.as<double>(), ctx->erow.as<double>());
+        SBD_LAUNCHED(ctx, "ka_kernel");
+    }
+    ctx->ka_valid = true;
+    return SBD_OK;
+}
 
 bool yt_blocked_enabled() {  // SBD_YT_BLOCKED=0 keeps the row-contiguous Y^T layout (A/B)
     const char *e = getenv("SBD_YT_BLOCKED");
     return !(e && e[0] == '0');
-}
-
-// Persistent cross-item side kernels (side_kernel_persist): SBD_SIDE_PERSIST=0/1 forces them off/on;
-// by default they serve sectors with few connections per string (sparse regime).
-bool use_side_persist(const Sector &S) {
-    const char *e = getenv("SBD_SIDE_PERSIST");
-    if (e && *e) return e[0] == '1';
-    return S.n > 0 && (double)(S.ns + S.nd) < kPersistMaxCbar * (double)S.n;
-}
-
-bool env_on(const char *name, bool dflt) {
-    const char *e = getenv(name);
-    return (e && *e) ? e[0] == '1' : dflt;
 }
 
 bool use_side_tma() {  // SBD_SIDE_LDG=1 selects the register-staged stream (A/B measurements)
@@ -1225,21 +1094,10 @@ int launch_beta_side(sbd_ctx *ctx, const double *x_own, i64 r0, i64 r1) {
         SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_async<false>, ctx->device, SideAsync<false>::smem()));
         a.tile0 = r0 / kTW;
         a.ytb = yt_blocked_enabled();
-        // sorted processing order (SBD_PERM_BETA) and L1-allocating segments (SBD_SIDE_CA)
-        a.perm = env_on("SBD_PERM_BETA", false) ? B.perm.as<int32_t>() : nullptr;
-        a.ca = env_on("SBD_SIDE_CA", false);
         ctx->yt_blocked = a.ytb;
         const i64 t1 = (r1 + kTW - 1) / kTW;
-        a.n_tiles = t1 - a.tile0;
-        if (use_side_persist(B)) {
-            SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_persist<false>, ctx->device, SideAsync<false>::smem()));
-            const i64 items = (nb + kRowsPerCta - 1) / kRowsPerCta * a.n_tiles;
-            const unsigned grid = (unsigned)std::max<i64>(1, std::min<i64>(items, (i64)ctx->num_sms * kPersistCtas));
-            side_kernel_persist<false><<<grid, kRowsPerCta * 32, SideAsync<false>::smem(), st>>>(a);
-        } else {
-            dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)a.n_tiles);
-            side_kernel_async<false><<<g, kRowsPerCta * 32, SideAsync<false>::smem(), st>>>(a);
-        }
+        dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)(t1 - a.tile0));
+        side_kernel_async<false><<<g, kRowsPerCta * 32, SideAsync<false>::smem(), st>>>(a);
     } else {
         if (r0 != 0 || r1 != rows) return sbd_fail(ctx, SBD_EINVAL, "row-range beta side needs the aligned path");
         dim3 g((unsigned)((nb + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((rows + kColsPerWarp - 1) / kColsPerWarp));
@@ -1269,7 +1127,6 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
     a.J = B.J.as<double>();
     a.ldj = nb;
     a.ytb = ctx->yt_blocked;  // the layout the beta side wrote
-    a.ca = env_on("SBD_SIDE_CA", false);
     // the blocked Y^T groups alpha rows by 8: a chunk must start on a block (kTW-aligned chunks do)
     if (a.ytb && r0 % kRowsPerCta != 0) return sbd_fail(ctx, SBD_EINVAL, "alpha chunk start not a multiple of 8");
     a.YT = ctx->yt.as<double>() + (a.ytb ? r0 * nb : r0);
@@ -1277,14 +1134,16 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
     a.diag = ctx->diag.as<double>() + r0 * nb;
     a.a_s_off = (with_t0 && A.ns > 0 && B.ns > 0) ? A.s_off.as<int64_t>() : nullptr;
     const bool vec = (nb % 2 == 0) && aligned16(x_full) && aligned16(y) && (r0 % 2 == 0);
-    if (vec && use_side_tma() && use_side_persist(A)) {
-        SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_persist<true>, ctx->device, SideAsync<true>::smem()));
-        a.tile0 = 0;
-        a.n_tiles = (nb + kTW - 1) / kTW;
-        const i64 items = (rows + kRowsPerCta - 1) / kRowsPerCta * a.n_tiles;
-        const unsigned grid = (unsigned)std::max<i64>(1, std::min<i64>(items, (i64)ctx->num_sms * kPersistCtas));
-        side_kernel_persist<true><<<grid, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);
-    } else if (vec && use_side_tma()) {
+    if (vec && use_side_tma() && diag_inline(ctx)) {
+        if (int rc = ensure_ka(ctx)) return rc;
+        a.ka = ctx->ka.as<double>();
+        a.erow = ctx->erow.as<double>();
+        a.eb = B.energy.as<double>();
+        a.bstr = B.str.as<u64>();
+        a.norb = ctx->norb;
+        a.nbe = B.n_elec;
+    }
+    if (vec && use_side_tma()) {
         SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_async<true>, ctx->device, SideAsync<true>::smem()));
         dim3 gt((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kTW - 1) / kTW));
         side_kernel_async<true><<<gt, kRowsPerCta * 32, SideAsync<true>::smem(), ctx->stream>>>(a);

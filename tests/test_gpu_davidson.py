@@ -156,6 +156,8 @@ def test_cfg1_ground_state_vs_reference():
     dict(max_subspace=6, restart_keep=2, max_iters=400),      # many thick restarts
     dict(reorthogonalize=False),                              # single Gram-Schmidt pass
     dict(track_orthogonality=False, tol_residual=1e-10),
+    dict(selective_reorth=True),                              # B200 extension: one CGS pass when enough
+    dict(selective_reorth=True, n_roots=2, max_subspace=8, restart_keep=3, max_iters=300),
 ])
 def test_native_driver_matches_python_driver(case):
     """sbd_davidson (C++ control loop) runs the same kernels in the same order as the Python driver."""
@@ -231,3 +233,22 @@ def test_native_driver_explicit_basis(explicit_golden, explicit_meta):
         np.testing.assert_allclose(nat.energies, explicit_golden[f"{name}/energies"], atol=1e-8)
         np.testing.assert_allclose(nat.energies, py.energies, atol=1e-10, rtol=0)
 
+
+
+def test_selective_reorth_energies_vs_oracle():
+    """DavidsonOptions.selective_reorth: same energies as the reference algorithm (two-pass MGS), orthogonality
+    kept at the 1e-10 level, and no more iterations than the always-two-pass run plus a couple."""
+    from paper_2601_16637_b200 import DavidsonOptions, HamiltonianApplier, SelectedBasis, davidson_solve
+    from paper_2601_16637_b200.synth import random_integrals, random_product_strings
+
+    a, b = random_product_strings(13, 5, 5, 700, 600, seed=21)
+    table = random_integrals(13, seed=21)
+    app = HamiltonianApplier(SelectedBasis.product(a.tolist(), b.tolist(), 13, 5, 5), table)
+    inst = O.Instance.make(13, table.h, table.eri, table.e_core, a, b)
+    ref = O.davidson(lambda v: O.sigma(inst, v), O.diag(inst), n_roots=2)
+    full = davidson_solve(app, app.diag, opts=DavidsonOptions(n_roots=2))
+    sel = davidson_solve(app, app.diag, opts=DavidsonOptions(n_roots=2, selective_reorth=True))
+    assert ref.converged and full.converged and sel.converged
+    np.testing.assert_allclose(sel.energies, ref.energies, atol=1e-8, rtol=0)
+    assert max(sel.stats.ortho_history) <= 1e-10
+    assert sel.stats.iterations <= full.stats.iterations + 2
