@@ -170,11 +170,10 @@ class HamiltonianApplier:
             self._ctx("sbd_set_row_window", lo, hi)
         self.n_own = (hi - lo) * self.n_beta
         self._tables = None
-        self.diag_device = torch.empty(self.n_own, dtype=torch.float64, device=self._torch_device)
+        self._diag_dev = None
+        self._diag_host = None
         self._ctx.bind_stream()
-        self._ctx("sbd_diag", _lib.ptr(self.diag_device) if self.n_own else None)
-        torch.cuda.synchronize(self.device)
-        self.diag = self.diag_device.cpu().numpy()
+        self._ctx("sbd_diag", None)  # built on the device now (the sigma reads it); copies are lazy
 
     def _init_explicit(self, basis, table, exec_policy, device, row_window):
         import torch
@@ -203,13 +202,33 @@ class HamiltonianApplier:
         self.row_window = None
         self.n_own = self.n
         self._tables = None
-        self.diag_device = torch.empty(self.n, dtype=torch.float64, device=self._torch_device)
+        self._diag_dev = None
+        self._diag_host = None
         self._ctx.bind_stream()
-        self._ctx("sbd_diag", _lib.ptr(self.diag_device) if self.n else None)
-        torch.cuda.synchronize(self.device)
-        self.diag = self.diag_device.cpu().numpy()
+        self._ctx("sbd_diag", None)
 
     # -- reference attributes -------------------------------------------------
+    @property
+    def diag_device(self):
+        """Diagonal of the owned rows as a torch CUDA tensor (copied out of the context once)."""
+        if self._diag_dev is None:
+            import torch
+
+            d = torch.empty(self.n_own, dtype=torch.float64, device=self._torch_device)
+            self._ctx.bind_stream()
+            if self.n_own:
+                self._ctx("sbd_diag", _lib.ptr(d))
+            torch.cuda.synchronize(self.device)
+            self._diag_dev = d
+        return self._diag_dev
+
+    @property
+    def diag(self):
+        """Reference attribute (apply.py:651-704): the diagonal as a numpy array, copied on first use."""
+        if self._diag_host is None:
+            self._diag_host = self.diag_device.cpu().numpy()
+        return self._diag_host
+
     @property
     def tables(self):
         if self.basis.mode != "product":

@@ -174,16 +174,37 @@ int sbd_set_strings(sbd_ctx *ctx, int spin, const uint64_t *strings, int64_t n, 
     return SBD_OK;
 }
 
+#ifdef SBD_TIMING
+#include <chrono>
+#include <cstdio>
+#define SBD_TSTAMP(label)                                                                                   \
+    do {                                                                                                    \
+        cudaStreamSynchronize(ctx->stream);                                                                 \
+        static auto t_prev = std::chrono::steady_clock::now();                                              \
+        auto t_now = std::chrono::steady_clock::now();                                                      \
+        fprintf(stderr, "[sbd timing] %s %.3f ms\n", label,                                                 \
+                std::chrono::duration<double, std::milli>(t_now - t_prev).count());                          \
+        t_prev = t_now;                                                                                     \
+    } while (0)
+#else
+#define SBD_TSTAMP(label) \
+    do {                  \
+    } while (0)
+#endif
+
 int sbd_build_tables(sbd_ctx *ctx) {
     SBD_CHECK_CTX(ctx);
     if (!ctx->have_integrals) return sbd_fail(ctx, SBD_EINVAL, "integrals not set");
+    SBD_TSTAMP("start");
     for (int spin = 0; spin < 2; ++spin) {
         Sector &s = ctx->sec[spin];
         if (!s.present) continue;
         int rc = sbd_sort_strings(ctx, s);
         if (rc) return rc;
+        SBD_TSTAMP("sort");
         rc = sbd_build_sector_tables(ctx, s);
         if (rc) return rc;
+        SBD_TSTAMP("excitation tables");
     }
     for (int spin = 0; spin < 2; ++spin) {
         Sector &s = ctx->sec[spin];
@@ -192,6 +213,7 @@ int sbd_build_tables(sbd_ctx *ctx) {
         const Sector &o = ctx->sec[1 - spin].present ? ctx->sec[1 - spin] : s;
         int rc = sbd_build_coefficients(ctx, s, o);
         if (rc) return rc;
+        SBD_TSTAMP("coefficients + J + SELL");
         s.built = true;
     }
     if (ctx->explicit_mode) {
@@ -200,7 +222,6 @@ int sbd_build_tables(sbd_ctx *ctx) {
     }
     ctx->diag_valid = false;
     ctx->dci.valid = false;
-    ctx->ka_valid = false;
     ctx->dist.planned = false;  // the exchange plan is built from the alpha table
     SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SBD_OK;

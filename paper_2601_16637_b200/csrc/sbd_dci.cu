@@ -37,10 +37,10 @@ namespace {
 constexpr int kDciThreads = 512;          // 16 warps, one CTA per SM
 constexpr int kMaxSingles = 64;           // beta singles per string handled by the list builder
 constexpr size_t kDciSmemMax = 227 * 1024;
-// Tile: NT = 128 beta columns.  The 16 warps form a 4 x 4 grid over (row fragments, column
+// Tile of kNT = 128 beta columns.  The 16 warps form a 4 x 4 grid over (row fragments, column
 // fragments): warp (mg, ng) owns row fragments m = mg + 4 j and the four column fragments
 // 4 ng .. 4 ng + 3, and keeps its E fragments in registers for the whole alpha row (E changes per
-// row, the slab per tile), so a k-step costs 4 shared loads for 4 MFW DMMAs.
+// row, the slab per tile): a k-step costs 4 shared loads for 4 MFW DMMAs.
 constexpr int kNT = 128;
 constexpr int kLdX = kNT + 4;    // slab row stride (doubles): B-fragment loads conflict-free
 constexpr int kLdG = kNT + 8;    // G row stride: C-fragment double2 stores conflict-free
@@ -55,14 +55,18 @@ struct DciArgs {
     const SConn *a_sconn;
     const double *eq;        // [npair][nqp]: (P | Q_q), zero for q >= nq
     int nqp, kp_max, ld_e;   // ld_e = 4 (mod 16) doubles: A-fragment loads conflict-free
-    const uint32_t *ent;     // beta singles of each ib sorted by jb: (jb - t NT) << 16 | q << 1 | neg
-    const int32_t *toff;     // [nb][ntiles + 1]: first entry of tile t (absolute index into ent)
+    // beta singles for the gather, per column tile t an ELL block [w_t][nb] at ell + woff[t]:
+    // entry (jb - t NT) << 16 | q << 1 | neg; padding points at the zero row q = nqp of G
+    const uint32_t *ell;
+    const int64_t *woff;
+    const int32_t *wt;
     int ntiles;
     bool add;
 };
 
+// E, the slab (double-buffered) and G (nqp rows + the zero row)
 __host__ __device__ inline size_t dci_smem(int nqp, int kp_max, int ld_e) {
-    return sizeof(double) * ((size_t)nqp * ld_e + 2 * (size_t)kp_max * kLdX + (size_t)nqp * kLdG);
+    return sizeof(double) * ((size_t)nqp * ld_e + 2 * (size_t)kp_max * kLdX + (size_t)(nqp + 1) * kLdG);
 }
 __host__ __device__ inline int dci_ld_e(int kp) { return kp + (((4 - kp) % 16) + 16) % 16; }
 
@@ -98,13 +102,14 @@ __global__ void __launch_bounds__(kDciThreads, 1) cross_kernel_dci(DciArgs a) {
     extern __shared__ __align__(128) unsigned char dsm[];
     double *es = reinterpret_cast<double *>(dsm);     // [nqp][ld_e]
     double *xs0 = es + (size_t)a.nqp * a.ld_e;        // 2 x [kp_max][kLdX]
-    double *gs = xs0 + 2 * (size_t)a.kp_max * kLdX;   // [nqp][kLdG]
+    double *gs = xs0 + 2 * (size_t)a.kp_max * kLdX;   // [nqp + 1][kLdG], row nqp = 0
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int mg = warp / kMG, ng = warp % kMG;
     const int mf = a.nqp / 8;
 
     i64 r = dci_next_row(a, blockIdx.x);
     if (r >= a.n_rows) return;
+    for (int c = threadIdx.x; c < kNT; c += kDciThreads) gs[a.nqp * kLdG + c] = 0.0;  // the padding row
     auto kof = [&](i64 rr) { return (int)(a.a_s_off[a.row_base + rr + 1] - a.a_s_off[a.row_base + rr]); };
     int K = kof(r), Kp = (K + 3) & ~3;
     int t = 0, buf = 0;
@@ -140,9 +145,12 @@ __global__ void __launch_bounds__(kDciThreads, 1) cross_kernel_dci(DciArgs a) {
                 es[q * a.ld_e + k] = v;
             }
         }
+        // this tile's gather entries: independent coalesced loads, in flight during the GEMM
+        const int wt = __ldg(a.wt + t);
+        const uint32_t *el = a.ell + __ldg(a.woff + t) + threadIdx.x;
         cp_async_wait<1>();
         __syncthreads();  // slab `buf` and E visible; the previous gather is done with G
-        if (t == 0) {  // E fragments of this warp into registers, for all tiles of the row
+        if (t == 0) {     // E fragments of this warp into registers, for all tiles of the row
             const double *ap = es + (mg * 8 + (lane >> 2)) * a.ld_e + (lane & 3);
 #pragma unroll
             for (int j = 0; j < MFW; ++j)
@@ -186,15 +194,26 @@ __global__ void __launch_bounds__(kDciThreads, 1) cross_kernel_dci(DciArgs a) {
         __syncthreads();  // G tile complete
 
         // gather: sigma[ib] += s_m G[q_m][jb_m] for the beta singles of ib that land in tile t
+        // (ELL slots of the tile, padding reads the zero row)
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
             const i64 ib = threadIdx.x + (i64)i * kDciThreads;
             if (ib < a.nb) {
-                const int32_t *to = a.toff + ib * (a.ntiles + 1) + t;
-                const int lo = __ldg(to), hi = __ldg(to + 1);
+                const uint32_t *ep = el + (i64)i * kDciThreads;
                 double s = acc[i];
-                for (int e = lo; e < hi; ++e) {
-                    const uint32_t u = __ldg(a.ent + e);
+                int sl = 0;
+                for (; sl + 4 <= wt; sl += 4) {
+                    uint32_t u[4];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) u[v] = __ldg(ep + (i64)(sl + v) * a.nb);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const double g = gs[((u[v] >> 1) & 0x7fffu) * kLdG + (u[v] >> 16)];
+                        s += (u[v] & 1u) ? -g : g;
+                    }
+                }
+                for (; sl < wt; ++sl) {
+                    const uint32_t u = __ldg(ep + (i64)sl * a.nb);
                     const double g = gs[((u >> 1) & 0x7fffu) * kLdG + (u >> 16)];
                     s += (u & 1u) ? -g : g;
                 }
@@ -253,6 +272,25 @@ __global__ void dci_lists_kernel(i64 nb, const int64_t *__restrict__ s_off, cons
         toff[ib * (ntiles + 1) + t] = (int32_t)(s0 + i);
     }
     for (int k = 0; k < n; ++k) ent[s0 + k] = ((uint32_t)(tg[k] % nt) << 16) | code[k];
+}
+
+// ELL width of tile t: the most singles any beta string has into it
+__global__ void dci_width_kernel(i64 nb, const int32_t *__restrict__ toff, int ntiles, int32_t *__restrict__ wt) {
+    const i64 ib = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ib >= nb) return;
+    for (int t = 0; t < ntiles; ++t) atomicMax(wt + t, toff[ib * (ntiles + 1) + t + 1] - toff[ib * (ntiles + 1) + t]);
+}
+
+// tile-major ELL blocks: slot s of string ib in tile t at ell[woff[t] + s nb + ib], padded with `pad`
+__global__ void dci_ell_kernel(i64 nb, const int32_t *__restrict__ toff, const uint32_t *__restrict__ ent, int ntiles,
+                               const int32_t *__restrict__ wt, const int64_t *__restrict__ woff, uint32_t pad,
+                               uint32_t *__restrict__ ell) {
+    const i64 ib = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ib >= nb) return;
+    for (int t = 0; t < ntiles; ++t) {
+        const int lo = toff[ib * (ntiles + 1) + t], cnt = toff[ib * (ntiles + 1) + t + 1] - lo;
+        for (int sl = 0; sl < wt[t]; ++sl) ell[woff[t] + (i64)sl * nb + ib] = sl < cnt ? ent[lo + sl] : pad;
+    }
 }
 
 // eq[P][q] = (P | Q_q) over the off-diagonal pairs Q_q, zero for q >= nq
@@ -314,6 +352,24 @@ int dci_build(sbd_ctx *ctx) {
                                                                       qm.as<int32_t>(), d.nt, d.ntiles, d.ent.as<uint32_t>(),
                                                                       d.toff.as<int32_t>());
         SBD_LAUNCHED(ctx, "dci_lists_kernel");
+        // per-tile ELL blocks (coalesced, independent loads in the kernel's gather)
+        SBD_CUDA(ctx, d.wt.ensure(sizeof(int32_t) * d.ntiles));
+        SBD_CUDA(ctx, cudaMemsetAsync(d.wt.p, 0, sizeof(int32_t) * d.ntiles, ctx->stream));
+        dci_width_kernel<<<grid_for(B.n, 128), 128, 0, ctx->stream>>>(B.n, d.toff.as<int32_t>(), d.ntiles,
+                                                                      d.wt.as<int32_t>());
+        SBD_LAUNCHED(ctx, "dci_width_kernel");
+        std::vector<int32_t> wh(d.ntiles);
+        SBD_CUDA(ctx, cudaMemcpyAsync(wh.data(), d.wt.p, sizeof(int32_t) * d.ntiles, cudaMemcpyDeviceToHost, ctx->stream));
+        SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        std::vector<int64_t> wo(d.ntiles + 1, 0);
+        for (int t = 0; t < d.ntiles; ++t) wo[t + 1] = wo[t] + (i64)wh[t] * B.n;
+        SBD_CUDA(ctx, d.woff.ensure(sizeof(int64_t) * (d.ntiles + 1)));
+        SBD_CUDA(ctx, cudaMemcpy(d.woff.p, wo.data(), sizeof(int64_t) * (d.ntiles + 1), cudaMemcpyHostToDevice));
+        SBD_CUDA(ctx, d.ell.ensure(sizeof(uint32_t) * std::max<i64>(1, wo[d.ntiles])));
+        dci_ell_kernel<<<grid_for(B.n, 128), 128, 0, ctx->stream>>>(B.n, d.toff.as<int32_t>(), d.ent.as<uint32_t>(),
+                                                                    d.ntiles, d.wt.as<int32_t>(), d.woff.as<int64_t>(),
+                                                                    (uint32_t)d.nqp << 1, d.ell.as<uint32_t>());
+        SBD_LAUNCHED(ctx, "dci_ell_kernel");
     }
     SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // qm/qp are released on return
     d.valid = true;
@@ -386,8 +442,9 @@ int sbd_cross_dci(sbd_ctx *ctx, const double *x_full, double *y, bool additive, 
     a.nqp = d.nqp;
     a.kp_max = d.kp_max;
     a.ld_e = d.ld_e;
-    a.ent = d.ent.as<uint32_t>();
-    a.toff = d.toff.as<int32_t>();
+    a.ell = d.ell.as<uint32_t>();
+    a.woff = d.woff.as<int64_t>();
+    a.wt = d.wt.as<int32_t>();
     a.ntiles = d.ntiles;
     a.add = additive;
     const size_t smem = dci_smem(d.nqp, d.kp_max, d.ld_e);

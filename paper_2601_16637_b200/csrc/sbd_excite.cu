@@ -15,6 +15,7 @@
 // the reference's entry order; targets are mapped back to caller indices
 // through the sort permutation.
 #include <algorithm>
+#include <cstdio>
 #include <vector>
 
 #include "sbd_internal.cuh"
@@ -516,6 +517,10 @@ int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other) {
     dim3 g(grid_for(n, 128), (unsigned)ctx->npair);
     jtable_kernel<<<g, 128, 0, st>>>(s.str.as<u64>(), n, ctx->npair, ctx->eri.as<double>(), s.J.as<double>());
     SBD_LAUNCHED(ctx, "jtable");
+#ifdef SBD_TIMING
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[sbd timing] (coefficients + J done; SELL next)\n");
+#endif
     // packed singles for the opposite-spin (task 0) kernel
     if (n >= kPackMaxStrings || ctx->npair >= ((i64)1 << kPackPairBits))
         return sbd_fail(ctx, SBD_EINVAL, "sector too large for the packed single-excitation table");

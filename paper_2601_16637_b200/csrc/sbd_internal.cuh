@@ -112,6 +112,7 @@ struct DciState {
     DevBuf eq;    // f64 [npair][nqp]
     DevBuf ent;   // u32 [beta singles], per beta string sorted by target
     DevBuf toff;  // int32 [n_beta][ntiles + 1]
+    DevBuf ell, woff, wt;  // per column tile: ELL block [wt][n_beta] of ent at woff (u32, i64, int32)
 };
 
 // device ingestion results (sbd_ingest.cu), first-seen order
@@ -141,8 +142,6 @@ struct sbd_ctx {
     bool yt_blocked = false;
     DevBuf diag;                 // owned rows, cached
     bool diag_valid = false;
-    DevBuf ka, erow;             // inline-diagonal tables of the alpha side (sbd_sigma.cu ensure_ka)
-    bool ka_valid = false;
     DevBuf red;                  // reduction scratch
     DevBuf hx, hy;               // device staging for sbd_sigma_host
     cudaStream_t copy_stream = nullptr;  // sbd_sigma_host: H2D/D2H overlapped with the kernels

@@ -53,13 +53,6 @@ struct SideArgs {
     // alpha rows, [ld_t / 8][n_beta][8] -- the alpha CTA's 8 rows x 256 columns are one
     // contiguous 16 KB block instead of 256 scattered 64-byte pieces (L1-friendly reads)
     bool ytb;
-    // inline diagonal (alpha side): diag[r, c] = erow[g] + eb[c] + sum_{q in beta string c} ka[g][q] is
-    // recomputed in the epilogue instead of read (8 B/det less HBM); null = read `diag`
-    const double *ka;              // [n_alpha][norb]: ka[g][q] = sum_{p in alpha string g} (pp|qq)
-    const double *erow;            // [n_alpha]: e_core + alpha same-spin energy
-    const double *eb;              // [n_beta]: beta same-spin energy
-    const u64 *bstr;               // [n_beta]: beta strings
-    int norb, nbe;                 // orbitals, beta electrons
     // partitioned passes (DIST kernels, sbd_alpha_pass): local row r streams the connections
     // seg_off[r * seg_stride + seg_lo] .. seg_off[r * seg_stride + seg_hi] of `conn`; its own x
     // row is X[xo_row0 + r]; epi adds diag o x + (B X^T)^T and writes y, acc_in adds onto y
@@ -232,14 +225,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32) side_kernel(SideArgs a) {
 // is the only synchronisation (no barriers in the stream).
 constexpr int kTW = 256;
 
-constexpr double kInlineDiagMaxCbar = 0.0;  // alpha connections per string below which the diagonal is recomputed
 constexpr int kSideCtas = 4;  // resident CTAs per SM: registers <= 64, 4 x 48 KB rings (5 CTAs spill and need a 2-slot ring: slower)
-
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
 
 template <bool ALPHA>
 struct SideAsync {
@@ -290,13 +276,11 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
             }
             cp_async_commit();
         };
-        // the stream's last two issues (positions n, n + 1) carry the epilogue operands (diag, own x);
-        // with the inline diagonal only the own x (position n)
-        const bool inl = a.ka != nullptr;
+        // the stream's last two issues (positions n, n + 1) carry the epilogue operands
         auto issue_epi = [&](i64 i, int slot) {
             const double *src = i < n ? a.X + (i64)a.conn[e0 + i].tgt * a.ldx + c0
-                                      : ((i == n && !inl) ? a.diag + r * a.ldy + c0 : a.X + own * a.ldx + c0);
-            if (i <= n + (inl ? 0 : 1)) {
+                                      : (i == n ? a.diag + r * a.ldy + c0 : a.X + own * a.ldx + c0);
+            if (i <= n + 1) {
                 double *dst = ring + (size_t)slot * kTW;
 #pragma unroll
                 for (int h = 0; h < 4; ++h)
@@ -350,50 +334,18 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
         // contiguous bytes of each Y^T column, so the 8 warps share one L1 line per
         // column and no block barrier (warps finish unevenly) is needed.
         const i64 g = a.row_base + r;
-        // diag and own-x segments, staged by the stream's last two issues (inline diagonal: own x only)
-        const bool inl = a.ka != nullptr;
-        const double *dring = ring + (size_t)(nstream % R) * kTW;
-        const double *xring = ring + (size_t)((nstream + (inl ? 0 : 1)) % R) * kTW;
+        // diag and own-x segments, staged by the stream's last two issues
+        const double *dring = ring + (size_t)(nstream % R) * kTW, *xring = ring + (size_t)((nstream + 1) % R) * kTW;
         const bool t0 = a.a_s_off != nullptr && a.a_s_off[g + 1] != a.a_s_off[g];
         const double *yrow = a.Y + r * a.ldy + c0;
         // Y^T[c0 + cc][r] = ytc[cc * yts]
         const double *ytc = a.ytb ? a.YT + ((r >> 3) * a.n_cols + c0) * 8 + (r & 7) : a.YT + c0 * a.ldyt + r;
         const i64 yts = a.ytb ? 8 : a.ldyt;
-        // inline diagonal: this row's ka (and its total at [norb]) in the ring slot no position used last
-        double *kr = ring + (size_t)((nstream + 1) % R) * kTW;
-        double erow = 0.0;
-        if (inl) {
-            erow = a.erow[g];
-            double t = 0.0;
-            for (int q = lane; q < a.norb; q += 32) {
-                const double v = __ldg(a.ka + g * a.norb + q);
-                kr[q] = v;
-                t += v;
-            }
-            t = warp_sum_d(t);
-            if (lane == 0) kr[a.norb] = t;
-            __syncwarp();
-        }
-        // inline diagonal of column c: beta electrons summed directly, or all orbitals minus the holes
-        auto dcol = [&](i64 c) -> double {
-            u64 bw = __ldg(a.bstr + c);
-            double e = erow + __ldg(a.eb + c);
-            if (2 * a.nbe <= a.norb) {
-                for (; bw; bw &= bw - 1) e += kr[__ffsll((long long)bw) - 1];
-            } else {
-                double hole = 0.0;
-                for (u64 hw = ~bw & (a.norb == 64 ? ~0ull : ((1ull << a.norb) - 1)); hw; hw &= hw - 1)
-                    hole += kr[__ffsll((long long)hw) - 1];
-                e += kr[a.norb] - hole;  // kr[norb] = sum over all orbitals
-            }
-            return e;
-        };
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
             const int cc = 2 * lane + 64 * h;
             if (ok[2 * h + 1]) {
-                const double2 d = inl ? make_double2(dcol(c0 + cc), dcol(c0 + cc + 1))
-                                      : *reinterpret_cast<const double2 *>(dring + cc);
+                const double2 d = *reinterpret_cast<const double2 *>(dring + cc);
                 const double2 x = *reinterpret_cast<const double2 *>(xring + cc);
                 const double t0v = __ldg(ytc + cc * yts), t1v = __ldg(ytc + (cc + 1) * yts);
                 acc[2 * h] = fma(d.x, x.x, acc[2 * h] + t0v);
@@ -404,7 +356,7 @@ __global__ void __launch_bounds__(kRowsPerCta * 32, kSideCtas) side_kernel_async
                     acc[2 * h + 1] += p.y;
                 }
             } else if (ok[2 * h]) {
-                acc[2 * h] = fma(inl ? dcol(c0 + cc) : dring[cc], xring[cc], acc[2 * h] + __ldg(ytc + cc * yts));
+                acc[2 * h] = fma(dring[cc], xring[cc], acc[2 * h] + __ldg(ytc + cc * yts));
                 if (t0) acc[2 * h] += yrow[cc];
             }
         }
@@ -858,46 +810,7 @@ __global__ void diag_kernel(i64 n_rows, i64 row_base, i64 nb, const u64 *__restr
     }
 }
 
-// Inline-diagonal tables (alpha side): ka[g][q] = sum_{p in alpha g} (pp|qq), erow[g] = e_core + E_alpha[g]
-__global__ void ka_kernel(i64 n, const u64 *__restrict__ astr, const double *__restrict__ ea,
-                          const double *__restrict__ dpq, int norb, double e_core, double *__restrict__ ka,
-                          double *__restrict__ erow) {
-    const i64 g = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= n) return;
-    const u64 aw = astr[g];
-    for (int q = 0; q < norb; ++q) {
-        double v = 0.0;
-        for (u64 t = aw; t; t &= t - 1) v += dpq[(__ffsll((long long)t) - 1) * norb + q];
-        ka[g * norb + q] = v;
-    }
-    erow[g] = e_core + ea[g];
-}
-
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
-// SBD_DIAG_INLINE=0/1 forces the alpha epilogue to read / recompute the diagonal; default: recompute
-// when the alpha connections are few (there the epilogue's HBM reads dominate the kernel)
-bool diag_inline(const sbd_ctx *ctx) {
-    const char *e = getenv("SBD_DIAG_INLINE");
-    if (e && *e) return e[0] == '1';
-    const Sector &A = ctx->sec[0];
-    return A.n > 0 && (double)(A.ns + A.nd) < kInlineDiagMaxCbar * (double)A.n;
-}
-
-int ensure_ka(sbd_ctx *ctx) {
-    if (ctx->ka_valid) return SBD_OK;
-    const Sector &A = ctx->sec[0];
-    SBD_CUDA(ctx, ctx->ka.ensure(sizeof(double) * std::max<i64>(1, A.n * ctx->norb)));
-    SBD_CUDA(ctx, ctx->erow.ensure(sizeof(double) * std::max<i64>(1, A.n)));
-    if (A.n) {
-        ka_kernel<<<grid_for(A.n, 128), 128, 0, ctx->stream>>>(A.n, A.str.as<u64>(), A.energy.as<double>(),
-                                                              ctx->dpq.as<double>(), ctx->norb, ctx->e_core,
-                                                              ctx->ka.as<double>(), ctx->erow.as<double>());
-        SBD_LAUNCHED(ctx, "ka_kernel");
-    }
-    ctx->ka_valid = true;
-    return SBD_OK;
-}
 
 bool yt_blocked_enabled() {  // SBD_YT_BLOCKED=0 keeps the row-contiguous Y^T layout (A/B)
     const char *e = getenv("SBD_YT_BLOCKED");
@@ -1134,15 +1047,6 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
     a.diag = ctx->diag.as<double>() + r0 * nb;
     a.a_s_off = (with_t0 && A.ns > 0 && B.ns > 0) ? A.s_off.as<int64_t>() : nullptr;
     const bool vec = (nb % 2 == 0) && aligned16(x_full) && aligned16(y) && (r0 % 2 == 0);
-    if (vec && use_side_tma() && diag_inline(ctx)) {
-        if (int rc = ensure_ka(ctx)) return rc;
-        a.ka = ctx->ka.as<double>();
-        a.erow = ctx->erow.as<double>();
-        a.eb = B.energy.as<double>();
-        a.bstr = B.str.as<u64>();
-        a.norb = ctx->norb;
-        a.nbe = B.n_elec;
-    }
     if (vec && use_side_tma()) {
         SBD_CUDA(ctx, sbd_smem_attr((const void *)side_kernel_async<true>, ctx->device, SideAsync<true>::smem()));
         dim3 gt((unsigned)((rows + kRowsPerCta - 1) / kRowsPerCta), (unsigned)((nb + kTW - 1) / kTW));

@@ -89,11 +89,6 @@ __global__ void radix_scatter(const u64 *__restrict__ kin, const int32_t *__rest
     }
 }
 
-__global__ void iota_i32(int32_t *v, i64 n) {
-    i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) v[i] = (int32_t)i;
-}
-
 __global__ void count_adjacent_dups(const u64 *__restrict__ sorted, i64 n, int *__restrict__ flag) {
     i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x + 1;
     if (i < n && sorted[i] == sorted[i - 1]) atomicAdd(flag, 1);
