@@ -135,6 +135,9 @@ int sbd_dense_rows(sbd_ctx *ctx, int64_t row0, int64_t nrows, double *out_dev);
 /* Mean in-set alpha connections per alpha string (c-bar)
  * and the algorithmic sigma bytes 8*N_own*(3 + c-bar). */
 int sbd_sigma_model(sbd_ctx *ctx, double *cbar_alpha, double *bytes_per_sigma);
+/* Which task-0 kernel (the alpha-single x beta-single term, apply.py:228-238) the last sigma ran:
+ * 0 none, 1 SELL cluster multicast, 2 SELL TMA-staged, 3 SELL flat, 4 direct-CI on DMMA. */
+int sbd_last_task0(sbd_ctx *ctx, int *kind);
 
 /* ---- Multi-GPU: alpha-block partition, one context (process) per GPU ----
  * Replaces DistributedApplier (distsim.py:130-316) and its ring

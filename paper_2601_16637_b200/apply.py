@@ -242,6 +242,13 @@ class HamiltonianApplier:
     def context(self) -> _lib.Context:
         return self._ctx
 
+    def task0_kernel(self) -> str:
+        """The task-0 kernel the last sigma ran (B200 introspection: "sell-cluster", "sell-tma",
+        "sell-flat", "direct-ci" or "none")."""
+        k = ctypes.c_int()
+        self._ctx("sbd_last_task0", ctypes.byref(k))
+        return {0: "none", 1: "sell-cluster", 2: "sell-tma", 3: "sell-flat", 4: "direct-ci"}[k.value]
+
     def sigma_model(self):
         """(c-bar_alpha, algorithmic bytes per sigma) -- BASELINE.md section 4."""
         cb, by = ctypes.c_double(), ctypes.c_double()

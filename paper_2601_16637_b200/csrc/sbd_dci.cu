@@ -56,17 +56,19 @@ struct DciArgs {
     const double *eq;        // [npair][nqp]: (P | Q_q), zero for q >= nq
     int nqp, kp_max, ld_e;   // ld_e = 4 (mod 16) doubles: A-fragment loads conflict-free
     // beta singles for the gather, per column tile t an ELL block [w_t][nb] at ell + woff[t]:
-    // entry (jb - t NT) << 16 | q << 1 | neg; padding points at the zero row q = nqp of G
-    const uint32_t *ell;
+    // u16 entry (jb - t NT) << 8 | q << 1 | neg; padding points at the zero row q = nqp (< 128) of G
+    const uint16_t *ell;
     const int64_t *woff;
     const int32_t *wt;
     int ntiles;
+    int wmax;                // widest tile block (its [wmax][nb] u16 is staged into shared memory)
     bool add;
 };
 
-// E, the slab (double-buffered) and G (nqp rows + the zero row)
-__host__ __device__ inline size_t dci_smem(int nqp, int kp_max, int ld_e) {
-    return sizeof(double) * ((size_t)nqp * ld_e + 2 * (size_t)kp_max * kLdX + (size_t)(nqp + 1) * kLdG);
+// E, the slab (double-buffered), G (nqp rows + the zero row) and one tile's ELL block
+__host__ __device__ inline size_t dci_smem(int nqp, int kp_max, int ld_e, i64 ell_entries = 0) {
+    return sizeof(double) * ((size_t)nqp * ld_e + 2 * (size_t)kp_max * kLdX + (size_t)(nqp + 1) * kLdG) +
+           sizeof(uint16_t) * (size_t)((ell_entries + 7) & ~(i64)7);
 }
 __host__ __device__ inline int dci_ld_e(int kp) { return kp + (((4 - kp) % 16) + 16) % 16; }
 
@@ -89,6 +91,14 @@ __device__ __forceinline__ void dci_stage(const DciArgs &a, double *xs, i64 row,
     }
 }
 
+// tile t's ELL block [wt][nb] (contiguous in global memory) into shared memory, 16-byte copies
+__device__ __forceinline__ void dci_stage_ell(const DciArgs &a, uint16_t *es_ell, int t) {
+    // blocks are padded to 8 entries (16 bytes) in global memory, so whole 16-byte chunks copy
+    const i64 chunks = ((i64)__ldg(a.wt + t) * a.nb + 7) / 8, base = __ldg(a.woff + t);
+    const uint16_t *src = a.ell + base;
+    for (i64 c = threadIdx.x; c < chunks; c += kDciThreads) cp_async16(es_ell + 8 * c, src + 8 * c);
+}
+
 // next row of this CTA that has alpha singles (n_rows if none)
 __device__ __forceinline__ i64 dci_next_row(const DciArgs &a, i64 r) {
     for (; r < a.n_rows; r += gridDim.x)
@@ -103,6 +113,7 @@ __global__ void __launch_bounds__(kDciThreads, 1) cross_kernel_dci(DciArgs a) {
     double *es = reinterpret_cast<double *>(dsm);     // [nqp][ld_e]
     double *xs0 = es + (size_t)a.nqp * a.ld_e;        // 2 x [kp_max][kLdX]
     double *gs = xs0 + 2 * (size_t)a.kp_max * kLdX;   // [nqp + 1][kLdG], row nqp = 0
+    uint16_t *els = reinterpret_cast<uint16_t *>(gs + (size_t)(a.nqp + 1) * kLdG);  // [wt][nb] of the tile
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int mg = warp / kMG, ng = warp % kMG;
     const int mf = a.nqp / 8;
@@ -114,6 +125,8 @@ __global__ void __launch_bounds__(kDciThreads, 1) cross_kernel_dci(DciArgs a) {
     int K = kof(r), Kp = (K + 3) & ~3;
     int t = 0, buf = 0;
     dci_stage(a, xs0, a.row_base + r, 0, K, Kp);
+    cp_async_commit();
+    dci_stage_ell(a, els, 0);
     cp_async_commit();
 
     double acc[PPT];
@@ -145,11 +158,9 @@ __global__ void __launch_bounds__(kDciThreads, 1) cross_kernel_dci(DciArgs a) {
                 es[q * a.ld_e + k] = v;
             }
         }
-        // this tile's gather entries: independent coalesced loads, in flight during the GEMM
         const int wt = __ldg(a.wt + t);
-        const uint32_t *el = a.ell + __ldg(a.woff + t) + threadIdx.x;
-        cp_async_wait<1>();
-        __syncthreads();  // slab `buf` and E visible; the previous gather is done with G
+        cp_async_wait<1>();  // everything but the next item's slab: this slab and this tile's ELL block
+        __syncthreads();  // slab `buf`, E and the ELL block visible; the previous gather is done with G
         if (t == 0) {     // E fragments of this warp into registers, for all tiles of the row
             const double *ap = es + (mg * 8 + (lane >> 2)) * a.ld_e + (lane & 3);
 #pragma unroll
@@ -194,32 +205,24 @@ __global__ void __launch_bounds__(kDciThreads, 1) cross_kernel_dci(DciArgs a) {
         __syncthreads();  // G tile complete
 
         // gather: sigma[ib] += s_m G[q_m][jb_m] for the beta singles of ib that land in tile t
-        // (ELL slots of the tile, padding reads the zero row)
+        // (ELL slots of the tile from shared memory, padding reads the zero row)
 #pragma unroll
         for (int i = 0; i < PPT; ++i) {
             const i64 ib = threadIdx.x + (i64)i * kDciThreads;
             if (ib < a.nb) {
-                const uint32_t *ep = el + (i64)i * kDciThreads;
+                const uint16_t *ep = els + ib;
                 double s = acc[i];
-                int sl = 0;
-                for (; sl + 4 <= wt; sl += 4) {
-                    uint32_t u[4];
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) u[v] = __ldg(ep + (i64)(sl + v) * a.nb);
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const double g = gs[((u[v] >> 1) & 0x7fffu) * kLdG + (u[v] >> 16)];
-                        s += (u[v] & 1u) ? -g : g;
-                    }
-                }
-                for (; sl < wt; ++sl) {
-                    const uint32_t u = __ldg(ep + (i64)sl * a.nb);
-                    const double g = gs[((u >> 1) & 0x7fffu) * kLdG + (u >> 16)];
+                for (int sl = 0; sl < wt; ++sl) {
+                    const uint32_t u = ep[(i64)sl * a.nb];
+                    const double g = gs[((u >> 1) & 0x7fu) * kLdG + (u >> 8)];
                     s += (u & 1u) ? -g : g;
                 }
                 acc[i] = s;
             }
         }
+        __syncthreads();  // every thread is done with this tile's ELL block
+        if (rn < a.n_rows) dci_stage_ell(a, els, tn);  // the next item's block, in flight over its GEMM
+        cp_async_commit();
         if (t == a.ntiles - 1) {
             double *yr = a.Y + r * a.nb;
 #pragma unroll
@@ -281,15 +284,19 @@ __global__ void dci_width_kernel(i64 nb, const int32_t *__restrict__ toff, int n
     for (int t = 0; t < ntiles; ++t) atomicMax(wt + t, toff[ib * (ntiles + 1) + t + 1] - toff[ib * (ntiles + 1) + t]);
 }
 
-// tile-major ELL blocks: slot s of string ib in tile t at ell[woff[t] + s nb + ib], padded with `pad`
+// tile-major u16 ELL blocks: slot s of string ib in tile t at ell[woff[t] + s nb + ib], padded with `pad`;
+// ent holds (jb - t NT) << 16 | q << 1 | neg, re-packed as (jb - t NT) << 8 | q << 1 | neg
 __global__ void dci_ell_kernel(i64 nb, const int32_t *__restrict__ toff, const uint32_t *__restrict__ ent, int ntiles,
                                const int32_t *__restrict__ wt, const int64_t *__restrict__ woff, uint32_t pad,
-                               uint32_t *__restrict__ ell) {
+                               uint16_t *__restrict__ ell) {
     const i64 ib = (i64)blockIdx.x * blockDim.x + threadIdx.x;
     if (ib >= nb) return;
     for (int t = 0; t < ntiles; ++t) {
         const int lo = toff[ib * (ntiles + 1) + t], cnt = toff[ib * (ntiles + 1) + t + 1] - lo;
-        for (int sl = 0; sl < wt[t]; ++sl) ell[woff[t] + (i64)sl * nb + ib] = sl < cnt ? ent[lo + sl] : pad;
+        for (int sl = 0; sl < wt[t]; ++sl) {
+            const uint32_t e = sl < cnt ? ent[lo + sl] : pad;
+            ell[woff[t] + (i64)sl * nb + ib] = (uint16_t)(((e >> 16) << 8) | (e & 0xffu));
+        }
     }
 }
 
@@ -362,13 +369,17 @@ int dci_build(sbd_ctx *ctx) {
         SBD_CUDA(ctx, cudaMemcpyAsync(wh.data(), d.wt.p, sizeof(int32_t) * d.ntiles, cudaMemcpyDeviceToHost, ctx->stream));
         SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
         std::vector<int64_t> wo(d.ntiles + 1, 0);
-        for (int t = 0; t < d.ntiles; ++t) wo[t + 1] = wo[t] + (i64)wh[t] * B.n;
+        d.wmax = 0;
+        for (int t = 0; t < d.ntiles; ++t) {  // blocks start 16-byte aligned (cp.async staging)
+            wo[t + 1] = wo[t] + (((i64)wh[t] * B.n + 7) & ~(i64)7);
+            d.wmax = std::max(d.wmax, wh[t]);
+        }
         SBD_CUDA(ctx, d.woff.ensure(sizeof(int64_t) * (d.ntiles + 1)));
         SBD_CUDA(ctx, cudaMemcpy(d.woff.p, wo.data(), sizeof(int64_t) * (d.ntiles + 1), cudaMemcpyHostToDevice));
-        SBD_CUDA(ctx, d.ell.ensure(sizeof(uint32_t) * std::max<i64>(1, wo[d.ntiles])));
+        SBD_CUDA(ctx, d.ell.ensure(sizeof(uint16_t) * std::max<i64>(8, wo[d.ntiles])));
         dci_ell_kernel<<<grid_for(B.n, 128), 128, 0, ctx->stream>>>(B.n, d.toff.as<int32_t>(), d.ent.as<uint32_t>(),
                                                                     d.ntiles, d.wt.as<int32_t>(), d.woff.as<int64_t>(),
-                                                                    (uint32_t)d.nqp << 1, d.ell.as<uint32_t>());
+                                                                    (uint32_t)d.nqp << 1, d.ell.as<uint16_t>());
         SBD_LAUNCHED(ctx, "dci_ell_kernel");
     }
     SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // qm/qp are released on return
@@ -409,7 +420,7 @@ bool sbd_dci_eligible(sbd_ctx *ctx, const double *x_full) {
     if (env && env[0] == '0') return false;
     const int norb = ctx->norb, nq = norb * (norb - 1) / 2;
     const int nqp = std::max(8, (nq + 7) / 8 * 8);
-    if (nqp > 128 || B.n % 2 != 0 || B.n > (i64)kDciThreads * 8 || B.n * (i64)((B.n + 31) / 32 + 1) >= (1ll << 31) ||
+    if (nqp > 120 || B.n % 2 != 0 || B.n > (i64)kDciThreads * 8 || B.n * (i64)((B.n + 31) / 32 + 1) >= (1ll << 31) ||
         B.ns >= (1ll << 31) || (reinterpret_cast<uintptr_t>(x_full) & 15) != 0 || A.ns == 0 || B.ns == 0)
         return false;
     const int na = A.n_elec, nbe = B.n_elec;
@@ -417,11 +428,16 @@ bool sbd_dci_eligible(sbd_ctx *ctx, const double *x_full) {
     const int kp = std::max(4, (na * (norb - na) + 3) & ~3);
     int mfw, ks;
     if (!dci_shape(nqp, kp, &mfw, &ks) || dci_smem(nqp, kp, dci_ld_e(kp)) > kDciSmemMax) return false;
-    if (env && env[0] == '1') return true;
-    // tensor-core FMAs (nqp per beta column) against SELL terms (in-set beta singles per string):
-    // the contraction runs ~14x faster per FMA than the gathered terms (cfg1 measurement)
-    const double cbar_b = (double)B.ns / (double)std::max<i64>(1, B.n);
-    return 8.0 * cbar_b >= (double)nqp;
+    if (!(env && env[0] == '1')) {
+        // tensor-core FMAs (nqp per beta column) against SELL terms (in-set beta singles per string):
+        // the contraction runs ~14x faster per FMA than the gathered terms (cfg1 measurement)
+        const double cbar_b = (double)B.ns / (double)std::max<i64>(1, B.n);
+        if (8.0 * cbar_b < (double)nqp) return false;
+    }
+    // the widest tile's gather block must fit next to E, the slab and G (known once the lists exist)
+    if (dci_build(ctx) != SBD_OK) return false;
+    const DciState &d = ctx->dci;
+    return d.kb_max <= kMaxSingles && dci_smem(nqp, kp, dci_ld_e(kp), (i64)d.wmax * B.n) <= kDciSmemMax;
 }
 
 int sbd_cross_dci(sbd_ctx *ctx, const double *x_full, double *y, bool additive, const SConn *sconn) {
@@ -442,14 +458,16 @@ int sbd_cross_dci(sbd_ctx *ctx, const double *x_full, double *y, bool additive, 
     a.nqp = d.nqp;
     a.kp_max = d.kp_max;
     a.ld_e = d.ld_e;
-    a.ell = d.ell.as<uint32_t>();
+    a.ell = d.ell.as<uint16_t>();
     a.woff = d.woff.as<int64_t>();
     a.wt = d.wt.as<int32_t>();
     a.ntiles = d.ntiles;
+    a.wmax = d.wmax;
     a.add = additive;
-    const size_t smem = dci_smem(d.nqp, d.kp_max, d.ld_e);
+    const size_t smem = dci_smem(d.nqp, d.kp_max, d.ld_e, (i64)d.wmax * B.n);
     int mfw, ks;
-    if (!dci_shape(d.nqp, d.kp_max, &mfw, &ks)) return sbd_fail(ctx, SBD_EINVAL, "direct-CI task 0: shape not served");
+    if (!dci_shape(d.nqp, d.kp_max, &mfw, &ks) || smem > kDciSmemMax)
+        return sbd_fail(ctx, SBD_EINVAL, "direct-CI task 0: shape not served");
     if (ks == 4) {
         if (mfw <= 2) return launch_dci_ppt<2, 4>(ctx, a, smem);
         if (mfw == 3) return launch_dci_ppt<3, 4>(ctx, a, smem);

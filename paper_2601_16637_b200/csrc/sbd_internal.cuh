@@ -108,7 +108,7 @@ struct DistState {
 // direct-CI task 0 (sbd_dci.cu): pair-pair ERI block and the beta singles re-sorted for the gather
 struct DciState {
     bool valid = false;
-    int nq = 0, nqp = 0, kp_max = 0, kb_max = 0, ld_e = 0, nt = 128, ntiles = 0;
+    int nq = 0, nqp = 0, kp_max = 0, kb_max = 0, ld_e = 0, nt = 128, ntiles = 0, wmax = 0;
     DevBuf eq;    // f64 [npair][nqp]
     DevBuf ent;   // u32 [beta singles], per beta string sorted by target
     DevBuf toff;  // int32 [n_beta][ntiles + 1]
@@ -159,6 +159,7 @@ struct sbd_ctx {
     IngestState ingest;
     DistState dist;
     DciState dci;
+    int last_task0 = 0;          // sbd_last_task0
 
     i64 own_lo() const { return row_lo; }
     i64 own_hi() const { return row_hi < 0 ? sec[0].n : row_hi; }

@@ -916,7 +916,10 @@ bool cross_additive(const sbd_ctx *ctx) {
 
 int launch_cross(sbd_ctx *ctx, const double *x_full, double *y, bool additive = false,
                  const SConn *sconn = nullptr) {
-    if (sbd_dci_eligible(ctx, x_full)) return sbd_cross_dci(ctx, x_full, y, additive, sconn);
+    if (sbd_dci_eligible(ctx, x_full)) {
+        ctx->last_task0 = 4;
+        return sbd_cross_dci(ctx, x_full, y, additive, sconn);
+    }
     const Sector &A = ctx->sec[0], &B = ctx->sec[1];
     CrossArgs ca{};
     ca.n_rows = ctx->own_rows();
@@ -960,6 +963,7 @@ int launch_cross(sbd_ctx *ctx, const double *x_full, double *y, bool additive = 
                                sizeof(uint32_t) * (size_t)std::max(ent0, ent1);
         const i64 cpt_mc = (ngl + kCrossThreads / 32 - 2) / (kCrossThreads / 32 - 1);
         if (smem_mc <= kSmemMax && cpt_mc <= 8) {
+            ctx->last_task0 = 1;
             if (cpt_mc <= 2) return launch_cross_mc<2>(ctx, ca, smem_mc);
             if (cpt_mc <= 4) return launch_cross_mc<4>(ctx, ca, smem_mc);
             if (cpt_mc <= 6) return launch_cross_mc<6>(ctx, ca, smem_mc);
@@ -967,8 +971,12 @@ int launch_cross(sbd_ctx *ctx, const double *x_full, double *y, bool additive = 
         }
     }
     const bool staged_ok = !(force && force[0] == '1') && (B.n % 2 == 0) && aligned16(x_full) && cpt <= 14;
-    if (staged_ok && with_ent <= kSmemMax) return launch_cross_tma_cpt<true>(ctx, ca, with_ent, cpt);
-    if (staged_ok && base <= kSmemMax) return launch_cross_tma_cpt<false>(ctx, ca, base, cpt);
+    if (staged_ok && (with_ent <= kSmemMax || base <= kSmemMax)) {
+        ctx->last_task0 = 2;
+        if (with_ent <= kSmemMax) return launch_cross_tma_cpt<true>(ctx, ca, with_ent, cpt);
+        return launch_cross_tma_cpt<false>(ctx, ca, base, cpt);
+    }
+    ctx->last_task0 = 3;
     constexpr int kCpt = 8;
     const i64 gpt = (i64)(kCrossThreadsFlat / 32) * kCpt;
     const i64 tiles = std::max<i64>(1, (ca.gz + gpt - 1) / gpt);
@@ -1270,6 +1278,13 @@ int sbd_sigma_host(sbd_ctx *ctx, const double *x_host, double *y_host) {
     }
     SBD_CUDA(ctx, cudaStreamSynchronize(cs));
     SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SBD_OK;
+}
+
+int sbd_last_task0(sbd_ctx *ctx, int *kind) {
+    SBD_CHECK_CTX(ctx);
+    if (!kind) return sbd_fail(ctx, SBD_EINVAL, "null output");
+    *kind = ctx->last_task0;
     return SBD_OK;
 }
 

@@ -234,8 +234,9 @@ def test_direct_ci_task0_vs_oracle(env, monkeypatch):
 
     for key, val in env.items():
         monkeypatch.setenv(key, val)
-    # (14, 7, 3) and (16, 3, 8) are outside the shapes the kernel serves (49 alpha singles; 15 row fragments):
-    # the forced knob then falls back to the SELL kernels, which must still agree
+    # (14, 7, 3), (16, 3, 8) and the 3000-string beta sectors are outside the shapes the kernel serves (49
+    # alpha singles; 15 row fragments; gather block too wide for shared memory): the forced knob then
+    # falls back to the SELL kernels, which must still agree
     cases = [(12, 6, 6, 924, 924, 1), (12, 5, 6, 500, 862, 2), (13, 4, 5, 300, 1286, 3), (14, 7, 3, 400, 364, 4),
              (16, 3, 8, 200, 3000, 5), (14, 3, 7, 200, 3000, 8), (9, 2, 3, 36, 84, 6), (12, 1, 11, 12, 12, 7),
              (10, 3, 3, 120, 120, 9), (11, 2, 2, 55, 54, 10)]
@@ -250,6 +251,8 @@ def test_direct_ci_task0_vs_oracle(env, monkeypatch):
         app = HamiltonianApplier(basis, table)
         yh = app(x)
         yd = app.sigma_device(torch.from_numpy(x).cuda()).cpu().numpy()
+        if nsb <= 1300 and (norb, na, nb) != (14, 7, 3):  # shapes whose buffers fit must run the DMMA kernel
+            assert app.task0_kernel() == "direct-ci", (norb, na, nb)
         for y in (yh, yd):
             assert np.abs(y - ref).max() <= 1e-10 * np.abs(ref).max(), (norb, na, nb, nsa, nsb)
         assert np.array_equal(app.sigma_device(torch.from_numpy(x).cuda()).cpu().numpy(), yd)  # reproducible
