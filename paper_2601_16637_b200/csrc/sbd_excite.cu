@@ -266,9 +266,7 @@ __global__ void jtable_kernel(const u64 *__restrict__ str, i64 n, i64 npair, con
 
 }  // namespace
 
-// Sliced-ELL layout of the singles for the opposite-spin (task 0) kernel
-// (host side: O(n log n) on tables that are already final; the layout only
-// balances work, it never changes which terms are summed).
+// Sliced-ELL layout of the singles for the opposite-spin (task 0) kernel, built on the device.
 //
 // Strings are sorted by single count (descending, stable) into groups of 32
 // positions.  The target index space [0, n) is cut into H chunks of
@@ -279,15 +277,180 @@ __global__ void jtable_kernel(const u64 *__restrict__ str, i64 n, i64 npair, con
 // i.e. the chunk-local target and the column of the sign-folded ERI row
 // (sbd_context.cu: row (Pa, s_a) = [s_a (Pa|.), -s_a (Pa|.)]).  Unused slots
 // point at local target `chunk`, a zero slot the kernel keeps after the
-// staged chunk, so padding adds exactly 0.0 with no branch.
+// staged chunk, so padding adds exactly 0.0 with no branch.  The layout only
+// balances work and bank conflicts; it never changes which terms are summed.
+namespace {
+
+constexpr int kSellKeyChunks = 7;  // chunk counts in the sort key (after the 11-bit total)
+
+// per string: singles per target chunk, and the sort key (total desc, then chunk counts desc)
+__global__ void sell_count_kernel(i64 n, const int64_t *__restrict__ off, const SConn *__restrict__ sc, i64 H,
+                                  i64 chunk, int32_t *__restrict__ cc, u64 *__restrict__ key) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (i64 h = 0; h < H; ++h) cc[i * H + h] = 0;
+    for (i64 k = off[i]; k < off[i + 1]; ++k) ++cc[i * H + sc[k].tgt / chunk];
+    const i64 tot = min(off[i + 1] - off[i], (i64)2047);
+    u64 kk = (u64)(2047 - tot);
+    const i64 hk = H < kSellKeyChunks ? H : kSellKeyChunks;
+    for (i64 h = 0; h < hk; ++h) kk = (kk << 7) | (u64)(127 - min(cc[i * H + h], 127));
+    key[i] = kk;
+}
+
+// W_{h,g} = widest position of group g in chunk h, as a slot count x 32
+__global__ void sell_width_kernel(i64 n, i64 H, i64 groups, const int32_t *__restrict__ cc,
+                                  const int32_t *__restrict__ order, int64_t *__restrict__ wcount) {
+    const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= H * groups) return;
+    const i64 h = t / groups, g = t % groups;
+    int32_t w = 0;
+    for (i64 l = 0; l < 32 && g * 32 + l < n; ++l) w = max(w, cc[(i64)order[g * 32 + l] * H + h]);
+    wcount[t] = 32 * (int64_t)w;
+}
+
+// goff[h][g] (int32, groups + 1 per chunk) from the flat exclusive scan over (h, g)
+__global__ void sell_goff_kernel(i64 H, i64 groups, const int64_t *__restrict__ flat, int32_t *__restrict__ goff) {
+    const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= H * (groups + 1)) return;
+    const i64 h = t / (groups + 1), g = t % (groups + 1);
+    goff[t] = (int32_t)flat[h * groups + g];
+}
+
+__global__ void sell_col_kernel(i64 n, i64 groups, const int32_t *__restrict__ order, int32_t *__restrict__ col) {
+    const i64 p = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < groups * 32) col[p] = p < n ? order[p] : -1;
+}
+
+// Distinct shared-memory addresses per 64-bit bank of one half-warp slot (<= 16 addresses in all).
+struct BankSet {
+    int64_t addr[16];
+    int n = 0;
+    __device__ int load(int64_t a) const {  // wavefronts of a's bank if a were added
+        int same = 0;
+        bool present = false;
+        for (int i = 0; i < n; ++i)
+            if ((addr[i] & 15) == (a & 15)) {
+                ++same;
+                present |= addr[i] == a;
+            }
+        return same + (present ? 0 : 1);
+    }
+    __device__ void add(int64_t a) {
+        for (int i = 0; i < n; ++i)
+            if (addr[i] == a) return;
+        addr[n++] = a;
+    }
+    __device__ int maxload() const {
+        int m = 0;
+        for (int i = 0; i < n; ++i) {
+            int c = 0;
+            for (int j = 0; j < n; ++j) c += (addr[j] & 15) == (addr[i] & 15) && (j == i || addr[j] != addr[i]);
+            m = max(m, c);
+        }
+        return m;
+    }
+};
+
+constexpr int kSellGreedyMax = 32;  // widest slot count the greedy assignment handles (wider: enumeration order)
+
+// One thread per (group, chunk).  A position's singles may sit in its slots in any order (the sum
+// is the same up to rounding), so each slot's 32 entries can be chosen to spread the two
+// shared-memory gathers of the task-0 inner loop -- x[jl] and the ERI row at (chunk + 2 + q) --
+// over the 16 64-bit banks of each half-warp.  Cost model: per half-warp and slot, a gather takes
+// as many wavefronts as the most-loaded bank has DISTINCT addresses (equal addresses broadcast).
+// The table keeps the better of the enumeration order and a greedy assignment (per lane, the
+// remaining entry that adds the fewest wavefronts).
+__global__ void sell_fill_kernel(i64 n, i64 H, i64 groups, i64 chunk, int pbits, i64 ldv,
+                                 const int64_t *__restrict__ off, const SConn *__restrict__ sc,
+                                 const int32_t *__restrict__ order, const int32_t *__restrict__ goff,
+                                 uint32_t *__restrict__ ent) {
+    const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= H * groups) return;
+    const i64 g = t / H, h = t % H;
+    const i64 base = goff[h * (groups + 1) + g];
+    const i64 w = (goff[h * (groups + 1) + g + 1] - base) / 32;
+    if (w == 0) return;
+    const uint32_t null_ent = (uint32_t)chunk << pbits, qmask = (1u << pbits) - 1u;
+    auto entry = [&](int l, i64 q) -> uint32_t {  // q-th single of position l inside chunk h (enumeration order)
+        const i64 p = g * 32 + l;
+        if (p >= n) return null_ent;
+        const int32_t c = order[p];
+        i64 seen = 0;
+        for (i64 k = off[c]; k < off[c + 1]; ++k) {
+            if (sc[k].tgt / chunk != h) continue;
+            if (seen++ == q) {
+                const i64 jl = sc[k].tgt - h * chunk;
+                const i64 P = abs(sc[k].info) - 1, neg = sc[k].info < 0;
+                return ((uint32_t)jl << pbits) | (uint32_t)(P + neg * ldv);
+            }
+        }
+        return null_ent;
+    };
+    auto xaddr = [&](uint32_t e) { return (int64_t)(e >> pbits); };
+    auto vaddr = [&](uint32_t e) { return (int64_t)(chunk + 2 + (e & qmask)); };
+    // enumeration order and its cost
+    int cost_nat = 0;
+    for (i64 q = 0; q < w; ++q)
+        for (int half = 0; half < 2; ++half) {
+            BankSet bx, bv;
+            for (int l = 16 * half; l < 16 * half + 16; ++l) {
+                const uint32_t e = entry(l, q);
+                if (e == null_ent) continue;
+                bx.add(xaddr(e));
+                bv.add(vaddr(e));
+            }
+            cost_nat += bx.maxload() + bv.maxload();
+        }
+    bool greedy = false;
+    if (w <= kSellGreedyMax) {
+        // greedy assignment, written straight into the table; kept if cheaper
+        uint32_t rem[16][kSellGreedyMax];
+        int nrem[16];
+        int cost_gr = 0;
+        for (int half = 0; half < 2; ++half) {
+            for (int l = 0; l < 16; ++l) {
+                nrem[l] = 0;
+                for (i64 q = 0; q < w; ++q) {
+                    const uint32_t e = entry(16 * half + l, q);
+                    if (e != null_ent) rem[l][nrem[l]++] = e;
+                }
+            }
+            for (i64 q = 0; q < w; ++q) {
+                BankSet bx, bv;
+                for (int l = 0; l < 16; ++l) {
+                    uint32_t e = null_ent;
+                    if (nrem[l] > 0) {
+                        int best = 0, best_cost = 1 << 30;
+                        for (int k = 0; k < nrem[l]; ++k) {
+                            const int lx = bx.load(xaddr(rem[l][k])), lv = bv.load(vaddr(rem[l][k]));
+                            const int cost = 4 * max(lx, lv) + lx + lv;
+                            if (cost < best_cost) {
+                                best_cost = cost;
+                                best = k;
+                            }
+                        }
+                        e = rem[l][best];
+                        rem[l][best] = rem[l][--nrem[l]];
+                        bx.add(xaddr(e));
+                        bv.add(vaddr(e));
+                    }
+                    ent[base + 32 * q + 16 * half + l] = e;
+                }
+                cost_gr += bx.maxload() + bv.maxload();
+            }
+        }
+        greedy = cost_gr < cost_nat;
+    }
+    if (!greedy)
+        for (i64 q = 0; q < w; ++q)
+            for (int l = 0; l < 32; ++l) ent[base + 32 * q + l] = entry(l, q);
+}
+
+}  // namespace
+
 static int build_sell(sbd_ctx *ctx, Sector &s) {
     const i64 n = s.n;
     cudaStream_t st = ctx->stream;
-    std::vector<int64_t> off(n + 1);
-    std::vector<SConn> sc(s.ns + 1);
-    SBD_CUDA(ctx, cudaMemcpyAsync(off.data(), s.s_off.p, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
-    if (s.ns) SBD_CUDA(ctx, cudaMemcpyAsync(sc.data(), s.sconn.p, sizeof(SConn) * s.ns, cudaMemcpyDeviceToHost, st));
-    SBD_CUDA(ctx, cudaStreamSynchronize(st));
     const i64 H = n <= kSellWhole ? 1 : (n + kSellChunk - 1) / kSellChunk;
     const i64 chunk = std::max<i64>(2, ((n + H - 1) / H + 1) & ~(i64)1);  // even: 16-byte TMA rows
     int pbits = 1;
@@ -295,146 +458,49 @@ static int build_sell(sbd_ctx *ctx, Sector &s) {
     int cbits = 1;
     while (((i64)1 << cbits) <= chunk) ++cbits;
     if (pbits + cbits > 32) return sbd_fail(ctx, SBD_EINVAL, "sector too large for the packed single-excitation table");
-    // per-string, per-chunk counts; sort by (total, count in chunk 0, 1, ...)
-    // descending, so the 32 positions of a group have (nearly) equal counts in
-    // every chunk and padding stays small
-    std::vector<int32_t> cc((size_t)n * H, 0);
-    for (i64 i = 0; i < n; ++i)
-        for (i64 k = off[i]; k < off[i + 1]; ++k) ++cc[(size_t)i * H + sc[k].tgt / chunk];
-    std::vector<int32_t> order(n);
-    for (i64 i = 0; i < n; ++i) order[i] = (int32_t)i;
-    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-        const i64 ta = off[a + 1] - off[a], tb = off[b + 1] - off[b];
-        if (ta != tb) return ta > tb;
-        for (i64 h = 0; h < H; ++h)
-            if (cc[(size_t)a * H + h] != cc[(size_t)b * H + h]) return cc[(size_t)a * H + h] > cc[(size_t)b * H + h];
-        return false;
-    });
     const i64 groups = (n + 31) / 32;
-    std::vector<int64_t> goff((size_t)H * (groups + 1), 0);
-    i64 total = 0;
-    for (i64 h = 0; h < H; ++h) {
-        for (i64 g = 0; g < groups; ++g) {
-            i64 w = 0;
-            for (i64 l = 0; l < 32 && g * 32 + l < n; ++l) w = std::max<i64>(w, cc[(size_t)order[g * 32 + l] * H + h]);
-            goff[h * (groups + 1) + g] = total;
-            total += 32 * w;
-        }
-        goff[h * (groups + 1) + groups] = total;
-    }
+    DevBuf cc, key, skey, order, wcount, flat;
+    SBD_CUDA(ctx, cc.ensure(sizeof(int32_t) * std::max<i64>(1, n * H)));
+    SBD_CUDA(ctx, key.ensure(sizeof(u64) * std::max<i64>(1, n)));
+    sell_count_kernel<<<grid_for(n, 128), 128, 0, st>>>(n, s.s_off.as<int64_t>(), s.sconn.as<SConn>(), H, chunk,
+                                                        cc.as<int32_t>(), key.as<u64>());
+    SBD_LAUNCHED(ctx, "sell counts");
+    // stable sort by (total, per-chunk counts) descending: padding stays small in every chunk
+    int rc = sbd_radix_sort(ctx, key.as<u64>(), n, 11 + 7 * (int)std::min<i64>(H, kSellKeyChunks), skey, order);
+    if (rc) return rc;
+    SBD_CUDA(ctx, wcount.ensure(sizeof(int64_t) * std::max<i64>(1, H * groups)));
+    SBD_CUDA(ctx, flat.ensure(sizeof(int64_t) * (H * groups + 1)));
+    sell_width_kernel<<<grid_for(H * groups, 128), 128, 0, st>>>(n, H, groups, cc.as<int32_t>(), order.as<int32_t>(),
+                                                                 wcount.as<int64_t>());
+    offsets_from_counts<<<1, 1024, 0, st>>>(wcount.as<int64_t>(), flat.as<int64_t>(), H * groups);
+    SBD_LAUNCHED(ctx, "sell widths");
+    int64_t total = 0;
+    SBD_CUDA(ctx, cudaMemcpyAsync(&total, flat.as<int64_t>() + H * groups, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SBD_CUDA(ctx, cudaStreamSynchronize(st));
     if (total >= (int64_t)INT32_MAX) return sbd_fail(ctx, SBD_EINVAL, "singles table too large");
-    const uint32_t null_ent = (uint32_t)chunk << pbits;
-    std::vector<uint32_t> ent((size_t)total + 4, null_ent);
-    std::vector<int32_t> col((size_t)groups * 32 + 1, -1), go((size_t)H * (groups + 1));
-    // Slot assignment.  A position's singles may sit in its slots in any order (the
-    // sum is the same up to rounding), so each slot's 32 entries can be chosen to
-    // spread the two shared-memory gathers of the task-0 inner loop -- x[jl] and
-    // the ERI row at (chunk + 2 + q) -- over the 16 64-bit banks of each half-warp.
-    // Cost model: per half-warp and slot, a gather takes as many wavefronts as the
-    // most-loaded bank has DISTINCT addresses (equal addresses broadcast).  Per
-    // (group, chunk) the table keeps the better of the enumeration order (often
-    // well spread and broadcast-friendly for structured string sets) and a greedy
-    // assignment (per lane, the remaining entry that adds the fewest wavefronts).
-    for (i64 p = 0; p < n; ++p) col[p] = order[p];
-    const uint32_t qmask = (1u << pbits) - 1u;
-    auto xaddr = [&](uint32_t e) { return (i64)(e >> pbits); };
-    auto vaddr = [&](uint32_t e) { return chunk + 2 + (i64)(e & qmask); };
-    struct BankSet {  // distinct addresses per 64-bit bank
-        std::vector<i64> a[16];
-        int load(i64 addr) const {
-            const auto &v = a[addr & 15];
-            return (int)v.size() + (std::find(v.begin(), v.end(), addr) == v.end() ? 1 : 0);
-        }
-        void add(i64 addr) {
-            auto &v = a[addr & 15];
-            if (std::find(v.begin(), v.end(), addr) == v.end()) v.push_back(addr);
-        }
-        int maxload() const {
-            size_t m = 0;
-            for (const auto &v : a) m = std::max(m, v.size());
-            return (int)m;
-        }
-    };
-    std::vector<std::vector<uint32_t>> rem(32), nat(32);
-    std::vector<uint32_t> slots;
-    for (i64 g = 0; g < groups; ++g) {
-        for (i64 h = 0; h < H; ++h) {
-            const i64 base = goff[h * (groups + 1) + g];
-            const i64 w = (goff[h * (groups + 1) + g + 1] - base) / 32;
-            if (w == 0) continue;
-            for (int l = 0; l < 32; ++l) {
-                nat[l].clear();
-                const i64 p = g * 32 + l;
-                if (p >= n) continue;
-                const int32_t c = order[p];
-                for (i64 k = off[c]; k < off[c + 1]; ++k) {
-                    if (sc[k].tgt / chunk != h) continue;
-                    const i64 jl = sc[k].tgt - h * chunk;
-                    const i64 P = std::abs(sc[k].info) - 1, neg = sc[k].info < 0;
-                    nat[l].push_back(((uint32_t)jl << pbits) | (uint32_t)(P + neg * ctx->ld_vpp));
-                }
-            }
-            // enumeration order and its cost
-            slots.assign((size_t)32 * w, null_ent);
-            int cost_nat = 0;
-            for (i64 q = 0; q < w; ++q)
-                for (int half = 0; half < 2; ++half) {
-                    BankSet bx, bv;
-                    for (int l = 16 * half; l < 16 * half + 16; ++l)
-                        if (q < (i64)nat[l].size()) {
-                            bx.add(xaddr(nat[l][q]));
-                            bv.add(vaddr(nat[l][q]));
-                        }
-                    cost_nat += bx.maxload() + bv.maxload();
-                }
-            // greedy
-            for (int l = 0; l < 32; ++l) rem[l] = nat[l];
-            int cost_gr = 0;
-            for (i64 q = 0; q < w; ++q)
-                for (int half = 0; half < 2; ++half) {
-                    BankSet bx, bv;
-                    for (int l = 16 * half; l < 16 * half + 16; ++l) {
-                        auto &r = rem[l];
-                        if (r.empty()) continue;
-                        size_t best = 0;
-                        int best_cost = 1 << 30;
-                        for (size_t t = 0; t < r.size(); ++t) {
-                            const int lx = bx.load(xaddr(r[t])), lv = bv.load(vaddr(r[t]));
-                            const int cost = 4 * std::max(lx, lv) + lx + lv;
-                            if (cost < best_cost) {
-                                best_cost = cost;
-                                best = t;
-                            }
-                        }
-                        const uint32_t e = r[best];
-                        r[best] = r.back();
-                        r.pop_back();
-                        bx.add(xaddr(e));
-                        bv.add(vaddr(e));
-                        slots[(size_t)32 * q + l] = e;
-                    }
-                    cost_gr += bx.maxload() + bv.maxload();
-                }
-            const bool use_greedy = cost_gr < cost_nat;
-            for (i64 q = 0; q < w; ++q)
-                for (int l = 0; l < 32; ++l)
-                    ent[base + 32 * q + l] = use_greedy ? slots[(size_t)32 * q + l]
-                                                        : (q < (i64)nat[l].size() ? nat[l][q] : null_ent);
-        }
-    }
-    for (size_t i = 0; i < go.size(); ++i) go[i] = (int32_t)goff[i];
+    SBD_CUDA(ctx, s.sell_ent.ensure(sizeof(uint32_t) * (total + 4)));
+    SBD_CUDA(ctx, s.sell_goff.ensure(sizeof(int32_t) * H * (groups + 1)));
+    SBD_CUDA(ctx, s.sell_col.ensure(sizeof(int32_t) * (groups * 32 + 1)));
+    sell_goff_kernel<<<grid_for(H * (groups + 1), 128), 128, 0, st>>>(H, groups, flat.as<int64_t>(),
+                                                                     s.sell_goff.as<int32_t>());
+    sell_col_kernel<<<grid_for(groups * 32, 128), 128, 0, st>>>(n, groups, order.as<int32_t>(), s.sell_col.as<int32_t>());
+    sell_fill_kernel<<<grid_for(H * groups, 64), 64, 0, st>>>(n, H, groups, chunk, pbits, ctx->ld_vpp,
+                                                               s.s_off.as<int64_t>(), s.sconn.as<SConn>(),
+                                                               order.as<int32_t>(), s.sell_goff.as<int32_t>(),
+                                                               s.sell_ent.as<uint32_t>());
+    SBD_LAUNCHED(ctx, "sell fill");
+    const uint32_t pad[4] = {(uint32_t)chunk << pbits, (uint32_t)chunk << pbits, (uint32_t)chunk << pbits,
+                             (uint32_t)chunk << pbits};
+    SBD_CUDA(ctx, cudaMemcpyAsync(s.sell_ent.as<uint32_t>() + total, pad, sizeof(pad), cudaMemcpyHostToDevice, st));
+    s.sell_goff_host.resize((size_t)(H * (groups + 1)));
+    SBD_CUDA(ctx, cudaMemcpyAsync(s.sell_goff_host.data(), s.sell_goff.p, sizeof(int32_t) * s.sell_goff_host.size(),
+                                  cudaMemcpyDeviceToHost, st));
+    SBD_CUDA(ctx, cudaStreamSynchronize(st));
     s.sell_groups = groups;
-    s.sell_goff_host = go;
     s.sell_nent = total;
     s.sell_h = H;
     s.sell_chunk = chunk;
     s.sell_pbits = pbits;
-    SBD_CUDA(ctx, s.sell_ent.ensure(sizeof(uint32_t) * ent.size()));
-    SBD_CUDA(ctx, s.sell_goff.ensure(sizeof(int32_t) * go.size()));
-    SBD_CUDA(ctx, s.sell_col.ensure(sizeof(int32_t) * col.size()));
-    SBD_CUDA(ctx, cudaMemcpy(s.sell_ent.p, ent.data(), sizeof(uint32_t) * ent.size(), cudaMemcpyHostToDevice));
-    SBD_CUDA(ctx, cudaMemcpy(s.sell_goff.p, go.data(), sizeof(int32_t) * go.size(), cudaMemcpyHostToDevice));
-    SBD_CUDA(ctx, cudaMemcpy(s.sell_col.p, col.data(), sizeof(int32_t) * col.size(), cudaMemcpyHostToDevice));
     return SBD_OK;
 }
 

@@ -18,7 +18,6 @@
 // short binary search inside one group, and the row's sum is a fixed-order
 // warp reduction (deterministic, no atomics).
 #include <algorithm>
-#include <unordered_map>
 
 #include "sbd_internal.cuh"
 
@@ -220,35 +219,31 @@ int sbd_set_dets(sbd_ctx *ctx, const uint64_t *alpha, const uint64_t *beta, int6
     SBD_CHECK_CTX(ctx);
     if (n < 0 || (n > 0 && (!alpha || !beta))) return sbd_fail(ctx, SBD_EINVAL, "bad determinant list");
     if (n >= (int64_t)INT32_MAX) return sbd_fail(ctx, SBD_EINVAL, "too many determinants");
-    // unique strings per spin in first-seen order; dets become index pairs
-    std::vector<u64> ua, ub;
-    std::unordered_map<u64, int32_t> ia, ib;
-    ia.reserve((size_t)n * 2 + 1);
-    ib.reserve((size_t)n * 2 + 1);
-    std::vector<int32_t> A((size_t)n), B((size_t)n);
-    for (int64_t i = 0; i < n; ++i) {
-        auto fa = ia.emplace(alpha[i], (int32_t)ua.size());
-        if (fa.second) ua.push_back(alpha[i]);
-        A[i] = fa.first->second;
-        auto fb = ib.emplace(beta[i], (int32_t)ub.size());
-        if (fb.second) ub.push_back(beta[i]);
-        B[i] = fb.first->second;
+    // unique strings per spin in first-seen order and dets as index pairs, on the device
+    // (stable radix sort, run heads, runs re-sorted by first occurrence)
+    if (!ctx->have_integrals) return sbd_fail(ctx, SBD_EINVAL, "set integrals before strings");
+    SBD_CUDA(ctx, ctx->det_a.ensure(sizeof(int32_t) * (n + 1)));
+    SBD_CUDA(ctx, ctx->det_b.ensure(sizeof(int32_t) * (n + 1)));
+    std::vector<u64> uniq[2];
+    for (int spin = 0; spin < 2; ++spin) {
+        const uint64_t *src = spin ? beta : alpha;
+        DevBuf keys, u;
+        i64 nu = 0;
+        SBD_CUDA(ctx, keys.ensure(sizeof(u64) * (n + 1)));
+        if (n) SBD_CUDA(ctx, cudaMemcpy(keys.p, src, sizeof(u64) * n, cudaMemcpyHostToDevice));
+        int rc = sbd_unique_first_seen_index(ctx, keys.as<u64>(), n, ctx->norb, u, &nu,
+                                             spin ? ctx->det_b.as<int32_t>() : ctx->det_a.as<int32_t>());
+        if (rc) return rc;
+        uniq[spin].resize((size_t)nu);
+        if (nu) SBD_CUDA(ctx, cudaMemcpy(uniq[spin].data(), u.p, sizeof(u64) * nu, cudaMemcpyDeviceToHost));
     }
-    int rc = sbd_set_strings(ctx, 0, ua.data(), (int64_t)ua.size(), n_alpha_elec);
+    int rc = sbd_set_strings(ctx, 0, uniq[0].data(), (int64_t)uniq[0].size(), n_alpha_elec);
     if (rc) return rc;
-    rc = sbd_set_strings(ctx, 1, ub.data(), (int64_t)ub.size(), n_beta_elec);
+    rc = sbd_set_strings(ctx, 1, uniq[1].data(), (int64_t)uniq[1].size(), n_beta_elec);
     if (rc) return rc;
     ctx->explicit_mode = true;
     ctx->explicit_built = false;
     ctx->n_det = n;
-    ctx->det_a_host = std::move(A);
-    ctx->det_b_host = std::move(B);
-    SBD_CUDA(ctx, ctx->det_a.ensure(sizeof(int32_t) * (n + 1)));
-    SBD_CUDA(ctx, ctx->det_b.ensure(sizeof(int32_t) * (n + 1)));
-    if (n) {
-        SBD_CUDA(ctx, cudaMemcpy(ctx->det_a.p, ctx->det_a_host.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
-        SBD_CUDA(ctx, cudaMemcpy(ctx->det_b.p, ctx->det_b_host.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
-    }
     ctx->diag_valid = false;
     return SBD_OK;
 }

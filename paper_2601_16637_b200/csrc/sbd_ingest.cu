@@ -192,7 +192,56 @@ int unique_first_seen(sbd_ctx *ctx, const u64 *sorted1, const u64 *sorted2, cons
     return SBD_OK;
 }
 
+__global__ void rank_of_run(const int32_t *__restrict__ order_by_first, i64 nruns, int32_t *__restrict__ rank) {
+    const i64 u = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < nruns) rank[order_by_first[u]] = (int32_t)u;
+}
+
+// rid is the EXCLUSIVE scan of the head flags: the run of slot i is rid[i] + head[i] - 1
+__global__ void index_of_sample(const int32_t *__restrict__ order, const int32_t *__restrict__ rid,
+                                const int32_t *__restrict__ head, const int32_t *__restrict__ rank, i64 n,
+                                int32_t *__restrict__ index) {
+    const i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) index[order[i]] = rank[rid[i] + head[i] - 1];
+}
+
 }  // namespace
+
+// Unique values of keys[0..n) in first-seen order (uniq, *nuniq) and, per element, the position of its
+// value in that list (index, device int32[n]) -- the explicit basis's string dedupe (sbd_set_dets).
+int sbd_unique_first_seen_index(sbd_ctx *ctx, const u64 *keys, i64 n, int key_bits, DevBuf &uniq, i64 *nuniq,
+                                int32_t *index) {
+    cudaStream_t st = ctx->stream;
+    *nuniq = 0;
+    if (n == 0) return SBD_OK;
+    DevBuf sorted, perm, head, rid, first, start, sfirst, operm, rank;
+    int rc = sbd_radix_sort(ctx, keys, n, key_bits, sorted, perm);
+    if (rc) return rc;
+    SBD_CUDA(ctx, head.ensure(sizeof(int32_t) * (n + 1)));
+    SBD_CUDA(ctx, rid.ensure(sizeof(int32_t) * (n + 1)));
+    heads_kernel<<<grid_for(n, 256), 256, 0, st>>>(sorted.as<u64>(), nullptr, n, head.as<int32_t>());
+    int64_t nr = 0;
+    rc = scan_i32(ctx, head.as<int32_t>(), n, rid.as<int32_t>(), &nr);
+    if (rc) return rc;
+    SBD_CUDA(ctx, first.ensure(sizeof(u64) * (nr + 1)));
+    SBD_CUDA(ctx, start.ensure(sizeof(int32_t) * (nr + 1)));
+    runs_kernel<<<grid_for(n, 256), 256, 0, st>>>(head.as<int32_t>(), rid.as<int32_t>(), perm.as<int32_t>(), n, nr,
+                                                  first.as<u64>(), start.as<int32_t>());
+    SBD_LAUNCHED(ctx, "runs");
+    rc = sbd_radix_sort(ctx, first.as<u64>(), nr, bits_for((u64)n), sfirst, operm);
+    if (rc) return rc;
+    SBD_CUDA(ctx, uniq.ensure(sizeof(u64) * (nr + 1)));
+    SBD_CUDA(ctx, rank.ensure(sizeof(int32_t) * (nr + 1)));
+    run_values<<<grid_for(nr, 256), 256, 0, st>>>(start.as<int32_t>(), operm.as<int32_t>(), nr, sorted.as<u64>(),
+                                                  nullptr, uniq.as<u64>(), nullptr, nullptr);
+    rank_of_run<<<grid_for(nr, 256), 256, 0, st>>>(operm.as<int32_t>(), nr, rank.as<int32_t>());
+    index_of_sample<<<grid_for(n, 256), 256, 0, st>>>(perm.as<int32_t>(), rid.as<int32_t>(), head.as<int32_t>(),
+                                                      rank.as<int32_t>(), n, index);
+    SBD_LAUNCHED(ctx, "first-seen index");
+    SBD_CUDA(ctx, cudaStreamSynchronize(st));
+    *nuniq = nr;
+    return SBD_OK;
+}
 
 extern "C" {
 

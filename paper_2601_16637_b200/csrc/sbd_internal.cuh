@@ -151,7 +151,6 @@ struct sbd_ctx {
     // indices; sec[0]/sec[1] hold the unique alpha/beta strings (first-seen order)
     bool explicit_mode = false;
     i64 n_det = 0;
-    std::vector<int32_t> det_a_host, det_b_host;
     DevBuf det_a, det_b;         // int32[n_det], caller order
     DevBuf grp_off;              // int32[n_alpha + 1]: dets sorted by (A, B), group of alpha A
     DevBuf grp_b, grp_perm;      // int32[n_det]: sorted B and caller index
@@ -210,6 +209,9 @@ int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other);  // sb
 // LSD radix sort of n u64 keys (low key_bits significant) with the sort permutation (sbd_strings.cu)
 int sbd_radix_sort(sbd_ctx *ctx, const u64 *keys, i64 n, int key_bits, DevBuf &sorted, DevBuf &perm);
 int sbd_build_explicit_index(sbd_ctx *ctx);                 // sbd_explicit.cu
+// unique keys in first-seen order + per-element position in that list (sbd_ingest.cu)
+int sbd_unique_first_seen_index(sbd_ctx *ctx, const u64 *keys, i64 n, int key_bits, DevBuf &uniq, i64 *nuniq,
+                                int32_t *index);
 int sbd_explicit_diag(sbd_ctx *ctx, double *out);           // sbd_explicit.cu
 int sbd_explicit_sigma(sbd_ctx *ctx, const double *x, double *y);  // sbd_explicit.cu
 // sigma building blocks used by the partitioned sigma (sbd_sigma.cu)
