@@ -86,6 +86,7 @@ int sbd_destroy(sbd_ctx *ctx) {
     }
     for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
     sbd_dist_release(ctx);
+    sbd_samespin_gemm_release(ctx);
     delete ctx;
     return SBD_OK;
 }
@@ -222,6 +223,7 @@ int sbd_build_tables(sbd_ctx *ctx) {
     }
     ctx->diag_valid = false;
     ctx->dci.valid = false;
+    ctx->ssg_valid = false;
     ctx->dist.planned = false;  // the exchange plan is built from the alpha table
     SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SBD_OK;

@@ -65,6 +65,9 @@ struct Sector {
     DevBuf sell_col;         // int32[groups*32]: string at each position (-1: padding)
     i64 sell_groups = 0, sell_nent = 0, sell_h = 1, sell_chunk = 0;
     std::vector<int32_t> sell_goff_host;  // host copy of sell_goff
+    // dense-set mode (sbd_samespin_gemm.cu): spectator-independent coefficients as a dense n x n
+    // matrix, and the singles (offsets s_off) with c = 0 for the spectator-dependent J term
+    DevBuf dense, conn_j;
     int sell_pbits = 1;
     bool built = false;
 };
@@ -159,6 +162,11 @@ struct sbd_ctx {
     DistState dist;
     DciState dci;
     int last_task0 = 0;          // sbd_last_task0
+    bool ssg_valid = false;      // same-spin dense matrices built (sbd_samespin_gemm.cu)
+    void *cublas = nullptr;      // cublasHandle_t, created on first dense-set sigma
+    cudaStream_t aux_stream = nullptr;    // dense-set DGEMMs, concurrent with the streams
+    cudaEvent_t aux_ev[2] = {nullptr, nullptr};
+    DevBuf ssg_z;                         // their result, added after the alpha side
 
     i64 own_lo() const { return row_lo; }
     i64 own_hi() const { return row_hi < 0 ? sec[0].n : row_hi; }
@@ -222,6 +230,13 @@ int sbd_beta_side(sbd_ctx *ctx, const double *x_own);      // transpose + beta s
 int sbd_alpha_pass(sbd_ctx *ctx, const double *X, double *y, const Conn *conn, const int64_t *seg_off, i64 stride,
                    int s_lo, int s_hi, i64 xo_row0, bool epi, bool acc_in);
 int sbd_cross_add(sbd_ctx *ctx, const double *X, double *y, const SConn *sconn);  // y += task 0
+// same-spin parts as cuBLAS DGEMMs for dense string sets (sbd_samespin_gemm.cu)
+bool sbd_samespin_gemm_on(const sbd_ctx *ctx);
+int sbd_samespin_gemm_prepare(sbd_ctx *ctx);
+int sbd_samespin_gemm_start(sbd_ctx *ctx, const double *x_full);
+int sbd_samespin_gemm_mark(sbd_ctx *ctx);
+int sbd_samespin_gemm_finish(sbd_ctx *ctx, double *y);
+void sbd_samespin_gemm_release(sbd_ctx *ctx);
 // direct-CI task 0 on the fp64 tensor cores (sbd_dci.cu): dense string sets
 bool sbd_dci_eligible(sbd_ctx *ctx, const double *x_full);
 int sbd_cross_dci(sbd_ctx *ctx, const double *x_full, double *y, bool additive, const SConn *sconn);

@@ -987,6 +987,13 @@ int launch_cross(sbd_ctx *ctx, const double *x_full, double *y, bool additive = 
     return SBD_OK;
 }
 
+// Dense string sets: the same-spin streams carry only the singles' spectator-dependent term and
+// the rest is added by two DGEMMs after the alpha side (sbd_samespin_gemm.cu).  Prepared lazily.
+int dense_mode(sbd_ctx *ctx, bool *on) {
+    *on = sbd_samespin_gemm_on(ctx);
+    return *on ? sbd_samespin_gemm_prepare(ctx) : SBD_OK;
+}
+
 // Beta side for own alpha rows [r0, r1) (local): transpose those rows of x into
 // X^T columns, then stream Y^T's column tiles covering them.  r0 is a
 // multiple of kTW unless the whole range is launched.
@@ -1007,8 +1014,10 @@ int launch_beta_side(sbd_ctx *ctx, const double *x_own, i64 r0, i64 r1) {
     a.ldx = ctx->ld_t;
     a.Y = ctx->yt.as<double>();
     a.ldy = ctx->ld_t;
-    a.conn_off = B.conn_off.as<int64_t>();
-    a.conn = B.conn.as<Conn>();
+    bool dense = false;
+    if (int rc = dense_mode(ctx, &dense)) return rc;
+    a.conn_off = dense ? B.s_off.as<int64_t>() : B.conn_off.as<int64_t>();
+    a.conn = dense ? B.conn_j.as<Conn>() : B.conn.as<Conn>();
     a.J = A.J.as<double>();
     a.ldj = A.n;
     if (use_side_tma() && aligned16(a.X) && a.ldx % 2 == 0) {
@@ -1043,8 +1052,10 @@ int launch_alpha_side(sbd_ctx *ctx, const double *x_full, double *y, i64 r0, i64
     a.ldx = nb;
     a.Y = y + r0 * nb;
     a.ldy = nb;
-    a.conn_off = A.conn_off.as<int64_t>();
-    a.conn = A.conn.as<Conn>();
+    bool dense = false;
+    if (int rc = dense_mode(ctx, &dense)) return rc;
+    a.conn_off = dense ? A.s_off.as<int64_t>() : A.conn_off.as<int64_t>();
+    a.conn = dense ? A.conn_j.as<Conn>() : A.conn.as<Conn>();
     a.J = B.J.as<double>();
     a.ldj = nb;
     a.ytb = ctx->yt_blocked;  // the layout the beta side wrote
@@ -1124,6 +1135,30 @@ int ensure_events(sbd_ctx *ctx, size_t n) {
 
 }  // namespace
 
+// Dense string sets (sbd_samespin_gemm.cu): the auxiliary stream runs the two same-spin DGEMMs and
+// then the beta stream (transpose + singles' J term) while the main stream runs task 0 (the longest
+// kernel there); the alpha stream waits for both, and the DGEMMs' result is added last.
+static int sigma_dense(sbd_ctx *ctx, const double *x_full, double *y) {
+    int rc = require_product(ctx);
+    if (rc) return rc;
+    if ((rc = ensure_scratch(ctx)) || (rc = ensure_diag(ctx)) || (rc = sbd_samespin_gemm_prepare(ctx))) return rc;
+    const Sector &A = ctx->sec[0], &B = ctx->sec[1];
+    if (ctx->own_rows() == 0 || B.n == 0) return SBD_OK;
+    if ((rc = sbd_samespin_gemm_start(ctx, x_full))) return rc;
+    cudaStream_t main = ctx->stream;
+    ctx->stream = ctx->aux_stream;  // the beta stream after the DGEMMs, on the auxiliary stream
+    rc = launch_beta_side(ctx, x_full + ctx->own_lo() * B.n, 0, ctx->own_rows());
+    ctx->stream = main;
+    if (rc) return rc;
+    if ((rc = sbd_samespin_gemm_mark(ctx))) return rc;
+    const bool additive = A.ns > 0 && B.ns > 0 && cross_additive(ctx);
+    if (A.ns > 0 && B.ns > 0 && !additive && (rc = launch_cross(ctx, x_full, y))) return rc;
+    SBD_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));  // Y^T (and Z) ready
+    if ((rc = launch_alpha_side(ctx, x_full, y, 0, ctx->own_rows(), !additive))) return rc;
+    if (additive && (rc = launch_cross(ctx, x_full, y, true))) return rc;
+    return sbd_samespin_gemm_finish(ctx, y);
+}
+
 int sbd_require_sigma_ready(sbd_ctx *ctx) {
     int rc = require_ready(ctx);
     if (rc) return rc;
@@ -1182,16 +1217,25 @@ int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full, double *y) {
     if (rc) return rc;
     const Sector &A = ctx->sec[0], &B = ctx->sec[1];
     if (ctx->own_rows() == 0 || B.n == 0) return SBD_OK;
+    const bool dense = sbd_samespin_gemm_on(ctx);
+    if (dense) {  // the dense same-spin products run beside task 0 and the alpha stream
+        if ((rc = sbd_samespin_gemm_prepare(ctx))) return rc;
+        if ((rc = sbd_samespin_gemm_start(ctx, x_full))) return rc;
+        if ((rc = sbd_samespin_gemm_mark(ctx))) return rc;
+    }
     if (A.ns > 0 && B.ns > 0 && cross_additive(ctx)) {  // sparse singles: task 0 added afterwards
         rc = launch_alpha_side(ctx, x_full, y, 0, ctx->own_rows(), false);
         if (rc) return rc;
-        return launch_cross(ctx, x_full, y, true);
+        rc = launch_cross(ctx, x_full, y, true);
+    } else {
+        if (A.ns > 0 && B.ns > 0) {  // task 0 exists only when both sectors have in-set singles
+            rc = launch_cross(ctx, x_full, y);
+            if (rc) return rc;
+        }
+        rc = launch_alpha_side(ctx, x_full, y, 0, ctx->own_rows());
     }
-    if (A.ns > 0 && B.ns > 0) {  // task 0 exists only when both sectors have in-set singles
-        rc = launch_cross(ctx, x_full, y);
-        if (rc) return rc;
-    }
-    return launch_alpha_side(ctx, x_full, y, 0, ctx->own_rows());
+    if (rc) return rc;
+    return dense ? sbd_samespin_gemm_finish(ctx, y) : SBD_OK;
 }
 
 int sbd_sigma(sbd_ctx *ctx, const double *x_full, double *y) {
@@ -1204,6 +1248,7 @@ int sbd_sigma(sbd_ctx *ctx, const double *x_full, double *y) {
         if (rc) return rc;
         return sbd_explicit_sigma(ctx, x_full, y);
     }
+    if (sbd_samespin_gemm_on(ctx)) return sigma_dense(ctx, x_full, y);
     rc = sbd_sigma_local(ctx, x_full + ctx->own_lo() * ctx->sec[1].n);
     if (rc) return rc;
     return sbd_sigma_remote(ctx, x_full, y);
@@ -1229,7 +1274,7 @@ int sbd_sigma_host(sbd_ctx *ctx, const double *x_host, double *y_host) {
     SBD_CUDA(ctx, ctx->hy.ensure(sizeof(double) * (nown + 2)));
     double *dx = ctx->hx.as<double>(), *dy = ctx->hy.as<double>();
     const bool pipelined = !ctx->explicit_mode && rows == A.n && nb % 2 == 0 && use_side_tma() && rows > 2 * kTW &&
-                           !(A.ns > 0 && B.ns > 0 && cross_additive(ctx));
+                           !(A.ns > 0 && B.ns > 0 && cross_additive(ctx)) && !sbd_samespin_gemm_on(ctx);
     if (!pipelined) {
         if (nfull) SBD_CUDA(ctx, cudaMemcpyAsync(dx, x_host, sizeof(double) * nfull, cudaMemcpyHostToDevice, ctx->stream));
         rc = sbd_sigma(ctx, dx, dy);

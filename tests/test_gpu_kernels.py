@@ -178,6 +178,9 @@ SIGMA_VARIANTS = [
     {"SBD_CROSS_UNSTAGED": "1"},
     {"SBD_CROSS_ADD": "1"},
     {"SBD_CROSS_ADD": "0", "SBD_YT_BLOCKED": "0"},
+    {"SBD_DENSE_GEMM": "1"},
+    {"SBD_DENSE_GEMM": "1", "SBD_CROSS_ADD": "1"},
+    {"SBD_DENSE_GEMM": "0"},
 ]
 
 
