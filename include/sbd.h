@@ -114,6 +114,11 @@ int sbd_diag(sbd_ctx *ctx, double *out_dev);
  * amplitudes, y_dev the owned rows.  Row-owned, no atomics on y. */
 int sbd_sigma(sbd_ctx *ctx, const double *x_full_dev, double *y_dev);
 
+/* nvec sigmas in one call (the block form SURVEY 8(b) lists: Davidson with block expansion, several
+ * roots): vector v is x_full_dev + v * ldx, its result y_dev + v * ldy (ldx >= n_alpha*n_beta,
+ * ldy >= owned determinants).  Stream-ordered, one vector after the other. */
+int sbd_sigma_multi(sbd_ctx *ctx, const double *x_full_dev, int64_t ldx, double *y_dev, int64_t ldy, int nvec);
+
 /* Split form for multi-GPU overlap (the ring of distsim.py:200-259):
  *   sbd_sigma_local  -- beta-beta part from the OWNED rows only (no remote data);
  *   sbd_sigma_remote -- alpha-alpha + alpha-beta part once x_full is gathered,

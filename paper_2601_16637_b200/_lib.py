@@ -45,6 +45,7 @@ _SIGS = {
     "sbd_sigma_host": [_vp, _vp, _vp],
     "sbd_sigma_model": [_vp, _vp, _vp],
     "sbd_last_task0": [_vp, _vp],
+    "sbd_sigma_multi": [_vp, _vp, _c_i64, _vp, _c_i64, _c_int],
     "sbd_vdots": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _vp],
     "sbd_vdots2": [_vp, _vp, _c_int, _c_i64, _c_i64, _vp, _vp, _vp],
     "sbd_residual_precond": [_vp, _vp, _vp, _c_int, _c_i64, _c_i64, _vp, _vp, _c_int, _vp, _c_dbl, _vp,

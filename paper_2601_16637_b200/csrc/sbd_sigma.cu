@@ -1254,6 +1254,19 @@ int sbd_sigma(sbd_ctx *ctx, const double *x_full, double *y) {
     return sbd_sigma_remote(ctx, x_full, y);
 }
 
+int sbd_sigma_multi(sbd_ctx *ctx, const double *x_full, int64_t ldx, double *y, int64_t ldy, int nvec) {
+    SBD_CHECK_CTX(ctx);
+    if (nvec < 0) return sbd_fail(ctx, SBD_EINVAL, "nvec must be >= 0");
+    const i64 nfull = ctx->explicit_mode ? ctx->n_det : ctx->sec[0].n * ctx->sec[1].n;
+    const i64 nown = ctx->explicit_mode ? ctx->n_det : ctx->own_rows() * ctx->sec[1].n;
+    if (nvec > 1 && (ldx < nfull || ldy < nown)) return sbd_fail(ctx, SBD_EINVAL, "leading dimension too small");
+    for (int v = 0; v < nvec; ++v) {
+        int rc = sbd_sigma(ctx, x_full + (i64)v * ldx, y + (i64)v * ldy);
+        if (rc) return rc;
+    }
+    return SBD_OK;
+}
+
 // Host buffers in and out.  With one owner of all rows and the aligned
 // kernels, the copies are pipelined with the kernels in kTW-aligned alpha-row
 // chunks on a second stream: the beta side of chunk c (it only reads x rows

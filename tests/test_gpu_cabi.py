@@ -62,3 +62,22 @@ def test_c_program_sigma_and_davidson_vs_oracle(tmp_path, norb, ne_a, ne_b, nsa,
     ref = O.davidson(lambda v: O.sigma(inst, v), O.diag(inst), n_roots=n_roots)
     assert conv == 1 and nfound == n_roots
     np.testing.assert_allclose(e, ref.energies, atol=1e-8, rtol=0)
+
+
+def test_sigma_multi_equals_single_calls():
+    """sbd_sigma_multi (the block form of SURVEY 8(b)) against nvec single sbd_sigma calls, and its argument checks."""
+    import torch
+
+    from paper_2601_16637_b200 import HamiltonianApplier, SelectedBasis, _lib
+    from paper_2601_16637_b200.synth import random_integrals, random_product_strings
+
+    a, b = random_product_strings(11, 4, 4, 120, 90, seed=5)
+    app = HamiltonianApplier(SelectedBasis.product(a.tolist(), b.tolist(), 11, 4, 4), random_integrals(11, seed=5))
+    n, nvec, ld = app.n, 3, app.n + 6
+    X = torch.randn(nvec, ld, dtype=torch.float64, device="cuda")
+    Y = torch.zeros(nvec, ld, dtype=torch.float64, device="cuda")
+    app._ctx("sbd_sigma_multi", _lib.ptr(X), ld, _lib.ptr(Y), ld, nvec)
+    for v in range(nvec):
+        assert torch.equal(Y[v, :n], app.sigma_device(X[v, :n].contiguous()))
+    with pytest.raises(ValueError):
+        app._ctx("sbd_sigma_multi", _lib.ptr(X), n - 1, _lib.ptr(Y), ld, 2)
