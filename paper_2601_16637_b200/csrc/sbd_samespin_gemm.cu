@@ -55,8 +55,9 @@ bool sbd_samespin_gemm_on(const sbd_ctx *ctx) {
     if (A.n == 0 || B.n == 0 || A.n > kGemmMaxStrings || B.n > kGemmMaxStrings) return false;
     if (e && e[0] == '1') return true;
     // streaming 8 c-bar bytes from L2 vs 2 n flops on the DMMA pipe per determinant: dense wins above
-    // ~1/7 of the row; both sectors (the alpha and the beta products run together)
-    auto dense = [](const Sector &S) { return 8 * (S.ns + S.nd) >= S.n * S.n; };
+    // ~1/7 of the row; both sectors (the alpha and the beta products run together), and only where the
+    // products are worth a cuBLAS launch and a second stream (n >= 256)
+    auto dense = [](const Sector &S) { return S.n >= 256 && 8 * (S.ns + S.nd) >= S.n * S.n; };
     return dense(A) && dense(B);
 }
 
