@@ -25,7 +25,8 @@ import oracle as O  # noqa: E402  (checker)
 
 SIGMA_ENVS = [{}, {"SBD_SIDE_LDG": "1"}, {"SBD_YT_BLOCKED": "0"}, {"SBD_CROSS_NO_CLUSTER": "1"},
               {"SBD_CROSS_UNSTAGED": "1"}, {"SBD_CROSS_ADD": "1"}, {"SBD_CROSS_DCI": "1"},
-              {"SBD_CROSS_DCI": "1", "SBD_CROSS_ADD": "1"}]
+              {"SBD_CROSS_DCI": "1", "SBD_CROSS_ADD": "1"}, {"SBD_DENSE_GEMM": "1"},
+              {"SBD_DENSE_GEMM": "1", "SBD_CROSS_DCI": "1"}]
 DAV_ENVS = [{}, {"SBD_DAV_TMA": "1"}, {"SBD_NO_TMA": "1"}]
 
 
