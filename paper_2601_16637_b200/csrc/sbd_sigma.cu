@@ -817,6 +817,12 @@ bool yt_blocked_enabled() {  // SBD_YT_BLOCKED=0 keeps the row-contiguous Y^T la
     return !(e && e[0] == '0');
 }
 
+i64 sigma_host_chunks() {  // alpha-row chunks of the pipelined host-buffer sigma (SBD_HOST_CHUNKS, A/B)
+    const char *e = getenv("SBD_HOST_CHUNKS");
+    const long v = e ? strtol(e, nullptr, 10) : 0;
+    return v > 0 ? (i64)v : 8;
+}
+
 bool use_side_tma() {  // SBD_SIDE_LDG=1 selects the register-staged stream (A/B measurements)
     const char *e = getenv("SBD_SIDE_LDG");
     return !(e && e[0] == '1');
@@ -914,19 +920,21 @@ bool cross_additive(const sbd_ctx *ctx) {
     return B.sell_groups > 0 && 2 * sell_nonzero_groups(B) < B.sell_groups;
 }
 
+// Task 0 for the owned rows [r0, r1) (r1 < 0: all of them); y points at owned row 0.
 int launch_cross(sbd_ctx *ctx, const double *x_full, double *y, bool additive = false,
-                 const SConn *sconn = nullptr) {
-    if (sbd_dci_eligible(ctx, x_full)) {
+                 const SConn *sconn = nullptr, i64 r0 = 0, i64 r1 = -1) {
+    if (r1 < 0) r1 = ctx->own_rows();
+    if (r0 == 0 && r1 == ctx->own_rows() && sbd_dci_eligible(ctx, x_full)) {
         ctx->last_task0 = 4;
         return sbd_cross_dci(ctx, x_full, y, additive, sconn);
     }
     const Sector &A = ctx->sec[0], &B = ctx->sec[1];
     CrossArgs ca{};
-    ca.n_rows = ctx->own_rows();
-    ca.row_base = ctx->own_lo();
+    ca.n_rows = r1 - r0;
+    ca.row_base = ctx->own_lo() + r0;
     ca.nb = B.n;
     ca.X = x_full;
-    ca.Y = y;
+    ca.Y = y + r0 * B.n;
     ca.a_s_off = A.s_off.as<int64_t>();
     ca.a_sconn = sconn ? sconn : A.sconn.as<SConn>();
     ca.a_row = A.s_row.as<int32_t>();
@@ -1300,7 +1308,7 @@ int sbd_sigma_host(sbd_ctx *ctx, const double *x_host, double *y_host) {
     if (rc) return rc;
     rc = ensure_diag(ctx);
     if (rc) return rc;
-    const i64 nch = 8;
+    const i64 nch = sigma_host_chunks();
     const i64 step = std::max<i64>(kTW, (rows / nch + kTW - 1) / kTW * kTW);
     std::vector<i64> cut{0};
     while (cut.back() < rows) cut.push_back(std::min(rows, cut.back() + step));
@@ -1321,12 +1329,14 @@ int sbd_sigma_host(sbd_ctx *ctx, const double *x_host, double *y_host) {
         rc = launch_beta_side(ctx, dx, r0, r1);
         if (rc) return rc;
     }
-    if (A.ns > 0 && B.ns > 0) {
-        rc = launch_cross(ctx, dx, dy);
-        if (rc) return rc;
-    }
+    // task 0 chunk by chunk too: chunk 0's result (and its download) starts after its own rows'
+    // task 0 instead of the whole matrix's (PCIe idles less between the upload and the download)
     for (size_t c = 0; c < nc; ++c) {
         const i64 r0 = cut[c], r1 = cut[c + 1];
+        if (A.ns > 0 && B.ns > 0) {
+            rc = launch_cross(ctx, dx, dy, false, nullptr, r0, r1);
+            if (rc) return rc;
+        }
         rc = launch_alpha_side(ctx, dx, dy, r0, r1);
         if (rc) return rc;
         SBD_CUDA(ctx, cudaEventRecord(ev[nc + c], ctx->stream));

@@ -1,6 +1,6 @@
 """Same-process A/B of environment knobs on the Davidson solve at the bench workload (cfg2, 1e8 dets).
 
-    python tools/ab_davidson.py "SBD_RES_KEEPV=0" "SBD_RES_KEEPV=1" [--iters 60] [--rounds 2]
+    python tools/ab_davidson.py "SBD_RES_SPLIT=1" "SBD_RES_SPLIT=2" [--iters 60] [--rounds 2]
 
 Each variant runs the native solve at reference defaults (max_iters --iters) alternately; prints the
 mean s/iter after the first iteration, the iteration count and E0 per variant (one JSON line).

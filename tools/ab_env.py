@@ -1,6 +1,6 @@
 """Same-process A/B of environment knobs on the sigma build, over sweep points.
 
-    python tools/ab_env.py "SBD_SIDE_PERSIST=0" "SBD_SIDE_PERSIST=1" [--points cfg1,cfg2,cfg4,1e9] [--steps K]
+    python tools/ab_env.py "SBD_CROSS_DCI=0" "SBD_CROSS_DCI=1" [--points cfg1,cfg2,cfg4,1e9] [--steps K]
 
 Each point is built once; the variants are timed alternately (CUDA events over K
 sigma builds after 2 warm-ups, best of 3 rounds) so box-to-box clock drift cancels.
