@@ -820,7 +820,7 @@ bool yt_blocked_enabled() {  // SBD_YT_BLOCKED=0 keeps the row-contiguous Y^T la
 i64 sigma_host_chunks() {  // alpha-row chunks of the pipelined host-buffer sigma (SBD_HOST_CHUNKS, A/B)
     const char *e = getenv("SBD_HOST_CHUNKS");
     const long v = e ? strtol(e, nullptr, 10) : 0;
-    return v > 0 ? (i64)v : 8;
+    return v > 0 ? (i64)v : 24;  // 512-row chunks at cfg2: 29.6 vs 29.9 ms with 8 (profiles/r3c, r3d)
 }
 
 bool use_side_tma() {  // SBD_SIDE_LDG=1 selects the register-staged stream (A/B measurements)
