@@ -195,6 +195,7 @@ int sbd_set_strings(sbd_ctx *ctx, int spin, const uint64_t *strings, int64_t n, 
 
 int sbd_build_tables(sbd_ctx *ctx) {
     SBD_CHECK_CTX(ctx);
+    SbdRange range("sbd/build_tables");
     if (!ctx->have_integrals) return sbd_fail(ctx, SBD_EINVAL, "integrals not set");
     SBD_TSTAMP("start");
     for (int spin = 0; spin < 2; ++spin) {

@@ -457,6 +457,7 @@ int sbd_dist_plan(sbd_ctx *ctx, int exchange, double sparse_threshold, int group
 
 int sbd_sigma_dist(sbd_ctx *ctx, const double *x_own, double *y_own) {
     SBD_CHECK_CTX(ctx);
+    SbdRange range("sbd/sigma_dist");
     DistState &d = ctx->dist;
     if (!d.on) return sbd_fail(ctx, SBD_EINVAL, "sbd_sigma_dist: call sbd_dist_init first");
     if (!x_own || !y_own) return sbd_fail(ctx, SBD_EINVAL, "null vector");

@@ -11,6 +11,14 @@
 #include <vector>
 
 #include "../../include/sbd.h"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for profilers (no-ops without one attached)
+
+// Scoped NVTX range: sigma phases, table builds and Davidson iterations show up by name in
+// Nsight Compute / Systems timelines (`ncu --nvtx --nvtx-include "sbd/"`).
+struct SbdRange {
+    explicit SbdRange(const char *name) { nvtxRangePushA(name); }
+    ~SbdRange() { nvtxRangePop(); }
+};
 
 typedef uint64_t u64;
 typedef int64_t i64;

@@ -1248,6 +1248,7 @@ int sbd_sigma_remote(sbd_ctx *ctx, const double *x_full, double *y) {
 
 int sbd_sigma(sbd_ctx *ctx, const double *x_full, double *y) {
     SBD_CHECK_CTX(ctx);
+    SbdRange range("sbd/sigma");
     int rc = require_ready(ctx);
     if (rc) return rc;
     if (!x_full || !y) return sbd_fail(ctx, SBD_EINVAL, "null vector");
@@ -1284,6 +1285,7 @@ int sbd_sigma_multi(sbd_ctx *ctx, const double *x_full, int64_t ldx, double *y, 
 // be pinned for the copies to be asynchronous.
 int sbd_sigma_host(sbd_ctx *ctx, const double *x_host, double *y_host) {
     SBD_CHECK_CTX(ctx);
+    SbdRange range("sbd/sigma_host");
     int rc = require_ready(ctx);
     if (rc) return rc;
     const Sector &A = ctx->sec[0], &B = ctx->sec[1];

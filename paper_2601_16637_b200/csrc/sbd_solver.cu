@@ -394,6 +394,7 @@ struct Solver {
         std::vector<double> theta(m, 0.0), res(m, INFINITY);
         double sigma_ms = 0.0;
         for (int iteration = 1; iteration <= o.max_iters; ++iteration) {
+            SbdRange range("sbd/davidson_iteration");
             const auto t_iter = std::chrono::steady_clock::now();
             auto iter_done = [&]() {
                 if (st->iter_ms_hist)
