@@ -13,16 +13,17 @@
 //   sigma[ia,ib] = sum_m  s_m G[q(Pb_m)][jb_m]                  (36 gathers per determinant)
 // with q over the norb (norb - 1) / 2 off-diagonal orbital pairs.
 //
-// Kernel: one persistent CTA per SM walks its alpha rows; a row's beta
-// columns jb are cut into tiles of NT (64, or 32 when shared memory is short).  Per (row, tile):
-//   1. the row's K x NT slab of x (rows ja_k) is staged by cp.async, one
-//      tile ahead (double buffer);
-//   2. G tile (nqp x NT) = E (nqp x Kp, built per row from the pair-pair
-//      ERI matrix and the alpha phases) times the slab, on DMMA.8x8x4:
-//      warp w owns the 8 columns w*8.. of the tile and every row fragment;
-//   3. each thread owns beta positions ib and adds the G entries its beta
-//      singles point at inside this tile (lists sorted by jb, cut per tile),
-//      so every sigma element is summed by one thread in a fixed order: no
+// Kernel: one persistent CTA per SM (16 warps) walks its alpha rows; a row's beta
+// columns jb are cut into tiles of 128.  Per (row, tile):
+//   1. the row's K x 128 slab of x (rows ja_k) is staged by cp.async, one
+//      tile ahead (double buffer), with the tile's gather block (below);
+//   2. G tile (nqp x 128) = E (nqp x Kp, built once per row from the pair-pair
+//      ERI matrix and the alpha phases; each warp keeps its fragments of it in
+//      registers for the whole row) times the slab, on DMMA.8x8x4: the warps
+//      form a 4 x 4 grid over row fragments x 32-column quarters;
+//   3. each thread owns beta positions ib and adds, in a fixed order, the G
+//      entries its beta singles point at inside this tile (a u16 ELL block per
+//      tile, staged in shared memory; padding reads a zero row of G): no
 //      atomics, bitwise reproducible.
 // The row is written once (or added, for the additive task-0 order).
 #include <algorithm>
