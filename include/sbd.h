@@ -102,6 +102,25 @@ int sbd_export_table(sbd_ctx *ctx, int spin,
 /* Sorted strings and sort permutation (sorted[i] = strings[perm[i]]). */
 int sbd_export_sorted(sbd_ctx *ctx, int spin, uint64_t *sorted_host, int64_t *perm_host);
 
+/* 128-bit strings (norb <= 128): configuration processing and excitation
+ * generation only.  The reference's table builder works on Python ints of any
+ * width (enumerate_singles/doubles, build_excitation_table: basis.py:62-103,
+ * 362-403); its integrals stop at 64 orbitals (integrals.py:67-68), so there is
+ * no sigma for these strings.  words_host holds n (lo, hi) pairs: string i =
+ * words[2i] | words[2i+1] << 64.  Needs no integrals; replaces the table the
+ * previous call built.  Bits above norb-1 or a wrong electron count ->
+ * SBD_EINVAL (basis.py:185-194); duplicated strings -> SBD_EINVAL. */
+int sbd_table128_build(sbd_ctx *ctx, int norb, const uint64_t *words_host, int64_t n, int n_elec);
+int sbd_table128_counts(sbd_ctx *ctx, int64_t *n_strings, int64_t *n_singles, int64_t *n_doubles);
+int sbd_table128_export(sbd_ctx *ctx,
+                        int64_t *s_off_host, int64_t *s_tgt_host, int16_t *s_hole_host,
+                        int16_t *s_part_host, int8_t *s_phase_host,
+                        int64_t *d_off_host, int64_t *d_tgt_host, int16_t *d_hole1_host,
+                        int16_t *d_hole2_host, int16_t *d_part1_host, int16_t *d_part2_host,
+                        int8_t *d_phase_host);
+/* Sorted (lo, hi) pairs and the sort permutation. */
+int sbd_table128_sorted(sbd_ctx *ctx, uint64_t *sorted_words_host, int64_t *perm_host);
+
 /* Rows this context owns: alpha rows [alpha_lo, alpha_hi) x all beta
  * (make_partition semantics, distsim.py:63-77).  Default: all rows. */
 int sbd_set_row_window(sbd_ctx *ctx, int64_t alpha_lo, int64_t alpha_hi);

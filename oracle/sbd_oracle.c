@@ -434,6 +434,123 @@ void orc_table_fill(const u64 *strings, i64 n, int norb, const i64 *s_off, const
     free(sorted);
 }
 
+/* ---- the same tables for strings of up to 128 orbitals (two 64-bit words) ----
+ * basis.py:62-103 and 362-403 operate on Python ints of any width; only the integrals are
+ * capped at 64 orbitals (integrals.py:67-68).  Strings arrive as (lo, hi) word pairs. */
+
+typedef unsigned __int128 u128;
+typedef struct { u128 key; i64 idx; } keyidx128;
+static inline u128 bit128(int p) { return (u128)1 << p; }
+static inline u128 word128(const u64 *w, i64 i) { return (u128)w[2 * i] | ((u128)w[2 * i + 1] << 64); }
+static inline int popc128(u128 w) { return popc((u64)w) + popc((u64)(w >> 64)); }
+/* basis.py:62-69 */
+static inline int iphase128(u128 w, int p, int r) {
+    int lo = p < r ? p : r, hi = p < r ? r : p;
+    u128 mask = (bit128(hi) - 1) & ~((bit128(lo) << 1) - 1);
+    return popc128(w & mask) & 1 ? -1 : 1;
+}
+static int cmp_keyidx128(const void *a, const void *b) {
+    u128 x = ((const keyidx128 *)a)->key, y = ((const keyidx128 *)b)->key;
+    return x < y ? -1 : x > y;
+}
+static i64 lookup128(const keyidx128 *sorted, i64 n, u128 key) {
+    i64 lo = 0, hi = n;
+    while (lo < hi) {
+        i64 mid = (lo + hi) >> 1;
+        if (sorted[mid].key < key) lo = mid + 1; else hi = mid;
+    }
+    return (lo < n && sorted[lo].key == key) ? sorted[lo].idx : -1;
+}
+
+/* basis.py:72-103, same loop nesting as enum_string above */
+static void enum_string128(u128 s, int norb, const keyidx128 *sorted, i64 n, i64 *ns, i64 *nd,
+                           i64 *s_tgt, int16_t *s_hole, int16_t *s_part, int8_t *s_phase,
+                           i64 *d_tgt, int16_t *d_h1, int16_t *d_h2, int16_t *d_p1, int16_t *d_p2, int8_t *d_phase) {
+    int occ[128], virt[128], no = 0, nv = 0;
+    for (int o = 0; o < norb; ++o) { if ((s >> o) & 1) occ[no++] = o; else virt[nv++] = o; }
+    i64 cs = 0, cd = 0;
+    for (int a = 0; a < no; ++a)
+        for (int b = 0; b < nv; ++b) {
+            int p = occ[a], r = virt[b];
+            i64 j = lookup128(sorted, n, (s & ~bit128(p)) | bit128(r));
+            if (j < 0) continue;
+            if (s_tgt) { s_tgt[cs] = j; s_hole[cs] = p; s_part[cs] = r; s_phase[cs] = iphase128(s, p, r); }
+            ++cs;
+        }
+    for (int a = 0; a < no; ++a)
+        for (int a2 = a + 1; a2 < no; ++a2)
+            for (int b = 0; b < nv; ++b)
+                for (int b2 = b + 1; b2 < nv; ++b2) {
+                    int p = occ[a], q = occ[a2], r = virt[b], so = virt[b2];
+                    u128 inter = (s & ~bit128(p)) | bit128(r);
+                    i64 j = lookup128(sorted, n, (inter & ~bit128(q)) | bit128(so));
+                    if (j < 0) continue;
+                    if (d_tgt) {
+                        d_tgt[cd] = j; d_h1[cd] = p; d_h2[cd] = q; d_p1[cd] = r; d_p2[cd] = so;
+                        d_phase[cd] = iphase128(s, p, r) * iphase128(inter, q, so);
+                    }
+                    ++cd;
+                }
+    *ns = cs; *nd = cd;
+}
+
+typedef struct {
+    const u64 *words; i64 n; int norb; const keyidx128 *sorted;
+    i64 *s_off, *d_off;
+    i64 *s_tgt; int16_t *s_hole, *s_part; int8_t *s_phase;
+    i64 *d_tgt; int16_t *d_h1, *d_h2, *d_p1, *d_p2; int8_t *d_phase;
+} table128_job;
+
+static void count128_range(i64 lo, i64 hi, void *vp) {
+    table128_job *j = (table128_job *)vp;
+    for (i64 i = lo; i < hi; ++i) {
+        i64 ns, nd;
+        enum_string128(word128(j->words, i), j->norb, j->sorted, j->n, &ns, &nd, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0);
+        j->s_off[i + 1] = ns; j->d_off[i + 1] = nd;
+    }
+}
+
+static void fill128_range(i64 lo, i64 hi, void *vp) {
+    table128_job *j = (table128_job *)vp;
+    for (i64 i = lo; i < hi; ++i) {
+        i64 ns, nd, so = j->s_off[i], dof = j->d_off[i];
+        enum_string128(word128(j->words, i), j->norb, j->sorted, j->n, &ns, &nd, j->s_tgt + so, j->s_hole + so,
+                       j->s_part + so, j->s_phase + so, j->d_tgt + dof, j->d_h1 + dof, j->d_h2 + dof,
+                       j->d_p1 + dof, j->d_p2 + dof, j->d_phase + dof);
+    }
+}
+
+static keyidx128 *make_sorted128(const u64 *words, i64 n) {
+    keyidx128 *k = (keyidx128 *)malloc(sizeof(keyidx128) * (n ? n : 1));
+    for (i64 i = 0; i < n; ++i) { k[i].key = word128(words, i); k[i].idx = i; }
+    qsort(k, n, sizeof(keyidx128), cmp_keyidx128);
+    return k;
+}
+
+/* words: 2n u64, string i = words[2i] | words[2i+1] << 64.  -1 on duplicates (basis.py:364-366). */
+int orc_table128_count(const u64 *words, i64 n, int norb, i64 *s_off, i64 *d_off, int nthreads) {
+    keyidx128 *sorted = make_sorted128(words, n);
+    for (i64 i = 1; i < n; ++i)
+        if (sorted[i].key == sorted[i - 1].key) { free(sorted); return -1; }
+    s_off[0] = d_off[0] = 0;
+    table128_job j = {words, n, norb, sorted, s_off, d_off};
+    par_for(n, 4, nthreads, count128_range, &j);
+    for (i64 i = 0; i < n; ++i) { s_off[i + 1] += s_off[i]; d_off[i + 1] += d_off[i]; }
+    free(sorted);
+    return 0;
+}
+
+void orc_table128_fill(const u64 *words, i64 n, int norb, const i64 *s_off, const i64 *d_off,
+                       i64 *s_tgt, int16_t *s_hole, int16_t *s_part, int8_t *s_phase,
+                       i64 *d_tgt, int16_t *d_h1, int16_t *d_h2, int16_t *d_p1, int16_t *d_p2, int8_t *d_phase,
+                       int nthreads) {
+    keyidx128 *sorted = make_sorted128(words, n);
+    table128_job j = {words, n, norb, sorted, (i64 *)s_off, (i64 *)d_off, s_tgt, s_hole, s_part, s_phase,
+                      d_tgt, d_h1, d_h2, d_p1, d_p2, d_phase};
+    par_for(n, 4, nthreads, fill128_range, &j);
+    free(sorted);
+}
+
 /* davidson.py:86-124: cyclic Jacobi on a symmetric n x n (row-major a, v). */
 int orc_jacobi_kernel(double *a, double *v, int n, double tol, int max_sweeps) {
     for (int sweep = 0; sweep < max_sweeps; ++sweep) {

@@ -14,8 +14,11 @@ from .apply import (
     apply_H,
     apply_H_full,
     build_excitation_table,
+    build_excitation_table128,
     build_spin_tables,
     compute_diagonal,
+    sorted_strings128,
+    string_words,
 )
 from .basis import (
     Determinant,
@@ -55,6 +58,10 @@ __all__ = [
     # B200 extensions: device ingestion
     "ingest_sample_arrays",
     "start_vector",
+    # B200 extensions: 128-bit strings (north_star (1)-(2)), tables only
+    "build_excitation_table128",
+    "sorted_strings128",
+    "string_words",
     "ExcitationTable",
     "DavidsonStats",
     "FcidumpError",

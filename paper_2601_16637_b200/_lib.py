@@ -37,6 +37,10 @@ _SIGS = {
     "sbd_table_counts": [_vp, _c_int, _vp, _vp, _vp],
     "sbd_export_table": [_vp, _c_int] + [_vp] * 12,
     "sbd_export_sorted": [_vp, _c_int, _vp, _vp],
+    "sbd_table128_build": [_vp, _c_int, _vp, _c_i64, _c_int],
+    "sbd_table128_counts": [_vp, _vp, _vp, _vp],
+    "sbd_table128_export": [_vp] + [_vp] * 12,
+    "sbd_table128_sorted": [_vp, _vp, _vp],
     "sbd_set_row_window": [_vp, _c_i64, _c_i64],
     "sbd_diag": [_vp, _vp],
     "sbd_sigma": [_vp, _vp, _vp],

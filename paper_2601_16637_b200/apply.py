@@ -81,21 +81,84 @@ def _upload_instance(ctx: _lib.Context, table: IntegralTable, alpha: np.ndarray,
     ctx("sbd_build_tables")
 
 
-def _export_table(ctx: _lib.Context, spin: int, norb: int) -> ExcitationTable:
-    n, ns, nd = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-    ctx("sbd_table_counts", spin, ctypes.byref(n), ctypes.byref(ns), ctypes.byref(nd))
-    n, ns, nd = n.value, ns.value, nd.value
-    cols = dict(
+_TABLE_ORDER = ("s_off", "s_tgt", "s_hole", "s_part", "s_phase", "d_off", "d_tgt", "d_hole1", "d_hole2",
+                "d_part1", "d_part2", "d_phase")
+
+
+def _table_columns(n: int, ns: int, nd: int) -> dict:
+    return dict(
         s_off=np.zeros(n + 1, np.int64), s_tgt=np.zeros(ns, np.int64), s_hole=np.zeros(ns, np.int16),
         s_part=np.zeros(ns, np.int16), s_phase=np.zeros(ns, np.int8),
         d_off=np.zeros(n + 1, np.int64), d_tgt=np.zeros(nd, np.int64), d_hole1=np.zeros(nd, np.int16),
         d_hole2=np.zeros(nd, np.int16), d_part1=np.zeros(nd, np.int16), d_part2=np.zeros(nd, np.int16),
         d_phase=np.zeros(nd, np.int8),
     )
-    order = ("s_off", "s_tgt", "s_hole", "s_part", "s_phase", "d_off", "d_tgt", "d_hole1", "d_hole2",
-             "d_part1", "d_part2", "d_phase")
-    ctx("sbd_export_table", spin, *[_lib.ptr(cols[k]) if cols[k].size else None for k in order])
-    return ExcitationTable(n_strings=n, norb=norb, **cols)
+
+
+def _export_table(ctx: _lib.Context, spin: int, norb: int) -> ExcitationTable:
+    n, ns, nd = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    ctx("sbd_table_counts", spin, ctypes.byref(n), ctypes.byref(ns), ctypes.byref(nd))
+    cols = _table_columns(n.value, ns.value, nd.value)
+    ctx("sbd_export_table", spin, *[_lib.ptr(cols[k]) if cols[k].size else None for k in _TABLE_ORDER])
+    return ExcitationTable(n_strings=n.value, norb=norb, **cols)
+
+
+def string_words(strings) -> np.ndarray:
+    """Strings of up to 128 orbitals (Python ints, or an (n, 2) uint64 array) -> (n, 2) uint64 (lo, hi)."""
+    if isinstance(strings, np.ndarray) and strings.ndim == 2:
+        if strings.shape[1] != 2:
+            raise ValueError("a word array must have shape (n, 2)")
+        return np.ascontiguousarray(strings, dtype=np.uint64)
+    vals = [int(v) for v in strings]
+    if any(v < 0 or v >> 128 for v in vals):
+        raise ValueError("strings must be non-negative and below 2**128")
+    return np.array([[v & 0xFFFFFFFFFFFFFFFF, v >> 64] for v in vals], dtype=np.uint64).reshape(-1, 2)
+
+
+def build_excitation_table128(strings, norb: int, n_elec: Optional[int] = None, device=None) -> ExcitationTable:
+    """``build_excitation_table`` for strings of up to 128 orbitals (two-word masks), built on the GPU.
+
+    The reference's table builder (``basis.py:62-103,362-403``) works on Python ints of any width; its
+    integrals stop at 64 orbitals (``integrals.py:67-68``), so wide strings get tables (and the sorted
+    order, ``sorted_strings128``) but no Hamiltonian.  ``strings``: Python ints or (n, 2) uint64 words.
+    """
+    if not 1 <= norb <= 128:
+        raise ValueError(f"norb must be in [1, 128], got {norb}")
+    w = string_words(strings)
+    n = w.shape[0]
+    counts = [int(a).bit_count() + int(b).bit_count() for a, b in w.tolist()]
+    if n_elec is None:
+        n_elec = counts[0] if n else 0
+        if any(c != n_elec for c in counts):
+            raise ValueError("strings have different electron counts")
+    ctx = _lib.Context(_device_index(device))
+    try:
+        ctx("sbd_table128_build", int(norb), _lib.ptr(w) if n else None, int(n), int(n_elec))
+        nn, ns, nd = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        ctx("sbd_table128_counts", ctypes.byref(nn), ctypes.byref(ns), ctypes.byref(nd))
+        cols = _table_columns(nn.value, ns.value, nd.value)
+        ctx("sbd_table128_export", *[_lib.ptr(cols[k]) if cols[k].size else None for k in _TABLE_ORDER])
+        return ExcitationTable(n_strings=nn.value, norb=norb, **cols)
+    finally:
+        ctx.close()
+
+
+def sorted_strings128(strings, norb: int, device=None):
+    """Device radix sort of up to 128-bit strings: (sorted (n, 2) uint64 words, perm int64), sorted = words[perm].
+
+    Rejects duplicates (the uniqueness check of ``basis.py:364-366``)."""
+    w = string_words(strings)
+    n = w.shape[0]
+    n_elec = int(w[0, 0]).bit_count() + int(w[0, 1]).bit_count() if n else 0
+    ctx = _lib.Context(_device_index(device))
+    try:
+        ctx("sbd_table128_build", int(norb), _lib.ptr(w) if n else None, int(n), n_elec)
+        out, perm = np.zeros((n, 2), np.uint64), np.zeros(n, np.int64)
+        if n:
+            ctx("sbd_table128_sorted", _lib.ptr(out), _lib.ptr(perm))
+        return out, perm
+    finally:
+        ctx.close()
 
 
 def build_excitation_table(strings, norb: int, n_elec: Optional[int] = None, device=None) -> ExcitationTable:
@@ -103,9 +166,12 @@ def build_excitation_table(strings, norb: int, n_elec: Optional[int] = None, dev
 
     Same contract as reference ``basis.py:362-403`` (caller-order rows and
     targets, enumeration order within a row, ValueError on duplicates).
+    ``norb`` > 64 takes the two-word path (:func:`build_excitation_table128`).
     """
     from .integrals import IntegralTable as _IT
 
+    if norb > 64:
+        return build_excitation_table128(strings, norb, n_elec, device)
     arr = np.ascontiguousarray(np.asarray(list(strings) if not isinstance(strings, np.ndarray) else strings,
                                           dtype=np.uint64))
     if n_elec is None:

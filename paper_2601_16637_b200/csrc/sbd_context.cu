@@ -241,13 +241,9 @@ int sbd_table_counts(sbd_ctx *ctx, int spin, int64_t *n_strings, int64_t *n_sing
     return SBD_OK;
 }
 
-int sbd_export_table(sbd_ctx *ctx, int spin, int64_t *s_off, int64_t *s_tgt, int16_t *s_hole, int16_t *s_part,
-                     int8_t *s_phase, int64_t *d_off, int64_t *d_tgt, int16_t *d_h1, int16_t *d_h2, int16_t *d_p1,
-                     int16_t *d_p2, int8_t *d_phase) {
-    SBD_CHECK_CTX(ctx);
-    if (spin != 0 && spin != 1) return sbd_fail(ctx, SBD_EINVAL, "bad spin");
-    Sector &s = ctx->sec[spin];
-    if (!s.built) return sbd_fail(ctx, SBD_EINVAL, "tables not built");
+static int export_sector(sbd_ctx *ctx, Sector &s, int64_t *s_off, int64_t *s_tgt, int16_t *s_hole, int16_t *s_part,
+                         int8_t *s_phase, int64_t *d_off, int64_t *d_tgt, int16_t *d_h1, int16_t *d_h2, int16_t *d_p1,
+                         int16_t *d_p2, int8_t *d_phase) {
     SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     int rc = 0;
     rc |= copy_down(ctx, s_off, s.s_off, s.n + 1);
@@ -265,6 +261,16 @@ int sbd_export_table(sbd_ctx *ctx, int spin, int64_t *s_off, int64_t *s_tgt, int
     return rc ? SBD_ECUDA : SBD_OK;
 }
 
+int sbd_export_table(sbd_ctx *ctx, int spin, int64_t *s_off, int64_t *s_tgt, int16_t *s_hole, int16_t *s_part,
+                     int8_t *s_phase, int64_t *d_off, int64_t *d_tgt, int16_t *d_h1, int16_t *d_h2, int16_t *d_p1,
+                     int16_t *d_p2, int8_t *d_phase) {
+    SBD_CHECK_CTX(ctx);
+    if (spin != 0 && spin != 1) return sbd_fail(ctx, SBD_EINVAL, "bad spin");
+    Sector &s = ctx->sec[spin];
+    if (!s.built) return sbd_fail(ctx, SBD_EINVAL, "tables not built");
+    return export_sector(ctx, s, s_off, s_tgt, s_hole, s_part, s_phase, d_off, d_tgt, d_h1, d_h2, d_p1, d_p2, d_phase);
+}
+
 int sbd_export_sorted(sbd_ctx *ctx, int spin, uint64_t *sorted_host, int64_t *perm_host) {
     SBD_CHECK_CTX(ctx);
     if (spin != 0 && spin != 1) return sbd_fail(ctx, SBD_EINVAL, "bad spin");
@@ -272,6 +278,77 @@ int sbd_export_sorted(sbd_ctx *ctx, int spin, uint64_t *sorted_host, int64_t *pe
     if (!s.built) return sbd_fail(ctx, SBD_EINVAL, "tables not built");
     SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     int rc = copy_down(ctx, sorted_host, s.sorted, s.n);
+    rc |= copy_down_i32_to_i64(ctx, perm_host, s.perm, s.n);
+    return rc ? SBD_ECUDA : SBD_OK;
+}
+
+// 128-bit strings: basis.py:62-103 + 362-403 on two-word masks (the reference's table builder is
+// width-agnostic; its integrals stop at 64 orbitals, integrals.py:67-68, so no sigma here).
+int sbd_table128_build(sbd_ctx *ctx, int norb, const uint64_t *words, int64_t n, int n_elec) {
+    SBD_CHECK_CTX(ctx);
+    SbdRange range("sbd/table128_build");
+    Sector &s = ctx->t128;
+    s.built = false;
+    if (norb < 1 || norb > 128) return sbd_fail(ctx, SBD_EINVAL, "norb must be in [1, 128]");
+    if (n_elec < 0 || n_elec > norb) return sbd_fail(ctx, SBD_EINVAL, "n_elec must be in [0, norb]");
+    if (n < 0 || (n > 0 && !words)) return sbd_fail(ctx, SBD_EINVAL, "bad string array");
+    if (n >= (i64)INT32_MAX) return sbd_fail(ctx, SBD_EINVAL, "too many strings for int32 indexing");
+    const u64 hi_mask = norb >= 128 ? 0 : norb > 64 ? ~0ull << (norb - 64) : ~0ull;
+    const u64 lo_mask = norb >= 64 ? 0 : ~0ull << norb;
+    for (i64 i = 0; i < n; ++i) {  // SelectedBasis._validate_strings, basis.py:185-194
+        const u64 lo = words[2 * i], hi = words[2 * i + 1];
+        char buf[160];
+        if ((lo & lo_mask) || (hi & hi_mask)) {
+            snprintf(buf, sizeof buf, "string %lld (%#llx:%016llx) has bits above orbital %d", (long long)i,
+                     (unsigned long long)hi, (unsigned long long)lo, norb - 1);
+            return sbd_fail(ctx, SBD_EINVAL, buf);
+        }
+        const int pc = __builtin_popcountll(lo) + __builtin_popcountll(hi);
+        if (pc != n_elec) {
+            snprintf(buf, sizeof buf, "string %lld (%#llx:%016llx) has %d electrons, expected %d", (long long)i,
+                     (unsigned long long)hi, (unsigned long long)lo, pc, n_elec);
+            return sbd_fail(ctx, SBD_EINVAL, buf);
+        }
+    }
+    s.n = n;
+    s.n_elec = n_elec;
+    s.present = true;
+    ctx->t128_norb = norb;
+    SBD_CUDA(ctx, s.str.ensure(2 * sizeof(u64) * (n ? n : 1)));
+    if (n) SBD_CUDA(ctx, cudaMemcpyAsync(s.str.p, words, 2 * sizeof(u64) * n, cudaMemcpyHostToDevice, ctx->stream));
+    int rc = sbd_sort_strings128(ctx, s, norb);
+    if (rc) return rc;
+    rc = sbd_build_sector_tables128(ctx, s, norb);
+    if (rc) return rc;
+    s.built = true;
+    return SBD_OK;
+}
+
+int sbd_table128_counts(sbd_ctx *ctx, int64_t *n_strings, int64_t *n_singles, int64_t *n_doubles) {
+    SBD_CHECK_CTX(ctx);
+    const Sector &s = ctx->t128;
+    if (!s.built) return sbd_fail(ctx, SBD_EINVAL, "128-bit table not built");
+    if (n_strings) *n_strings = s.n;
+    if (n_singles) *n_singles = s.ns;
+    if (n_doubles) *n_doubles = s.nd;
+    return SBD_OK;
+}
+
+int sbd_table128_export(sbd_ctx *ctx, int64_t *s_off, int64_t *s_tgt, int16_t *s_hole, int16_t *s_part,
+                        int8_t *s_phase, int64_t *d_off, int64_t *d_tgt, int16_t *d_h1, int16_t *d_h2, int16_t *d_p1,
+                        int16_t *d_p2, int8_t *d_phase) {
+    SBD_CHECK_CTX(ctx);
+    Sector &s = ctx->t128;
+    if (!s.built) return sbd_fail(ctx, SBD_EINVAL, "128-bit table not built");
+    return export_sector(ctx, s, s_off, s_tgt, s_hole, s_part, s_phase, d_off, d_tgt, d_h1, d_h2, d_p1, d_p2, d_phase);
+}
+
+int sbd_table128_sorted(sbd_ctx *ctx, uint64_t *sorted_words_host, int64_t *perm_host) {
+    SBD_CHECK_CTX(ctx);
+    Sector &s = ctx->t128;
+    if (!s.built) return sbd_fail(ctx, SBD_EINVAL, "128-bit table not built");
+    SBD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    int rc = copy_down(ctx, sorted_words_host, s.sorted, 2 * s.n);
     rc |= copy_down_i32_to_i64(ctx, perm_host, s.perm, s.n);
     return rc ? SBD_ECUDA : SBD_OK;
 }

@@ -13,35 +13,37 @@
 // short search in the L1-resident sorted array).  A ballot + popc compaction
 // keeps enumeration order, so the count pass and the fill pass produce exactly
 // the reference's entry order; targets are mapped back to caller indices
-// through the sort permutation.
+// through the sort permutation.  The kernel is templated on the string word
+// (u64, or U128 for norb <= 128 -- sbd_table128_build, tables only).
 #include <algorithm>
 #include <cstdio>
 #include <vector>
 
 #include "sbd_internal.cuh"
+#include "sbd_words.cuh"
 
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr int kSplit = 4096;  // splitter keys kept in shared memory
 
+template <class W>
 struct EnumSmem {
-    u64 spl[kSplit];
-    uint16_t hole_pairs[2016];  // (a | a2 << 8) for a < a2 < n_occ, lexicographic
-    uint16_t virt_pairs[2016];
-    uint8_t occ[kWarpsPerBlock][64];
-    uint8_t virt[kWarpsPerBlock][64];
+    static constexpr int kMaxOrb = 8 * (int)sizeof(W);
+    static constexpr int kMaxPairs = kMaxOrb * (kMaxOrb - 1) / 2;
+    W spl[kSplit];
+    uint16_t hole_pairs[kMaxPairs];  // (a | a2 << 8) for a < a2 < n_occ, lexicographic
+    uint16_t virt_pairs[kMaxPairs];
+    uint8_t occ[kWarpsPerBlock][kMaxOrb];
+    uint8_t virt[kWarpsPerBlock][kMaxOrb];
 };
 
-__device__ __forceinline__ int sign_between(u64 w, int p, int r) {
-    int lo = min(p, r), hi = max(p, r);
-    u64 mask = ((1ull << hi) - 1) & ~((2ull << lo) - 1);
-    return (__popcll(w & mask) & 1) ? -1 : 1;
-}
+using words::sign_between;
 
 // sorted position of key or -1
-__device__ __forceinline__ int lookup(const EnumSmem &sm, int nspl, int stride, const u64 *__restrict__ sorted,
-                                      i64 n, u64 key) {
+template <class W>
+__device__ __forceinline__ int lookup(const EnumSmem<W> &sm, int nspl, int stride, const W *__restrict__ sorted,
+                                      i64 n, W key) {
     // largest j with spl[j] <= key
     int lo = 0, hi = nspl;  // invariant answer in [lo-1, hi-1]
     while (lo < hi) {
@@ -55,15 +57,15 @@ __device__ __forceinline__ int lookup(const EnumSmem &sm, int nspl, int stride, 
     i64 a = (i64)j * stride, b = min(n, a + stride);
     while (a < b) {
         i64 mid = (a + b) >> 1;
-        if (__ldg(sorted + mid) < key) a = mid + 1;
+        if (words::ldg(sorted + mid) < key) a = mid + 1;
         else b = mid;
     }
-    return (a < n && __ldg(sorted + a) == key) ? (int)a : -1;
+    return (a < n && words::ldg(sorted + a) == key) ? (int)a : -1;
 }
 
-template <bool FILL>
+template <bool FILL, class W>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-enum_kernel(const u64 *__restrict__ str, const u64 *__restrict__ sorted, const int32_t *__restrict__ perm, i64 n,
+enum_kernel(const W *__restrict__ str, const W *__restrict__ sorted, const int32_t *__restrict__ perm, i64 n,
             int norb, int n_elec, int stride, int nspl,
             int64_t *__restrict__ cnt_s, int64_t *__restrict__ cnt_d,            // count pass: [n]
             const int64_t *__restrict__ s_off, const int64_t *__restrict__ d_off,  // fill pass
@@ -72,7 +74,7 @@ enum_kernel(const u64 *__restrict__ str, const u64 *__restrict__ sorted, const i
             int16_t *__restrict__ d_h2, int16_t *__restrict__ d_p1, int16_t *__restrict__ d_p2,
             int8_t *__restrict__ d_phase) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    EnumSmem &sm = *reinterpret_cast<EnumSmem *>(smem_raw);
+    EnumSmem<W> &sm = *reinterpret_cast<EnumSmem<W> *>(smem_raw);
     const int no = n_elec, nv = norb - n_elec;
     const int nhp = no * (no - 1) / 2, nvp = nv * (nv - 1) / 2;
     for (int j = threadIdx.x; j < nspl; j += blockDim.x) sm.spl[j] = sorted[(i64)j * stride];
@@ -91,13 +93,13 @@ enum_kernel(const u64 *__restrict__ str, const u64 *__restrict__ sorted, const i
     const unsigned lt = (1u << lane) - 1;
     uint8_t *occ = sm.occ[w], *virt = sm.virt[w];
     for (i64 i = (i64)blockIdx.x * kWarpsPerBlock + w; i < n; i += (i64)gridDim.x * kWarpsPerBlock) {
-        const u64 s = str[i];
+        const W s = str[i];
         // occupied / virtual orbital lists in ascending order
         for (int base = 0; base < norb; base += 32) {
             int o = base + lane;
-            bool in = o < norb, occd = in && ((s >> o) & 1);
+            bool in = o < norb, occd = in && words::test(s, o);
             unsigned mo = __ballot_sync(0xffffffffu, occd), mv = __ballot_sync(0xffffffffu, in && !occd);
-            int before_o = __popcll(s & ((1ull << base) - 1));
+            int before_o = words::popc_below(s, base);
             int before_v = base - before_o;
             if (occd) occ[before_o + __popc(mo & lt)] = (uint8_t)o;
             if (in && !occd) virt[before_v + __popc(mv & lt)] = (uint8_t)o;
@@ -112,7 +114,7 @@ enum_kernel(const u64 *__restrict__ str, const u64 *__restrict__ sorted, const i
             if (c < ts) {
                 p = occ[c / nv];
                 r = virt[c % nv];
-                pos = lookup(sm, nspl, stride, sorted, n, (s & ~(1ull << p)) | (1ull << r));
+                pos = lookup(sm, nspl, stride, sorted, n, words::move(s, p, r));
             }
             unsigned m = __ballot_sync(0xffffffffu, pos >= 0);
             if (FILL && pos >= 0) {
@@ -129,15 +131,15 @@ enum_kernel(const u64 *__restrict__ str, const u64 *__restrict__ sorted, const i
         for (i64 base = 0; base < td; base += 32) {
             i64 c = base + lane;
             int pos = -1, p = 0, q = 0, r = 0, t = 0;
-            u64 mid = 0;
+            W mid{};
             if (c < td) {
                 uint16_t hp = sm.hole_pairs[c / nvp], vp = sm.virt_pairs[c % nvp];
                 p = occ[hp & 0xFF];
                 q = occ[hp >> 8];
                 r = virt[vp & 0xFF];
                 t = virt[vp >> 8];
-                mid = (s & ~(1ull << p)) | (1ull << r);
-                pos = lookup(sm, nspl, stride, sorted, n, (mid & ~(1ull << q)) | (1ull << t));
+                mid = words::move(s, p, r);
+                pos = lookup(sm, nspl, stride, sorted, n, words::move(mid, q, t));
             }
             unsigned m = __ballot_sync(0xffffffffu, pos >= 0);
             if (FILL && pos >= 0) {
@@ -504,7 +506,10 @@ static int build_sell(sbd_ctx *ctx, Sector &s) {
     return SBD_OK;
 }
 
-int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s) {
+namespace {
+
+template <class W>
+int build_tables(sbd_ctx *ctx, Sector &s, int norb) {
     const i64 n = s.n;
     cudaStream_t st = ctx->stream;
     SBD_CUDA(ctx, s.s_off.ensure(sizeof(int64_t) * (n + 1)));
@@ -520,12 +525,12 @@ int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s) {
     DevBuf cs, cd;
     SBD_CUDA(ctx, cs.ensure(sizeof(int64_t) * n));
     SBD_CUDA(ctx, cd.ensure(sizeof(int64_t) * n));
-    size_t smem = sizeof(EnumSmem);
-    SBD_CUDA(ctx, cudaFuncSetAttribute(enum_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    SBD_CUDA(ctx, cudaFuncSetAttribute(enum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    size_t smem = sizeof(EnumSmem<W>);
+    SBD_CUDA(ctx, cudaFuncSetAttribute(enum_kernel<false, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SBD_CUDA(ctx, cudaFuncSetAttribute(enum_kernel<true, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     unsigned blocks = (unsigned)std::min<i64>((n + kWarpsPerBlock - 1) / kWarpsPerBlock, (i64)ctx->num_sms * 8);
-    enum_kernel<false><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
-        s.str.as<u64>(), s.sorted.as<u64>(), s.perm.as<int32_t>(), n, ctx->norb, s.n_elec, stride, nspl,
+    enum_kernel<false, W><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
+        s.str.as<W>(), s.sorted.as<W>(), s.perm.as<int32_t>(), n, norb, s.n_elec, stride, nspl,
         cs.as<int64_t>(), cd.as<int64_t>(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
         nullptr, nullptr, nullptr, nullptr);
     SBD_LAUNCHED(ctx, "enum count");
@@ -549,8 +554,8 @@ int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s) {
     SBD_CUDA(ctx, s.d_p1.ensure(sizeof(int16_t) * (s.nd + 1)));
     SBD_CUDA(ctx, s.d_p2.ensure(sizeof(int16_t) * (s.nd + 1)));
     SBD_CUDA(ctx, s.d_phase.ensure(sizeof(int8_t) * (s.nd + 1)));
-    enum_kernel<true><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
-        s.str.as<u64>(), s.sorted.as<u64>(), s.perm.as<int32_t>(), n, ctx->norb, s.n_elec, stride, nspl, nullptr,
+    enum_kernel<true, W><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
+        s.str.as<W>(), s.sorted.as<W>(), s.perm.as<int32_t>(), n, norb, s.n_elec, stride, nspl, nullptr,
         nullptr, s.s_off.as<int64_t>(), s.d_off.as<int64_t>(), s.s_tgt.as<int32_t>(), s.s_hole.as<int16_t>(),
         s.s_part.as<int16_t>(), s.s_phase.as<int8_t>(), s.d_tgt.as<int32_t>(), s.d_h1.as<int16_t>(),
         s.d_h2.as<int16_t>(), s.d_p1.as<int16_t>(), s.d_p2.as<int16_t>(), s.d_phase.as<int8_t>());
@@ -558,6 +563,12 @@ int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s) {
     SBD_CUDA(ctx, cudaStreamSynchronize(st));
     return SBD_OK;
 }
+
+}  // namespace
+
+int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s) { return build_tables<u64>(ctx, s, ctx->norb); }
+
+int sbd_build_sector_tables128(sbd_ctx *ctx, Sector &s, int norb) { return build_tables<U128>(ctx, s, norb); }
 
 int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other) {
     (void)other;

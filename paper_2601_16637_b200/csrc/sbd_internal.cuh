@@ -175,6 +175,10 @@ struct sbd_ctx {
     cudaStream_t aux_stream = nullptr;    // dense-set DGEMMs, concurrent with the streams
     cudaEvent_t aux_ev[2] = {nullptr, nullptr};
     DevBuf ssg_z;                         // their result, added after the alpha side
+    // 128-bit string list (norb <= 128): configuration processing + excitation tables only
+    // (sbd_table128_*; U128 words in str/sorted)
+    Sector t128;
+    int t128_norb = 0;
 
     i64 own_lo() const { return row_lo; }
     i64 own_hi() const { return row_hi < 0 ? sec[0].n : row_hi; }
@@ -221,6 +225,8 @@ int sbd_cuda_fail(sbd_ctx *ctx, cudaError_t e, const char *where);
 // cross-TU entry points
 int sbd_sort_strings(sbd_ctx *ctx, Sector &s);              // sbd_strings.cu
 int sbd_build_sector_tables(sbd_ctx *ctx, Sector &s);       // sbd_excite.cu
+int sbd_sort_strings128(sbd_ctx *ctx, Sector &s, int norb);             // sbd_strings.cu
+int sbd_build_sector_tables128(sbd_ctx *ctx, Sector &s, int norb);      // sbd_excite.cu
 int sbd_build_coefficients(sbd_ctx *ctx, Sector &s, const Sector &other);  // sbd_excite.cu
 // LSD radix sort of n u64 keys (low key_bits significant) with the sort permutation (sbd_strings.cu)
 int sbd_radix_sort(sbd_ctx *ctx, const u64 *keys, i64 n, int key_bits, DevBuf &sorted, DevBuf &perm);

@@ -11,21 +11,25 @@
 // Sort: 8-bit LSD digits, only ceil(norb/8) passes (bits >= norb are zero).
 // Per pass: tile histogram -> digit-major exclusive scan -> stable scatter
 // (warp match_any ranking + per-warp digit prefix), tiles of 1024 keys.
+// Keys are one word (u64) or two (U128, norb <= 128: the digit passes walk
+// the low word, then the high one).
 #include <algorithm>
 
 #include "sbd_internal.cuh"
+#include "sbd_words.cuh"
 
 namespace {
 
 constexpr int kTile = 1024;  // keys per block == threads per block
 constexpr int kWarps = kTile / 32;
 
-__global__ void radix_hist(const u64 *__restrict__ keys, i64 n, int shift, int *__restrict__ hist, int nblocks) {
+template <class W>
+__global__ void radix_hist(const W *__restrict__ keys, i64 n, int shift, int *__restrict__ hist, int nblocks) {
     __shared__ int h[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
     __syncthreads();
     i64 i = (i64)blockIdx.x * kTile + threadIdx.x;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xFF], 1);
+    if (i < n) atomicAdd(&h[words::digit(keys[i], shift)], 1);
     __syncthreads();
     for (int d = threadIdx.x; d < 256; d += blockDim.x) hist[d * nblocks + blockIdx.x] = h[d];
 }
@@ -57,7 +61,8 @@ __global__ void exclusive_scan_small(int *__restrict__ a, int m) {
     }
 }
 
-__global__ void radix_scatter(const u64 *__restrict__ kin, const int32_t *__restrict__ vin, u64 *__restrict__ kout,
+template <class W>
+__global__ void radix_scatter(const W *__restrict__ kin, const int32_t *__restrict__ vin, W *__restrict__ kout,
                               int32_t *__restrict__ vout, i64 n, int shift, const int *__restrict__ offs,
                               int nblocks) {
     __shared__ int cnt[kWarps][256];
@@ -66,8 +71,9 @@ __global__ void radix_scatter(const u64 *__restrict__ kin, const int32_t *__rest
     __syncthreads();
     i64 i = (i64)blockIdx.x * kTile + t;
     bool valid = i < n;
-    u64 key = valid ? kin[i] : 0;
-    int d = valid ? (int)((key >> shift) & 0xFF) : 256 + lane;  // invalid lanes never match valid ones
+    W key{};
+    if (valid) key = kin[i];
+    int d = valid ? words::digit(key, shift) : 256 + lane;  // invalid lanes never match valid ones
     unsigned peers = __match_any_sync(0xffffffffu, d);
     int rank = __popc(peers & ((1u << lane) - 1));
     if (valid && rank == 0) cnt[w][d] = __popc(peers);
@@ -89,34 +95,34 @@ __global__ void radix_scatter(const u64 *__restrict__ kin, const int32_t *__rest
     }
 }
 
-__global__ void count_adjacent_dups(const u64 *__restrict__ sorted, i64 n, int *__restrict__ flag) {
+template <class W>
+__global__ void count_adjacent_dups(const W *__restrict__ sorted, i64 n, int *__restrict__ flag) {
     i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x + 1;
     if (i < n && sorted[i] == sorted[i - 1]) atomicAdd(flag, 1);
 }
 
-}  // namespace
-
-int sbd_radix_sort(sbd_ctx *ctx, const u64 *keys, i64 n, int key_bits, DevBuf &sorted, DevBuf &perm) {
+template <class W>
+int radix_sort(sbd_ctx *ctx, const W *keys, i64 n, int key_bits, DevBuf &sorted, DevBuf &perm) {
     cudaStream_t st = ctx->stream;
-    SBD_CUDA(ctx, sorted.ensure(sizeof(u64) * (n ? n : 1)));
+    SBD_CUDA(ctx, sorted.ensure(sizeof(W) * (n ? n : 1)));
     SBD_CUDA(ctx, perm.ensure(sizeof(int32_t) * (n ? n : 1)));
     if (n == 0) return SBD_OK;
     const int nblocks = (int)((n + kTile - 1) / kTile);
     DevBuf k2, v2, hist;
-    SBD_CUDA(ctx, k2.ensure(sizeof(u64) * n));
+    SBD_CUDA(ctx, k2.ensure(sizeof(W) * n));
     SBD_CUDA(ctx, v2.ensure(sizeof(int32_t) * n));
     SBD_CUDA(ctx, hist.ensure(sizeof(int) * 256 * nblocks + 64));
     const int passes = std::max(1, (key_bits + 7) / 8);
     // ping-pong from caller order with identity values; the LAST pass lands in sorted/perm
-    const u64 *kin = keys;
+    const W *kin = keys;
     const int32_t *vin = nullptr;
-    u64 *bufk[2] = {sorted.as<u64>(), k2.as<u64>()};
+    W *bufk[2] = {sorted.as<W>(), k2.as<W>()};
     int32_t *bufv[2] = {perm.as<int32_t>(), v2.as<int32_t>()};
     int cur = (passes % 2 == 1) ? 0 : 1;
     for (int p = 0; p < passes; ++p) {
-        radix_hist<<<nblocks, kTile, 0, st>>>(kin, n, 8 * p, hist.as<int>(), nblocks);
+        radix_hist<W><<<nblocks, kTile, 0, st>>>(kin, n, 8 * p, hist.as<int>(), nblocks);
         exclusive_scan_small<<<1, 1024, 0, st>>>(hist.as<int>(), 256 * nblocks);
-        radix_scatter<<<nblocks, kTile, 0, st>>>(kin, vin, bufk[cur], bufv[cur], n, 8 * p, hist.as<int>(), nblocks);
+        radix_scatter<W><<<nblocks, kTile, 0, st>>>(kin, vin, bufk[cur], bufv[cur], n, 8 * p, hist.as<int>(), nblocks);
         SBD_LAUNCHED(ctx, "radix sort");
         kin = bufk[cur];
         vin = bufv[cur];
@@ -125,15 +131,16 @@ int sbd_radix_sort(sbd_ctx *ctx, const u64 *keys, i64 n, int key_bits, DevBuf &s
     return SBD_OK;
 }
 
-int sbd_sort_strings(sbd_ctx *ctx, Sector &s) {
+template <class W>
+int sort_strings(sbd_ctx *ctx, Sector &s, int norb) {
     const i64 n = s.n;
     cudaStream_t st = ctx->stream;
-    int rc = sbd_radix_sort(ctx, s.str.as<u64>(), n, ctx->norb, s.sorted, s.perm);
+    int rc = radix_sort<W>(ctx, s.str.as<W>(), n, norb, s.sorted, s.perm);
     if (rc || n == 0) return rc;
     DevBuf flag;
     SBD_CUDA(ctx, flag.ensure(sizeof(int)));
     SBD_CUDA(ctx, cudaMemsetAsync(flag.p, 0, sizeof(int), st));
-    count_adjacent_dups<<<grid_for(n, 256), 256, 0, st>>>(s.sorted.as<u64>(), n, flag.as<int>());
+    count_adjacent_dups<W><<<grid_for(n, 256), 256, 0, st>>>(s.sorted.as<W>(), n, flag.as<int>());
     SBD_LAUNCHED(ctx, "dup check");
     int dups = 0;
     SBD_CUDA(ctx, cudaMemcpyAsync(&dups, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -141,3 +148,13 @@ int sbd_sort_strings(sbd_ctx *ctx, Sector &s) {
     if (dups) return sbd_fail(ctx, SBD_EINVAL, "strings must be deduplicated");
     return SBD_OK;
 }
+
+}  // namespace
+
+int sbd_radix_sort(sbd_ctx *ctx, const u64 *keys, i64 n, int key_bits, DevBuf &sorted, DevBuf &perm) {
+    return radix_sort<u64>(ctx, keys, n, key_bits, sorted, perm);
+}
+
+int sbd_sort_strings(sbd_ctx *ctx, Sector &s) { return sort_strings<u64>(ctx, s, ctx->norb); }
+
+int sbd_sort_strings128(sbd_ctx *ctx, Sector &s, int norb) { return sort_strings<U128>(ctx, s, norb); }

@@ -37,6 +37,17 @@ def explicit_meta():
 
 
 @pytest.fixture(scope="session")
+def table128_golden():
+    """Reference build_excitation_table on norb 65..128 string lists (make_golden.py table128)."""
+    with open(os.path.join(GOLDEN, "table128_meta.json")) as f:
+        meta = json.load(f)
+    return meta, dict(np.load(os.path.join(GOLDEN, "table128.npz")))
+
+
+TABLE128_CASES = ("w72_e4", "w100_e3", "w128_e2_all", "w128_e5", "w128_e127", "w128_e126", "w65_e3")
+
+
+@pytest.fixture(scope="session")
 def small_meta():
     with open(os.path.join(GOLDEN, "small_meta.json")) as f:
         return json.load(f)

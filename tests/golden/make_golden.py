@@ -1,7 +1,7 @@
 """Generate golden fixtures by running the REFERENCE (sbdiag) in this container.
 
     PYTHONPATH=/root/reference/pkg/src:/root/reference/pkg/tests \
-    NUMBA_CACHE_DIR=/tmp/nc python tests/golden/make_golden.py small cfg1 cfg2 [cfg1-davidson] [cfg4]
+    NUMBA_CACHE_DIR=/tmp/nc python tests/golden/make_golden.py small cfg1 cfg2 [cfg1-davidson] [cfg4] [table128]
 
 The reference is not present on the GPU box, so its outputs are committed as
 small fixtures here: full arrays for the small instances, and for cfg1/cfg2/
@@ -324,8 +324,88 @@ def make_cli():
         json.dump(out, f, indent=1, sort_keys=True)
 
 
+def _walk_strings(rng, norb, ne, n, seeds, window):
+    """A connected in-set string list for norb > 64: random single/double moves from seed strings,
+    orbitals drawn from `window` (so the set has many in-set excitations), caller order = discovery order."""
+    window = list(window)
+    out, seen = [], set()
+    for s in seeds:
+        assert bin(s).count("1") == ne and s not in seen
+        out.append(s)
+        seen.add(s)
+    while len(out) < n:
+        s = out[int(rng.integers(len(out)))]
+        occ = [p for p in window if (s >> p) & 1]
+        virt = [p for p in window if not (s >> p) & 1]
+        k = 1 if (len(occ) < 2 or len(virt) < 2 or rng.random() < 0.5) else 2
+        if not occ or not virt:
+            continue
+        holes = rng.choice(occ, size=min(k, len(occ)), replace=False)
+        parts = rng.choice(virt, size=len(holes), replace=False)
+        t = s
+        for p, r in zip(holes, parts):
+            t = (t & ~(1 << int(p))) | (1 << int(r))
+        if t not in seen:
+            seen.add(t)
+            out.append(t)
+    return out
+
+
+def _mask(orbs):
+    m = 0
+    for o in orbs:
+        m |= 1 << o
+    return m
+
+
+# name, norb, n_elec, string-list builder (rng -> list of Python ints)
+TABLE128_CASES = [
+    # electrons straddling the 64-bit word boundary
+    ("w72_e4", 72, 4, lambda rng: _walk_strings(rng, 72, 4, 300, [_mask([60, 62, 64, 66])], range(52, 72))),
+    ("w100_e3", 100, 3, lambda rng: _walk_strings(rng, 100, 3, 200, [_mask([1, 63, 99]), _mask([62, 64, 65])],
+                                                  list(range(0, 4)) + list(range(58, 70)) + list(range(95, 100)))),
+    # every string of 2 electrons in 24 orbitals around bit 64 and at the top (bit 127)
+    ("w128_e2_all", 128, 2, lambda rng: [a | b for a, b in (
+        (1 << i, 1 << j) for i, j in __import__("itertools").combinations(list(range(56, 72)) + list(range(120, 128)), 2))]),
+    ("w128_e5", 128, 5, lambda rng: _walk_strings(rng, 128, 5, 100, [_mask([0, 63, 64, 100, 127])],
+                                                  list(range(0, 3)) + list(range(61, 67)) + list(range(124, 128)))),
+    # one hole: nv = 1 (no doubles), 8001 hole pairs
+    ("w128_e127", 128, 127, lambda rng: [((1 << 128) - 1) & ~(1 << h) for h in rng.permutation(128).tolist()]),
+    # two holes inside a 24-orbital window: 7875 hole pairs, 1 particle pair
+    ("w128_e126", 128, 126, lambda rng: [((1 << 128) - 1) & ~((1 << i) | (1 << j)) for i, j in
+                                         __import__("itertools").combinations(list(range(52, 70)) + list(range(122, 128)), 2)]),
+    # 65 orbitals, the smallest two-word case
+    ("w65_e3", 65, 3, lambda rng: _walk_strings(rng, 65, 3, 250, [_mask([0, 32, 64])], range(65))),
+]
+
+
+def make_table128():
+    """Reference build_excitation_table (basis.py:362-403) on norb > 64 string lists.
+
+    The reference caps norb at 64 for integrals (integrals.py:67-68), but its table builder works on
+    Python ints of any width; these fixtures pin the 128-bit table path to it.  Strings are stored as
+    (lo, hi) uint64 word pairs."""
+    rng = np.random.default_rng(128)
+    out, meta = {}, {}
+    for name, norb, ne, make in TABLE128_CASES:
+        strings = [int(s) for s in make(rng)]
+        assert len(set(strings)) == len(strings) and all(bin(s).count("1") == ne for s in strings)
+        t0 = time.perf_counter()
+        tab = build_excitation_table(strings, norb)
+        out[f"{name}/words"] = np.array([[s & (2**64 - 1), s >> 64] for s in strings], dtype=np.uint64)
+        for f in FIELDS:
+            out[f"{name}/{f}"] = np.asarray(getattr(tab, f), dtype=DTYPES[f])
+        meta[name] = dict(norb=norb, n_elec=ne, n_strings=len(strings), n_singles=int(tab.s_off[-1]),
+                          n_doubles=int(tab.d_off[-1]))
+        print(name, meta[name], f"{time.perf_counter() - t0:.1f}s", flush=True)
+    np.savez_compressed(os.path.join(HERE, "table128.npz"), **out)
+    with open(os.path.join(HERE, "table128_meta.json"), "w") as f:
+        json.dump(meta, f, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     jobs = dict(small=make_small, cli=make_cli, ingest=make_ingest, cfg1=make_cfg1, cfg2=make_cfg2, cfg4=make_cfg4, explicit=make_explicit,
+                table128=make_table128,
                 **{"cfg1-davidson": make_cfg1_davidson})
     for arg in sys.argv[1:]:
         jobs[arg]()
