@@ -190,9 +190,12 @@ def build_spin_tables(basis: SelectedBasis, device=None) -> SpinTables:
     """Both sectors' tables (reference ``apply.py:557-563``), built on the GPU."""
     if basis.mode != "product":
         raise ValueError("spin-sector tables apply to product-mode bases only")
+    wide = basis.norb > 64  # two-word strings: tables only (build_excitation_table128)
     return SpinTables(
-        alpha=build_excitation_table(basis.alpha_array(), basis.norb, basis.n_alpha_elec, device),
-        beta=build_excitation_table(basis.beta_array(), basis.norb, basis.n_beta_elec, device),
+        alpha=build_excitation_table(basis.alpha_strings if wide else basis.alpha_array(), basis.norb,
+                                     basis.n_alpha_elec, device),
+        beta=build_excitation_table(basis.beta_strings if wide else basis.beta_array(), basis.norb,
+                                    basis.n_beta_elec, device),
     )
 
 

@@ -201,6 +201,8 @@ def parse_sample_lines(lines: Union[str, Iterable[str]], norb: int):
     orbital 0 of alpha; blank lines and '#' comments skipped; the first
     malformed line raises SampleFormatError with its 1-based line number.
     """
+    if not 1 <= norb <= 64:
+        raise ValueError(f"sample ingestion takes norb in [1, 64] (one-word strings), got {norb}")
     if isinstance(lines, str):
         lines = lines.splitlines()
     kept, nos = [], []

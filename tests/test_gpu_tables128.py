@@ -140,3 +140,15 @@ def test_table128_rejects_bad_input():
         build_excitation_table128([1], 129)
     empty = build_excitation_table128([], 100, 3)
     assert empty.n_strings == 0 and empty.s_off.tolist() == [0] and empty.d_off.tolist() == [0]
+
+
+def test_build_spin_tables_wide_product_basis():
+    """build_spin_tables (reference apply.py:557-563) on a product basis of 100 orbitals."""
+    from paper_2601_16637_b200 import SelectedBasis, build_spin_tables
+
+    rng = np.random.default_rng(100)
+    a = _walk(rng, 100, 5, 700, list(range(60, 72)) + list(range(94, 100)))
+    b = _walk(rng, 100, 3, 400, list(range(0, 6)) + list(range(62, 70)))
+    tabs = build_spin_tables(SelectedBasis.product(a, b, 100, 5, 3))
+    _assert_tables_equal(tabs.alpha, O.build_table128(a, 100), "alpha")
+    _assert_tables_equal(tabs.beta, O.build_table128(b, 100), "beta")

@@ -97,6 +97,8 @@ def test_sample_line_parser():
         parse_sample_lines(["11000011", "11002011", "110"], 4)  # the earlier line's error wins
     with pytest.raises(SampleFormatError, match="line 1"):
         parse_sample_lines(["1100001\u00e9"], 4)
+    with pytest.raises(ValueError, match="norb in \\[1, 64\\]"):
+        parse_sample_lines(["0" * 140], 70)  # wide strings: tables only (build_excitation_table128)
 
 
 def test_host_enumerators_match_golden(small_golden):
