@@ -26,6 +26,9 @@ def _assert_tables_equal(tab, ref, label=""):
 
 def _walk(rng, norb, ne, n, window):
     """Connected random string set: single/double moves inside `window`, discovery order."""
+    from math import comb
+
+    assert comb(len(window), ne) >= n, "window too small for n distinct strings"
     window = np.asarray(window)
     start = 0
     for o in rng.choice(window, size=ne, replace=False):
@@ -148,7 +151,7 @@ def test_build_spin_tables_wide_product_basis():
 
     rng = np.random.default_rng(100)
     a = _walk(rng, 100, 5, 700, list(range(60, 72)) + list(range(94, 100)))
-    b = _walk(rng, 100, 3, 400, list(range(0, 6)) + list(range(62, 70)))
+    b = _walk(rng, 100, 3, 400, list(range(0, 8)) + list(range(60, 70)))  # C(18, 3) = 816 >= 400
     tabs = build_spin_tables(SelectedBasis.product(a, b, 100, 5, 3))
     _assert_tables_equal(tabs.alpha, O.build_table128(a, 100), "alpha")
     _assert_tables_equal(tabs.beta, O.build_table128(b, 100), "beta")
