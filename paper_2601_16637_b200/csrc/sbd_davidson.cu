@@ -1315,6 +1315,170 @@ residual_reg(const double *__restrict__ V, const double *__restrict__ W, int k, 
     block_store_partials<K, S, 1 + M>(acc, xs, partial, K + 1 + M);
 }
 
+// Residual pass streamed through shared memory (the default for k <= 16, m <= 4).
+// One CTA per SM walks tiles of 256 elements.  A producer warp bulk-copies (cp.async.bulk)
+// each tile's 2k+1 slices (k V, k W, diag; 2 KB each) into one of NS stages, NS sized so the
+// stages hold ~210 KB (k = 5: 8 stages of 22 KB; k = 16: 3 of 66 KB), i.e. NS-1 tiles in
+// flight per SM while the consumers compute one.  Consumers (8 warps) take one element per
+// thread, release a stage per warp on its `empty` mbarrier (no CTA-wide barrier per tile),
+// and read the V^T t_jp projections' V from the stage instead of re-reading it.
+// Measured per k at 1e8 elements (profiles/r4f/ab_residual.log): 6.7-7.0 TB/s for k = 8-16
+// where the register pass with one lane per pair reaches 4.2-6.3.  Above k = 16 the register
+// pass with two lanes per pair reaches 6.1-6.5 TB/s and stays the default: a two-threads-per-
+// element form of this kernel (128-element tiles, 1 KB bulk copies) ran at 4.4-4.6.
+// partial per block (stride K+1+M): [0,K) dots | K: |t_jp|^2 | K+1+j: |r_j|^2
+constexpr int kResConsumers = 256;
+constexpr int kResThreads = kResConsumers + 32;  // + the producer warp
+constexpr int kResTile = kResConsumers;          // elements per tile: one per consumer thread
+constexpr int kResMaxStages = 8;
+constexpr int kResStreamMaxK = 16;
+constexpr size_t kResStageBudget = 210 * 1024;
+
+inline int res_stream_stages(int k) {
+    const size_t stage = sizeof(double) * (size_t)(2 * k + 1) * kResTile;
+    return (int)std::max<size_t>(2, std::min<size_t>(kResMaxStages, kResStageBudget / stage));
+}
+inline size_t res_stream_smem(int k) {
+    return 256 + sizeof(double) * (size_t)res_stream_stages(k) * (size_t)(2 * k + 1) * kResTile;
+}
+
+__device__ __forceinline__ void consumers_sync() {  // named barrier 1 over the consumer warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(kResConsumers) : "memory");
+}
+
+template <int K, int M>
+__global__ void __launch_bounds__(kResThreads, 1)
+residual_stream(const double *__restrict__ V, const double *__restrict__ W, int k, i64 ldv, i64 n,
+                const double *__restrict__ Y, const double *__restrict__ theta, int m, int jp,
+                const double *__restrict__ diag, double delta, double *__restrict__ T, i64 ldt,
+                double *__restrict__ partial, int ns) {
+    constexpr int TT = kResTile;
+    constexpr int NW = kResConsumers / 32;
+    extern __shared__ __align__(128) unsigned char rss[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(rss), *empty = full + kResMaxStages;
+    double *stage0 = reinterpret_cast<double *>(rss + 256);
+    __shared__ double ys[K * M];
+    __shared__ double th[M];
+    __shared__ double red[NW][K + 1 + M];
+    const i64 sstride = (i64)(2 * k + 1) * TT;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    for (int idx = t; idx < K * M; idx += kResThreads) {
+        const int i = idx / M, j = idx % M;
+        ys[idx] = (i < k && j < m) ? Y[i * m + j] : 0.0;
+    }
+    if (t < M) th[t] = t < m ? theta[t] : 0.0;
+    if (t == 0) {
+        for (int s = 0; s < ns; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const i64 ntiles = (n + TT - 1) / TT;
+    if (warp == NW) {  // producer
+        if (lane == 0) {
+            int it = 0;
+            for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+                const int s = it % ns;
+                if (it >= ns) mbar_wait(&empty[s], (uint32_t)(((it / ns) - 1) & 1));
+                const i64 base = tile * TT, cnt = min((i64)TT, n - base);
+                const uint32_t b = bulk_bytes(cnt);
+                double *st = stage0 + s * sstride;
+                mbar_arrive_expect_tx(&full[s], b * (uint32_t)(2 * k + 1));
+                if (b) {
+                    for (int i = 0; i < k; ++i) {
+                        tma_load_1d(st + (i64)i * TT, V + i * ldv + base, b, &full[s]);
+                        tma_load_1d(st + (i64)(k + i) * TT, W + i * ldv + base, b, &full[s]);
+                    }
+                    tma_load_1d(st + (i64)(2 * k) * TT, diag + base, b, &full[s]);
+                }
+            }
+        }
+        return;
+    }
+    const int e = t;
+    double acc[K], rn2[M], tn2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < K; ++q) acc[q] = 0.0;
+#pragma unroll
+    for (int j = 0; j < M; ++j) rn2[j] = 0.0;
+    int it = 0;
+    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int s = it % ns;
+        const i64 base = tile * TT, cnt = min((i64)TT, n - base);
+        double *st = stage0 + s * sstride;
+        mbar_wait(&full[s], (uint32_t)((it / ns) & 1));
+        if (cnt & 1) {  // odd last element: plain loads (bulk copies move 16-byte multiples)
+            if (t == 0) {
+                const i64 q = cnt - 1;
+                for (int i = 0; i < k; ++i) {
+                    st[(i64)i * TT + q] = V[i * ldv + base + q];
+                    st[(i64)(k + i) * TT + q] = W[i * ldv + base + q];
+                }
+                st[(i64)(2 * k) * TT + q] = diag[base + q];
+                fence_proxy_async_smem();  // before the stage can be refilled by bulk copies
+            }
+            consumers_sync();
+        }
+        double u[M], wy[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) u[j] = wy[j] = 0.0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            if (i < k) {
+                const double v = st[(i64)i * TT + e], w = st[(i64)(k + i) * TT + e];
+#pragma unroll
+                for (int j = 0; j < M; ++j) {
+                    const double y = ys[i * M + j];
+                    u[j] = fma(y, v, u[j]);
+                    wy[j] = fma(y, w, wy[j]);
+                }
+            }
+        }
+        if (e < cnt) {
+            const double d = st[(i64)(2 * k) * TT + e];
+            double tj = 0.0;
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+                if (j < m) {
+                    const double r = wy[j] - th[j] * u[j];
+                    const double tv = precond_div(r, d, th[j], delta);
+                    __stcs(T + j * ldt + base + e, tv);
+                    rn2[j] = fma(r, r, rn2[j]);
+                    if (j == jp) tj = tv;
+                }
+            }
+            tn2 = fma(tj, tj, tn2);
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+                if (i < k) acc[i] = fma(st[(i64)i * TT + e], tj, acc[i]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
+    }
+    // block reduction over the consumer warps
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const double v = warp_sum(acc[i]);
+        if (lane == 0) red[warp][i] = v;
+    }
+    tn2 = warp_sum(tn2);
+#pragma unroll
+    for (int j = 0; j < M; ++j) rn2[j] = warp_sum(rn2[j]);
+    if (lane == 0) {
+        red[warp][K] = tn2;
+#pragma unroll
+        for (int j = 0; j < M; ++j) red[warp][K + 1 + j] = rn2[j];
+    }
+    consumers_sync();
+    for (int i = t; i < K + 1 + M; i += kResConsumers) {
+        double sum = 0.0;
+        for (int w = 0; w < NW; ++w) sum += red[w][i];
+        partial[(i64)blockIdx.x * (K + 1 + M) + i] = (i < K && i >= k) ? 0.0 : sum;
+    }
+}
+
 // t_new = t - V c ; out = scale * t_new (out may alias t) ; dots V_i . t_new (i < kdot) ; |t_new|^2
 // partial per block (stride K+1): [0,K) dots | K: |t_new|^2 ; S threads per element pair.
 template <int K, bool DOTS, int S>
@@ -1466,6 +1630,11 @@ inline bool use_reg() {
     return !(e && *e == '1');
 }
 
+inline bool use_res_stream() {  // SBD_RES_STREAM=0: the register-staged residual pass (A/B, tests)
+    const char *e = getenv("SBD_RES_STREAM");
+    return !(e && *e == '0');
+}
+
 // lanes per element pair for pass `which` (0 residual, 1 CGS); SBD_RES_SPLIT / SBD_GS_SPLIT
 // override the default for A/B measurements
 inline int split_lanes(int which, int dflt) {
@@ -1546,6 +1715,17 @@ struct ResidL {
     static std::pair<int, int> launch(sbd_ctx *ctx, int nb, const double *V, const double *W, int k, i64 ldv, i64 n,
                                       const double *Y, const double *theta, int m, int jp, const double *diag,
                                       double delta, double *T, i64 ldt) {
+        if (K <= kResStreamMaxK && M <= kRegMaxRoots && vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 &&
+            use_reg() && use_res_stream()) {
+            constexpr int KS = K <= kResStreamMaxK ? K : kResStreamMaxK;
+            const size_t smem = res_stream_smem(k);
+            const int nt = (int)std::max<i64>(1, std::min<i64>((n + kResTile - 1) / kResTile, ctx->num_sms));
+            (void)sbd_smem_attr((const void *)residual_stream<KS, M>, ctx->device, smem);  // launch errors surface below
+            residual_stream<KS, M><<<nt, kResThreads, smem, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag,
+                                                                          delta, T, ldt, ctx->red.as<double>(),
+                                                                          res_stream_stages(k));
+            return {nt, K + 1 + M};
+        }
         if (K <= 32 && M <= kRegMaxRoots && vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_reg()) {
             const int nt = ctx->num_sms * 2;
             constexpr int KR = K <= 32 ? K : 32;

@@ -3,7 +3,8 @@
 The passes (csrc/sbd_davidson.cu) pick a kernel by subspace size, alignment
 and three knobs read per launch (register passes for k <= 32, TMA-staged
 passes for k > 32 or SBD_DAV_TMA=1, tile/generic passes with SBD_NO_TMA=1 or
-unaligned vectors; lane splits SBD_RES_SPLIT / SBD_GS_SPLIT and L2 prefetch
+unaligned vectors; the streamed residual pass, or the register one with
+SBD_RES_STREAM=0; lane splits SBD_RES_SPLIT / SBD_GS_SPLIT and L2 prefetch
 SBD_RES_PF / SBD_GS_PF).  Each is checked here against a float64 numpy
 restatement of the reference step it fuses (davidson.py:159-185,248-289).
 The sigma variants (SBD_SIDE_LDG, SBD_YT_BLOCKED, SBD_CROSS_NO_CLUSTER,
@@ -24,10 +25,11 @@ VARIANTS = [
     {},
     {"SBD_DAV_TMA": "1"},
     {"SBD_NO_TMA": "1"},
-    {"SBD_RES_SPLIT": "1", "SBD_GS_SPLIT": "1"},
-    {"SBD_RES_SPLIT": "2", "SBD_GS_SPLIT": "2"},
-    {"SBD_RES_SPLIT": "4"},
-    {"SBD_RES_PF": "1", "SBD_GS_PF": "1"},
+    {"SBD_RES_STREAM": "0"},
+    {"SBD_RES_SPLIT": "1", "SBD_GS_SPLIT": "1", "SBD_RES_STREAM": "0"},
+    {"SBD_RES_SPLIT": "2", "SBD_GS_SPLIT": "2", "SBD_RES_STREAM": "0"},
+    {"SBD_RES_SPLIT": "4", "SBD_RES_STREAM": "0"},
+    {"SBD_RES_PF": "1", "SBD_GS_PF": "1", "SBD_RES_STREAM": "0"},
     {"SBD_GS_PF": "0"},
 ]
 
@@ -69,7 +71,9 @@ def _np(t):
 
 @pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 @pytest.mark.parametrize("k,m,n,offset", [(1, 1, 1000, 0), (5, 2, 999, 0), (17, 3, 4097, 0), (24, 1, 3000, 0),
-                                          (32, 5, 2048, 0), (40, 2, 1500, 0), (64, 8, 1200, 0), (20, 2, 777, 1)])
+                                          (32, 5, 2048, 0), (40, 2, 1500, 0), (64, 8, 1200, 0), (20, 2, 777, 1),
+                                          # several tiles per CTA: the streamed residual's stage ring wraps
+                                          (16, 2, 300_001, 0), (12, 4, 200_003, 0), (3, 3, 1_000_001, 0)])
 def test_davidson_passes_match_numpy(env, k, m, n, offset, monkeypatch):
     import torch
 
