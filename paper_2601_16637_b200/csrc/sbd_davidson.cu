@@ -1315,45 +1315,46 @@ residual_reg(const double *__restrict__ V, const double *__restrict__ W, int k, 
     block_store_partials<K, S, 1 + M>(acc, xs, partial, K + 1 + M);
 }
 
-// Residual pass streamed through shared memory (the default for k <= 16, m <= 4).
-// One CTA per SM walks tiles of 256 elements.  A producer warp bulk-copies (cp.async.bulk)
-// each tile's 2k+1 slices (k V, k W, diag; 2 KB each) into one of NS stages, NS sized so the
-// stages hold ~210 KB (k = 5: 8 stages of 22 KB; k = 16: 3 of 66 KB), i.e. NS-1 tiles in
-// flight per SM while the consumers compute one.  Consumers (8 warps) take one element per
-// thread, release a stage per warp on its `empty` mbarrier (no CTA-wide barrier per tile),
-// and read the V^T t_jp projections' V from the stage instead of re-reading it.
-// Measured per k at 1e8 elements (profiles/r4f/ab_residual.log): 6.7-7.0 TB/s for k = 8-16
-// where the register pass with one lane per pair reaches 4.2-6.3.  Above k = 16 the register
-// pass with two lanes per pair reaches 6.1-6.5 TB/s and stays the default: a two-threads-per-
-// element form of this kernel (128-element tiles, 1 KB bulk copies) ran at 4.4-4.6.
+// Residual pass streamed through shared memory (the default for k <= 32, m <= 4).
+// One CTA per SM walks tiles of TT elements (256; 192 for K = 32).  A producer warp
+// bulk-copies (cp.async.bulk, the copies spread over its lanes) each tile's 2k+1 slices (k V,
+// k W, diag) into one of NS stages, NS sized so the stages hold ~210 KB (k = 5: 8 stages of
+// 22 KB; k = 16: 3 of 66 KB; k = 24-32: 2 of ~100 KB), i.e. NS-1 tiles in flight per SM
+// while the consumers compute one.  Consumers take one element per thread, release a stage
+// per warp on its `empty` mbarrier (no CTA-wide barrier per tile), and read the V^T t_jp
+// projections' V from the stage instead of re-reading it.
+// Measured per k at 1e8 elements against the register pass it replaced (profiles/r4j, r4k):
+// k = 4: 5.1 vs 4.7 TB/s, k = 8-24: 6.7-7.0 vs 4.2-6.3, k = 25-28: 6.2-6.6 vs 5.9-6.1,
+// k = 32: 6.1 vs 6.3; three roots k = 24/32: 6.4/5.9 vs 4.0/3.3.  A single issuing lane
+// (instead of the warp) made it clock-sensitive: 5.3-6.7 TB/s at k = 8 from box to box.
 // partial per block (stride K+1+M): [0,K) dots | K: |t_jp|^2 | K+1+j: |r_j|^2
-constexpr int kResConsumers = 256;
-constexpr int kResThreads = kResConsumers + 32;  // + the producer warp
-constexpr int kResTile = kResConsumers;          // elements per tile: one per consumer thread
+// elements per tile = consumer threads: 256, or 192 for K = 32 so that two stages of
+// 65 slices (97.5 KB each) fit in shared memory
+__host__ __device__ constexpr int res_stream_tile(int K) { return K <= 24 ? 256 : 192; }
 constexpr int kResMaxStages = 8;
-constexpr int kResStreamMaxK = 16;
+constexpr int kResStreamMaxK = 32;
 constexpr size_t kResStageBudget = 210 * 1024;
 
-inline int res_stream_stages(int k) {
-    const size_t stage = sizeof(double) * (size_t)(2 * k + 1) * kResTile;
+inline int res_stream_stages(int K, int k) {
+    const size_t stage = sizeof(double) * (size_t)(2 * k + 1) * res_stream_tile(K);
     return (int)std::max<size_t>(2, std::min<size_t>(kResMaxStages, kResStageBudget / stage));
 }
-inline size_t res_stream_smem(int k) {
-    return 256 + sizeof(double) * (size_t)res_stream_stages(k) * (size_t)(2 * k + 1) * kResTile;
+inline size_t res_stream_smem(int K, int k) {
+    return 256 + sizeof(double) * (size_t)res_stream_stages(K, k) * (size_t)(2 * k + 1) * res_stream_tile(K);
 }
 
+template <int NCONS>
 __device__ __forceinline__ void consumers_sync() {  // named barrier 1 over the consumer warps only
-    asm volatile("bar.sync 1, %0;" ::"n"(kResConsumers) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(NCONS) : "memory");
 }
 
 template <int K, int M>
-__global__ void __launch_bounds__(kResThreads, 1)
+__global__ void __launch_bounds__(res_stream_tile(K) + 32, 1)
 residual_stream(const double *__restrict__ V, const double *__restrict__ W, int k, i64 ldv, i64 n,
                 const double *__restrict__ Y, const double *__restrict__ theta, int m, int jp,
                 const double *__restrict__ diag, double delta, double *__restrict__ T, i64 ldt,
                 double *__restrict__ partial, int ns) {
-    constexpr int TT = kResTile;
-    constexpr int NW = kResConsumers / 32;
+    constexpr int TT = res_stream_tile(K), NW = TT / 32;  // + one producer warp
     extern __shared__ __align__(128) unsigned char rss[];
     uint64_t *full = reinterpret_cast<uint64_t *>(rss), *empty = full + kResMaxStages;
     double *stage0 = reinterpret_cast<double *>(rss + 256);
@@ -1362,7 +1363,7 @@ residual_stream(const double *__restrict__ V, const double *__restrict__ W, int 
     __shared__ double red[NW][K + 1 + M];
     const i64 sstride = (i64)(2 * k + 1) * TT;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    for (int idx = t; idx < K * M; idx += kResThreads) {
+    for (int idx = t; idx < K * M; idx += blockDim.x) {
         const int i = idx / M, j = idx % M;
         ys[idx] = (i < k && j < m) ? Y[i * m + j] : 0.0;
     }
@@ -1376,22 +1377,20 @@ residual_stream(const double *__restrict__ V, const double *__restrict__ W, int 
     }
     __syncthreads();
     const i64 ntiles = (n + TT - 1) / TT;
-    if (warp == NW) {  // producer
-        if (lane == 0) {
-            int it = 0;
-            for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-                const int s = it % ns;
-                if (it >= ns) mbar_wait(&empty[s], (uint32_t)(((it / ns) - 1) & 1));
-                const i64 base = tile * TT, cnt = min((i64)TT, n - base);
-                const uint32_t b = bulk_bytes(cnt);
-                double *st = stage0 + s * sstride;
-                mbar_arrive_expect_tx(&full[s], b * (uint32_t)(2 * k + 1));
-                if (b) {
-                    for (int i = 0; i < k; ++i) {
-                        tma_load_1d(st + (i64)i * TT, V + i * ldv + base, b, &full[s]);
-                        tma_load_1d(st + (i64)(k + i) * TT, W + i * ldv + base, b, &full[s]);
-                    }
-                    tma_load_1d(st + (i64)(2 * k) * TT, diag + base, b, &full[s]);
+    if (warp == NW) {  // producer warp: lane 0 arms the stage, the lanes issue its 2k+1 copies
+        int it = 0;
+        for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int s = it % ns;
+            if (it >= ns) mbar_wait(&empty[s], (uint32_t)(((it / ns) - 1) & 1));
+            const i64 base = tile * TT, cnt = min((i64)TT, n - base);
+            const uint32_t b = bulk_bytes(cnt);
+            double *st = stage0 + s * sstride;
+            if (lane == 0) mbar_arrive_expect_tx(&full[s], b * (uint32_t)(2 * k + 1));
+            __syncwarp();
+            if (b) {
+                for (int c = lane; c <= 2 * k; c += 32) {  // slice c: V_c, W_(c-k), diag
+                    const double *src = c < k ? V + c * ldv : (c < 2 * k ? W + (c - k) * ldv : diag);
+                    tma_load_1d(st + (i64)c * TT, src + base, b, &full[s]);
                 }
             }
         }
@@ -1419,7 +1418,7 @@ residual_stream(const double *__restrict__ V, const double *__restrict__ W, int 
                 st[(i64)(2 * k) * TT + q] = diag[base + q];
                 fence_proxy_async_smem();  // before the stage can be refilled by bulk copies
             }
-            consumers_sync();
+            consumers_sync<TT>();
         }
         double u[M], wy[M];
 #pragma unroll
@@ -1471,8 +1470,8 @@ residual_stream(const double *__restrict__ V, const double *__restrict__ W, int 
 #pragma unroll
         for (int j = 0; j < M; ++j) red[warp][K + 1 + j] = rn2[j];
     }
-    consumers_sync();
-    for (int i = t; i < K + 1 + M; i += kResConsumers) {
+    consumers_sync<TT>();
+    for (int i = t; i < K + 1 + M; i += TT) {
         double sum = 0.0;
         for (int w = 0; w < NW; ++w) sum += red[w][i];
         partial[(i64)blockIdx.x * (K + 1 + M) + i] = (i < K && i >= k) ? 0.0 : sum;
@@ -1715,15 +1714,16 @@ struct ResidL {
     static std::pair<int, int> launch(sbd_ctx *ctx, int nb, const double *V, const double *W, int k, i64 ldv, i64 n,
                                       const double *Y, const double *theta, int m, int jp, const double *diag,
                                       double delta, double *T, i64 ldt) {
-        if (K <= kResStreamMaxK && M <= kRegMaxRoots && vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 &&
-            use_reg() && use_res_stream()) {
+        if (K <= kResStreamMaxK && M <= kRegMaxRoots && vec_ok(V, ldv, W, diag, T) &&
+            ldt % 2 == 0 && use_reg() && use_res_stream()) {
             constexpr int KS = K <= kResStreamMaxK ? K : kResStreamMaxK;
-            const size_t smem = res_stream_smem(k);
-            const int nt = (int)std::max<i64>(1, std::min<i64>((n + kResTile - 1) / kResTile, ctx->num_sms));
+            constexpr int TT = res_stream_tile(KS);
+            const size_t smem = res_stream_smem(KS, k);
+            const int nt = (int)std::max<i64>(1, std::min<i64>((n + TT - 1) / TT, ctx->num_sms));
             (void)sbd_smem_attr((const void *)residual_stream<KS, M>, ctx->device, smem);  // launch errors surface below
-            residual_stream<KS, M><<<nt, kResThreads, smem, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag,
-                                                                          delta, T, ldt, ctx->red.as<double>(),
-                                                                          res_stream_stages(k));
+            residual_stream<KS, M><<<nt, TT + 32, smem, ctx->stream>>>(V, W, k, ldv, n, Y, theta, m, jp, diag,
+                                                                      delta, T, ldt, ctx->red.as<double>(),
+                                                                      res_stream_stages(KS, k));
             return {nt, K + 1 + M};
         }
         if (K <= 32 && M <= kRegMaxRoots && vec_ok(V, ldv, W, diag, T) && ldt % 2 == 0 && use_reg()) {
