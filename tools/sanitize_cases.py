@@ -27,7 +27,7 @@ SIGMA_ENVS = [{}, {"SBD_SIDE_LDG": "1"}, {"SBD_YT_BLOCKED": "0"}, {"SBD_CROSS_NO
               {"SBD_CROSS_UNSTAGED": "1"}, {"SBD_CROSS_ADD": "1"}, {"SBD_CROSS_DCI": "1"},
               {"SBD_CROSS_DCI": "1", "SBD_CROSS_ADD": "1"}, {"SBD_DENSE_GEMM": "1"},
               {"SBD_DENSE_GEMM": "1", "SBD_CROSS_DCI": "1"}]
-DAV_ENVS = [{}, {"SBD_DAV_TMA": "1"}, {"SBD_NO_TMA": "1"}]
+DAV_ENVS = [{}, {"SBD_RES_STREAM": "0"}, {"SBD_DAV_TMA": "1"}, {"SBD_NO_TMA": "1"}]
 
 
 def _with_env(env, fn):
@@ -120,6 +120,51 @@ def davidson_cases():
         print("davidson ok", k_max, flush=True)
 
 
+def residual_case():
+    """The streamed residual pass with several tiles per CTA (its stage ring wraps), odd n, k in each tile size."""
+    import torch
+
+    from paper_2601_16637_b200 import _lib
+
+    n = 148 * 256 * 3 + 77
+    ctx = _lib.Context(0)
+    ctx.bind_stream()
+    rng = np.random.default_rng(3)
+    for k, m in ((5, 1), (16, 2), (28, 3)):
+        V = torch.from_numpy(rng.standard_normal((k, n))).cuda()
+        W = torch.from_numpy(rng.standard_normal((k, n))).cuda()
+        Y = torch.from_numpy(rng.standard_normal((k, m))).cuda()
+        th = torch.from_numpy(rng.standard_normal(m)).cuda()
+        d = torch.from_numpy(rng.standard_normal(n)).cuda()
+        T = torch.empty((m, n), dtype=torch.float64, device="cuda")
+        out = torch.empty(k + 1 + m, dtype=torch.float64, device="cuda")
+        p = _lib.ptr
+        ctx("sbd_residual_precond_target", p(V), p(W), k, n, n, p(Y), p(th), m, m - 1, p(d), 1e-3, p(T), n, p(out))
+        Vn, Wn, Yn, thn, dn = (t.cpu().numpy() for t in (V, W, Y, th, d))
+        R = Yn.T @ Wn - thn[:, None] * (Yn.T @ Vn)
+        dd = dn[None, :] - thn[:, None]
+        Tn = R / (np.where(dd >= 0, 1.0, -1.0) * np.maximum(np.abs(dd), 1e-3))
+        assert np.abs(T.cpu().numpy() - Tn).max() <= 1e-10 * np.abs(Tn).max()
+        assert np.abs(out.cpu().numpy()[:k] - Vn @ Tn[m - 1]).max() <= 1e-9 * np.abs(Vn @ Tn[m - 1]).max()
+    print("residual ok", flush=True)
+
+
+def tables128_case():
+    from paper_2601_16637_b200 import build_excitation_table128, sorted_strings128
+
+    rng = np.random.default_rng(4)
+    window = list(range(56, 72)) + list(range(120, 128))
+    strings = sorted({sum(1 << int(o) for o in rng.choice(window, 4, replace=False)) for _ in range(3000)})
+    rng.shuffle(strings)
+    tab = build_excitation_table128(strings, 128)
+    ref = O.build_table128(strings, 128)
+    for f in O.TABLE_FIELDS:
+        assert np.array_equal(getattr(tab, f), ref[f]), f
+    w, perm = sorted_strings128(strings, 128)
+    assert [int(lo) | int(hi) << 64 for lo, hi in w.tolist()] == sorted(strings)
+    print("tables128 ok", flush=True)
+
+
 def dense_case():
     from paper_2601_16637_b200 import SelectedBasis
     from paper_2601_16637_b200.dense import assemble_dense
@@ -134,7 +179,7 @@ def dense_case():
 
 
 CASES = {"sigma": sigma_cases, "explicit": explicit_case, "ingest": ingest_case, "davidson": davidson_cases,
-         "dense": dense_case}
+         "dense": dense_case, "residual": residual_case, "tables128": tables128_case}
 
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
