@@ -1333,6 +1333,7 @@ residual_reg(const double *__restrict__ V, const double *__restrict__ W, int k, 
 __host__ __device__ constexpr int res_stream_tile(int K) { return K <= 24 ? 256 : 192; }
 constexpr int kResMaxStages = 8;
 constexpr int kResStreamMaxK = 32;
+constexpr int kResStreamTile = 256;  // vdots2_stream's tile
 constexpr size_t kResStageBudget = 210 * 1024;
 
 inline int res_stream_stages(int K, int k) {
@@ -1476,6 +1477,103 @@ residual_stream(const double *__restrict__ V, const double *__restrict__ W, int 
         for (int w = 0; w < NW; ++w) sum += red[w][i];
         partial[(i64)blockIdx.x * (K + 1 + M) + i] = (i < K && i >= k) ? 0.0 : sum;
     }
+}
+
+// V^T w and V^T u (the T column and the Gram row) streamed like residual_stream: a producer
+// warp bulk-copies each 256-element tile's k + 2 slices (k V, w, u) into stages sized to
+// ~210 KB; 8 consumer warps, one element per thread, 2k accumulators per thread.
+// partial per block (stride 2K): [0,K) V^T w | [K,2K) V^T u
+template <int K>
+__global__ void __launch_bounds__(kResStreamTile + 32, 1)
+vdots2_stream(const double *__restrict__ V, int k, i64 ldv, i64 n, const double *__restrict__ w,
+              const double *__restrict__ u, double *__restrict__ partial, int ns) {
+    constexpr int TT = kResStreamTile, NW = TT / 32;
+    extern __shared__ __align__(128) unsigned char vss[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(vss), *empty = full + kResMaxStages;
+    double *stage0 = reinterpret_cast<double *>(vss + 256);
+    __shared__ double red[NW][2 * K];
+    const i64 sstride = (i64)(k + 2) * TT;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    if (t == 0) {
+        for (int s = 0; s < ns; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const i64 ntiles = (n + TT - 1) / TT;
+    if (warp == NW) {  // producer warp
+        int it = 0;
+        for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int s = it % ns;
+            if (it >= ns) mbar_wait(&empty[s], (uint32_t)(((it / ns) - 1) & 1));
+            const i64 base = tile * TT, cnt = min((i64)TT, n - base);
+            const uint32_t b = bulk_bytes(cnt);
+            double *st = stage0 + s * sstride;
+            if (lane == 0) mbar_arrive_expect_tx(&full[s], b * (uint32_t)(k + 2));
+            __syncwarp();
+            if (b) {
+                for (int c = lane; c < k + 2; c += 32) {  // slice c: V_c, w, u
+                    const double *src = c < k ? V + c * ldv : (c == k ? w : u);
+                    tma_load_1d(st + (i64)c * TT, src + base, b, &full[s]);
+                }
+            }
+        }
+        return;
+    }
+    double aw[K], au[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) aw[i] = au[i] = 0.0;
+    int it = 0;
+    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int s = it % ns;
+        const i64 base = tile * TT, cnt = min((i64)TT, n - base);
+        double *st = stage0 + s * sstride;
+        mbar_wait(&full[s], (uint32_t)((it / ns) & 1));
+        if (cnt & 1) {  // odd last element: plain loads
+            if (t == 0) {
+                const i64 q = cnt - 1;
+                for (int i = 0; i < k; ++i) st[(i64)i * TT + q] = V[i * ldv + base + q];
+                st[(i64)k * TT + q] = w[base + q];
+                st[(i64)(k + 1) * TT + q] = u[base + q];
+                fence_proxy_async_smem();
+            }
+            consumers_sync<TT>();
+        }
+        if (t < cnt) {
+            const double we = st[(i64)k * TT + t], ue = st[(i64)(k + 1) * TT + t];
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+                if (i < k) {
+                    const double v = st[(i64)i * TT + t];
+                    aw[i] = fma(v, we, aw[i]);
+                    au[i] = fma(v, ue, au[i]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const double a = warp_sum(aw[i]), b = warp_sum(au[i]);
+        if (lane == 0) {
+            red[warp][i] = a;
+            red[warp][K + i] = b;
+        }
+    }
+    consumers_sync<TT>();
+    for (int i = t; i < 2 * K; i += TT) {
+        double sum = 0.0;
+        for (int ww = 0; ww < NW; ++ww) sum += red[ww][i];
+        partial[(i64)blockIdx.x * 2 * K + i] = (i % K) < k ? sum : 0.0;
+    }
+}
+
+inline int vdots2_stream_stages(int k) {
+    const size_t stage = sizeof(double) * (size_t)(k + 2) * kResStreamTile;
+    return (int)std::max<size_t>(2, std::min<size_t>(kResMaxStages, kResStageBudget / stage));
 }
 
 // t_new = t - V c ; out = scale * t_new (out may alias t) ; dots V_i . t_new (i < kdot) ; |t_new|^2
@@ -1691,6 +1789,20 @@ struct Vdots2L {
                    double *out) {
         int nb = red_blocks(ctx, n);
         if (int rc = ensure_red(ctx, nb, 2 * K)) return rc;
+        if (K <= 32 && vec_ok(V, ldv, w, u) && use_reg() && use_res_stream()) {
+            constexpr int KS = K <= 32 ? K : 32;
+            const int ns = vdots2_stream_stages(k);
+            const size_t smem = 256 + sizeof(double) * (size_t)ns * (size_t)(k + 2) * kResStreamTile;
+            const int nt = (int)std::max<i64>(1, std::min<i64>((n + kResStreamTile - 1) / kResStreamTile,
+                                                               ctx->num_sms));
+            (void)sbd_smem_attr((const void *)vdots2_stream<KS>, ctx->device, smem);  // launch errors surface below
+            vdots2_stream<KS><<<nt, kResStreamTile + 32, smem, ctx->stream>>>(V, k, ldv, n, w, u,
+                                                                                ctx->red.as<double>(), ns);
+            finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>(), nt, 2 * K, k, K, k, out);
+            finish_partials<<<kFinishBlocks, 128, 0, ctx->stream>>>(ctx->red.as<double>() + K, nt, 2 * K, k, K, k, out + k);
+            SBD_LAUNCHED(ctx, "vdots2");
+            return SBD_OK;
+        }
         if (vec_ok(V, ldv, w, u)) {
             const int nt = tile_blocks(ctx, n, 1024);
             vdots2_tile<K><<<nt, kBlock, 0, ctx->stream>>>(V, k, ldv, n, w, u, ctx->red.as<double>());
