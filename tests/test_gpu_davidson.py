@@ -252,3 +252,24 @@ def test_selective_reorth_energies_vs_oracle():
     np.testing.assert_allclose(sel.energies, ref.energies, atol=1e-8, rtol=0)
     assert max(sel.stats.ortho_history) <= 1e-10
     assert sel.stats.iterations <= full.stats.iterations + 2
+
+
+@pytest.mark.parametrize("roots", [1, 3])
+def test_streamed_passes_match_register_passes(roots, monkeypatch):
+    """The streamed residual and V^T w passes (default) and the register-staged ones (SBD_RES_STREAM=0) give
+    the same solve: equal iteration and restart counts, energies within 1e-10.  1.2e5 determinants, so every
+    CTA of the streamed passes walks several tiles and the subspace runs through k = 1..32."""
+    from paper_2601_16637_b200 import DavidsonOptions, HamiltonianApplier, SelectedBasis, davidson_solve
+    from paper_2601_16637_b200.synth import random_integrals, random_product_strings
+
+    a, b = random_product_strings(14, 6, 6, 400, 300, seed=41)
+    app = HamiltonianApplier(SelectedBasis.product(a.tolist(), b.tolist(), 14, 6, 6), random_integrals(14, seed=4))
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SBD_RES_STREAM", mode)
+        out[mode] = davidson_solve(app, app.diag, opts=DavidsonOptions(n_roots=roots, max_iters=400))
+    r, s = out["0"], out["1"]
+    assert r.converged and s.converged
+    assert r.stats.iterations == s.stats.iterations and r.stats.restarts == s.stats.restarts
+    np.testing.assert_allclose(s.energies, r.energies, atol=1e-10, rtol=0)
+    assert max(s.stats.ortho_history) <= 1e-10
