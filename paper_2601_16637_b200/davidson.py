@@ -24,6 +24,8 @@ any numpy callable (its input/output cross the host link each iteration).
 
 from __future__ import annotations
 
+import math
+
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional
@@ -431,12 +433,17 @@ def _solve(apply_h, diag_dev, x0, opts, n, n_loc, dev, return_device, allreduce,
             v0 = torch.from_numpy(np.asarray(x0, dtype=np.float64).reshape(-1).copy()).to(dev)
         if v0.numel() != n_loc:
             raise ValueError(f"x0 has {v0.numel()} entries, expected {n_loc}")
-        nrm2 = (v0 @ v0).reshape(1)
+        # the native driver's normalisation (sbd_solver.cu setup): sbd_vdots, then x0 * (1 / |x0|), so both
+        # control loops start from the same bits
+        v0 = v0.contiguous()
+        nrm2 = torch.zeros(1, **f64)
+        ld_native = max(32, (n_loc + 31) // 32 * 32)  # the native basis' leading dimension (same kernel choice)
+        eng("sbd_vdots", _lib.ptr(v0), 1, ld_native, n_loc, _lib.ptr(v0), _lib.ptr(nrm2))
         reduce(nrm2)
-        norm = float(torch.sqrt(nrm2).item())
-        if norm == 0.0:
+        norm = math.sqrt(max(float(nrm2.item()), 0.0))
+        if not norm > 0.0 or not math.isfinite(norm):
             raise ValueError("x0 must be nonzero")
-        V[0].copy_(v0 / norm)
+        V[0].copy_(v0 * (1.0 / norm))
 
     k = 1
     theta = np.zeros(m)

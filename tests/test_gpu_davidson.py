@@ -204,8 +204,8 @@ def test_native_driver_edge_cases():
     x0 = np.random.default_rng(5).random(app.n)
     r1 = davidson_solve(app, app.diag, x0=x0, native=True)
     r2 = davidson_solve(app, app.diag, x0=x0, native=False)
-    # x0 is normalised by a different reduction order (ulp-level start difference)
-    assert r1.converged and abs(r1.energies[0] - ref) <= 1e-8 and abs(r1.stats.iterations - r2.stats.iterations) <= 4
+    # both drivers normalise x0 the same way (sbd_vdots, then x0 * (1 / |x0|)), so they start from the same bits
+    assert r1.converged and abs(r1.energies[0] - ref) <= 1e-8 and r1.stats.iterations == r2.stats.iterations
     with pytest.raises(ValueError):
         davidson_solve(app, app.diag, x0=np.zeros(app.n), native=True)
     with pytest.raises(ValueError):
