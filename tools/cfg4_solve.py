@@ -43,11 +43,32 @@ def main():
     setup_s = time.perf_counter() - t0
     diag = app.diag_device
     opts = DavidsonOptions(n_roots=3, max_subspace=args.k_max, restart_keep=args.keep, max_iters=args.max_iters)
+    # device memory in use, sampled by NVML during the solve: the native solver's basis lives in
+    # libsbd_b200 allocations that torch.cuda.max_memory_allocated does not see
+    import threading
+
+    import pynvml
+
+    pynvml.nvmlInit()
+    handle = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    peak = {"used": 0}
+    done = threading.Event()
+
+    def sample():
+        while not done.is_set():
+            peak["used"] = max(peak["used"], pynvml.nvmlDeviceGetMemoryInfo(handle).used)
+            done.wait(0.05)
+
+    sampler = threading.Thread(target=sample, daemon=True)
+    sampler.start()
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     res = davidson_solve(app, diag, opts=opts, return_device=True)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t1
+    done.set()
+    sampler.join()
+    total_gb = pynvml.nvmlDeviceGetMemoryInfo(handle).total / 1e9
     its = res.stats.iter_seconds
     rec = {
         "config": "cfg4: 36 orbitals, 27a27b, 3e4 x 3e4 random strings (seed 2), integrals seed 1",
@@ -59,7 +80,8 @@ def main():
         "converged": bool(res.converged), "iterations": res.stats.iterations, "restarts": res.stats.restarts,
         "wall_s": wall, "s_per_iter": float(np.mean(its[1:])) if len(its) > 1 else float(its[0]),
         "sigma_s_per_iter": float(np.mean(res.stats.apply_seconds[1:] or res.stats.apply_seconds)),
-        "setup_s": setup_s, "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9,
+        "setup_s": setup_s, "torch_peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9,
+        "device_mem_used_peak_gb": peak["used"] / 1e9, "device_mem_total_gb": total_gb,
     }
     e_b200 = np.array(rec["energies"])
     del res
