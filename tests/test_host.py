@@ -179,3 +179,21 @@ def test_bench_gpus_flag_starts_that_many_ranks():
     assert len(lines) == 1  # only rank 0 prints
     rec = json.loads(lines[0])
     assert rec["n_gpus"] == 2 and rec["rank_sum"] == 1
+
+
+def test_string_words_host_conversion():
+    """Host side of the 128-bit path: Python ints <-> (lo, hi) uint64 word pairs, the layout sbd_table128_build takes."""
+    from paper_2601_16637_b200 import string_words
+
+    vals = [0, 1, (1 << 63), (1 << 64), (1 << 127) | 5, (1 << 128) - 1]
+    w = string_words(vals)
+    assert w.dtype == np.uint64 and w.shape == (len(vals), 2)
+    assert [int(lo) | (int(hi) << 64) for lo, hi in w.tolist()] == vals
+    assert string_words(w) is not None and np.array_equal(string_words(w), w)  # (n, 2) arrays pass through
+    assert string_words([]).shape == (0, 2)
+    with pytest.raises(ValueError):
+        string_words([1 << 128])
+    with pytest.raises(ValueError):
+        string_words([-1])
+    with pytest.raises(ValueError):
+        string_words(np.zeros((3, 3), dtype=np.uint64))
